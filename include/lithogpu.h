@@ -1,0 +1,191 @@
+/* lithogpu — C ABI of the B200-native SOCS imaging / ILT hot path.
+ *
+ * Drop-in boundary for the reference `litho` toolkit (arxiv 2602.15036,
+ * /root/reference/proj).  Each entry point replaces one reference function
+ * on the north-star path; the replaced interface is cited beside it.  The
+ * reference's own C ABI conventions are kept (proj/include/litho/litho.h:1-20):
+ * every call returns a status, failures leave a thread-local message in
+ * lithogpu_last_error(), objects returned through out-parameters are owned by
+ * the caller and released with the matching _destroy, and no C++ exception
+ * ever crosses this boundary (CUDA failures map to LITHOGPU_ERR_DOMAIN).
+ *
+ * Buffers are plain pointers.  Each pointer may be HOST memory (pageable or
+ * pinned: staged through the context's device scratch, the call returns after
+ * the results are back on the host) or DEVICE memory of the context's GPU
+ * (stream-ordered on the context stream, no host synchronisation; call
+ * lithogpu_ctx_synchronize before reading).  Images are row-major, x fastest,
+ * index iy*nx + ix (reference raster.hpp:18).
+ *
+ * Thread safety: a context (and the objects created from it) is used by one
+ * host thread at a time; different contexts are independent (one per GPU /
+ * per host thread).  Kernel stacks are read-only after creation.
+ */
+#ifndef LITHOGPU_H
+#define LITHOGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LITHOGPU_OK = 0,
+  LITHOGPU_ERR_DOMAIN = 1, /* invalid input data or failed computation (incl. CUDA errors) */
+  LITHOGPU_ERR_USAGE = 2   /* bad arguments (null pointers, unknown enums) */
+} lithogpu_status;
+
+typedef enum { LITHOGPU_F32 = 0, LITHOGPU_F64 = 1, LITHOGPU_U8 = 2 } lithogpu_dtype;
+
+/* Thread-local message for the last failing call; "" if none.
+ * Replaces litho_last_error (litho.h:19-20, litho_c.cpp:22-42). */
+const char* lithogpu_last_error(void);
+
+/* Uniform pixel grid; pixel (ix,iy) covers [origin + i*pitch, origin+(i+1)*pitch)
+ * (reference Grid, raster.hpp:10-20). */
+typedef struct {
+  int nx, ny;
+  double pitch_nm;
+  double origin_x_nm, origin_y_nm;
+} lithogpu_grid;
+
+/* ---- context ---------------------------------------------------------- */
+typedef struct lithogpu_ctx lithogpu_ctx;
+lithogpu_status lithogpu_ctx_create(int device, lithogpu_ctx** out);
+void lithogpu_ctx_destroy(lithogpu_ctx* ctx);
+/* cudaStream_t to launch on (NULL = the legacy default stream) */
+lithogpu_status lithogpu_ctx_set_stream(lithogpu_ctx* ctx, void* stream);
+lithogpu_status lithogpu_ctx_synchronize(lithogpu_ctx* ctx);
+/* number of kernels this context launched so far (instrumentation) */
+long long lithogpu_ctx_launch_count(const lithogpu_ctx* ctx);
+
+/* ---- rasterization ------------------------------------------------------
+ * Exact area-weighted coverage in fp64, bit-exact with the reference
+ * rasterize_layer (raster.cpp:53-95) on a HEALED layer: polygons must be the
+ * output of the reference heal() (boolean.hpp:40-42) — disjoint, CCW outers /
+ * CW holes, canonical order.  Vertices are int64 dbu (geometry.hpp:15);
+ * polygon p is xy[2*poly_start[p] .. 2*poly_start[p+1]).  out: nx*ny f64. */
+lithogpu_status lithogpu_rasterize(lithogpu_ctx* ctx, const lithogpu_grid* grid,
+                                   const int64_t* xy, const int64_t* poly_start, int n_poly,
+                                   double dbu_per_nm, double* out);
+
+/* ---- SOCS kernel stacks -------------------------------------------------
+ * Replaces SocsKernelSet (imaging.hpp:78-87) and build_optics' per-focus
+ * stacks (opc.cpp:114-124).  n_focus stacks of `order` kernels share one
+ * frequency support of n_support signed DFT indices (kx, ky) (the TCC support,
+ * imaging.cpp:120-129); values[f][k][s] = kernels_freq[k] at that index
+ * (interleaved re, im).  weights[f][k] >= 0.  precision LITHOGPU_F32 (fast
+ * path) or LITHOGPU_F64 (reference-tolerance path). */
+typedef struct lithogpu_kernels lithogpu_kernels;
+lithogpu_status lithogpu_kernels_create(lithogpu_ctx* ctx, const lithogpu_grid* grid,
+                                        lithogpu_dtype precision, int n_focus, int order,
+                                        const double* weights, int n_support,
+                                        const int32_t* support, const double* values,
+                                        lithogpu_kernels** out);
+void lithogpu_kernels_destroy(lithogpu_kernels* ks);
+/* geometry chosen for the tile: decimated grid and kernel band */
+lithogpu_status lithogpu_kernels_info(const lithogpu_kernels* ks, int* nx_sub, int* ny_sub,
+                                      int* band_x, int* band_y);
+
+/* ---- imaging ------------------------------------------------------------
+ * image_socs (imaging.cpp:218-241): I = dose * sum_k w_k |IFFT(FFT(mask)/N^2 H_k)|^2
+ * for focus stack `focus`.  mask: nx*ny real (f32/f64); intensity: nx*ny. */
+lithogpu_status lithogpu_image_socs(lithogpu_kernels* ks, int focus, const void* mask,
+                                    lithogpu_dtype mask_dtype, double dose, void* intensity,
+                                    lithogpu_dtype out_dtype);
+
+/* Fused forward: aerial image + resist_filter (imaging.cpp:316-323, Gaussian
+ * blur sigma_nm) + threshold map (ResistImage threshold, v >= threshold -> 1).
+ * Any of intensity / resist / print may be NULL. */
+lithogpu_status lithogpu_image_resist(lithogpu_kernels* ks, int focus, const void* mask,
+                                      lithogpu_dtype mask_dtype, double dose, double sigma_nm,
+                                      double threshold, void* intensity, void* resist,
+                                      lithogpu_dtype out_dtype, unsigned char* print);
+
+/* gaussian_blur (imaging.cpp:287-314): cyclic unit-sum truncated Gaussian,
+ * radius min(N/2, ceil(6 sigma_px)+1); sigma 0 = identity. */
+lithogpu_status lithogpu_gaussian_blur(lithogpu_ctx* ctx, const lithogpu_grid* grid,
+                                       const void* in, lithogpu_dtype dtype, double sigma_nm,
+                                       void* out);
+
+/* z_print / threshold semantics (ai.cpp:85-94): out[i] = in[i] >= tau ? 1 : 0 */
+lithogpu_status lithogpu_threshold(lithogpu_ctx* ctx, size_t n, const void* in,
+                                   lithogpu_dtype in_dtype, double tau, void* out,
+                                   lithogpu_dtype out_dtype);
+
+/* ---- adjoint --------------------------------------------------------------
+ * intensity_gradient (ai.cpp:11-42) generalised with a per-pixel weight W:
+ *   grad(x) = sum_r W(r) dI(r)/dM(x)
+ *           = sum_k 2 dose w_k Re IFFT(FFT(W E_k) conj(H_k)/N^2)(x).
+ * weight == NULL is the reference's uniform case (d sum_r I / dM). */
+lithogpu_status lithogpu_intensity_gradient(lithogpu_kernels* ks, int focus, const void* mask,
+                                            lithogpu_dtype mask_dtype, const void* weight,
+                                            lithogpu_dtype weight_dtype, double dose, void* grad,
+                                            lithogpu_dtype grad_dtype);
+
+/* ---- pixel ILT (through-focus) --------------------------------------------
+ * Not in the reference.  Per tile:
+ *   M = sigmoid(mask_steepness * theta);  for each focus stack f:
+ *   R_f = blur(image_socs(M, H_f, dose), resist_sigma_nm),
+ *   Z_f = sigmoid(resist_beta * (R_f - threshold)),
+ *   cost = sum_f focus_weights[f] * sum_r (Z_f - target)^2,
+ *   theta <- theta - step * dcost/dtheta   (exact adjoint, all foci).   */
+typedef struct {
+  double mask_steepness;
+  double resist_beta;
+  double threshold;
+  double resist_sigma_nm;
+  double dose;
+  double step;
+  const double* focus_weights; /* n_focus entries (host) */
+} lithogpu_ilt_params;
+
+typedef struct lithogpu_ilt lithogpu_ilt;
+lithogpu_status lithogpu_ilt_create(lithogpu_kernels* ks, const lithogpu_ilt_params* params,
+                                    int n_tiles, lithogpu_ilt** out);
+void lithogpu_ilt_destroy(lithogpu_ilt* ilt);
+/* target: nx*ny in [0,1]; theta0 NULL -> theta0 = (2*target-1)*2/steepness */
+lithogpu_status lithogpu_ilt_set_tile(lithogpu_ilt* ilt, int tile, const void* target,
+                                      const void* theta0, lithogpu_dtype dtype);
+/* all tiles target/theta at once: n_tiles*nx*ny each (theta0 may be NULL) */
+lithogpu_status lithogpu_ilt_set_tiles(lithogpu_ilt* ilt, const void* target,
+                                       const void* theta0, lithogpu_dtype dtype);
+/* Run `iterations` steps on all tiles.  cost (nullable): iterations*n_tiles
+ * f64, cost[i*n_tiles+t] = cost of tile t BEFORE update i; gmax (nullable):
+ * max |dcost/dtheta| per iteration and tile, same layout. */
+lithogpu_status lithogpu_ilt_run(lithogpu_ilt* ilt, int iterations, double* cost,
+                                 double* gmax);
+/* theta and/or mask = sigmoid(steepness*theta) of one tile (nullable outs) */
+lithogpu_status lithogpu_ilt_get_tile(lithogpu_ilt* ilt, int tile, void* theta, void* mask,
+                                      lithogpu_dtype dtype);
+/* all tiles: n_tiles*nx*ny (nullable outs) */
+lithogpu_status lithogpu_ilt_get_tiles(lithogpu_ilt* ilt, void* theta, void* mask,
+                                       lithogpu_dtype dtype);
+
+/* ---- host-side kernel generation (precompute, not on the timed path) ----
+ * Replaces build_tcc + decompose_tcc (imaging.cpp:113-216) with the same
+ * semantics via the TCC = Q Q^H factorisation (no dense S x S eigensolve, so
+ * no 6000-frequency budget).  Error text: lithogpu_host_last_error(). */
+const char* lithogpu_host_last_error(void);
+/* make_annular_source (imaging.cpp:50-64); sigma_out <= 0 -> point source.
+ * out_xyw (3*count doubles: sx, sy, weight) may be NULL to query count. */
+lithogpu_status lithogpu_source_annular(double sigma_in, double sigma_out, int grid_n, int* count,
+                                        double* out_xyw);
+/* TCC support (imaging.cpp:115-129), reference order; out may be NULL */
+lithogpu_status lithogpu_tcc_support(int nx, int ny, double pitch_nm, double wavelength_nm,
+                                     double na, double max_source_radius, int* count,
+                                     int32_t* out_kxky);
+/* One focus plane's SOCS kernels on `support`: out_weights[K] descending,
+ * out_values[K][n_support] interleaved complex, K <= max_order. */
+lithogpu_status lithogpu_socs_kernels(int nx, int ny, double pitch_nm, double wavelength_nm,
+                                      double na, int high_na, const double* source_xyw,
+                                      int n_source, double focus_nm, int n_support,
+                                      const int32_t* support, int k_fixed, double energy_floor,
+                                      int max_order, int* out_order, double* out_captured,
+                                      double* out_weights, double* out_values);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,1251 @@
+// lithogpu C ABI implementation: contexts, band-sparse kernel stacks, tile
+// plans, launch orchestration (include/lithogpu.h documents the contract and
+// the reference interface each entry point replaces).
+#include <cuda_runtime.h>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/lithogpu.h"
+#include "raster_kernels.cuh"
+#include "socs_kernels.cuh"
+#include "util_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct UsageError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define LG_CUDA(call)                                                                      \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      throw std::runtime_error(std::string("CUDA error: ") + cudaGetErrorString(e_) + " (" + \
+                               #call + ")");                                               \
+  } while (0)
+
+template <typename Fn>
+lithogpu_status guarded(Fn&& fn) {
+  try {
+    fn();
+    g_last_error.clear();
+    return LITHOGPU_OK;
+  } catch (const UsageError& e) {
+    g_last_error = e.what();
+    return LITHOGPU_ERR_USAGE;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return LITHOGPU_ERR_DOMAIN;
+  } catch (...) {
+    g_last_error = "unknown error";
+    return LITHOGPU_ERR_DOMAIN;
+  }
+}
+
+void require(bool ok, const char* msg) {
+  if (!ok) throw UsageError(msg);
+}
+
+size_t dtype_size(lithogpu_dtype d) {
+  switch (d) {
+    case LITHOGPU_F32:
+      return 4;
+    case LITHOGPU_F64:
+      return 8;
+    case LITHOGPU_U8:
+      return 1;
+  }
+  throw UsageError("unknown dtype");
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  void ensure(size_t b) {
+    if (b <= bytes) return;
+    release();
+    if (b == 0) return;
+    LG_CUDA(cudaMalloc(&p, b));
+    bytes = b;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+struct lithogpu_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  long long launches = 0;
+  std::vector<std::unique_ptr<DevBuf>> scratch;  // staging pool (per call slots)
+  DevBuf raster_tmp;
+  std::unordered_map<const void*, int> smem_set;
+
+  DevBuf& slot(size_t i) {
+    while (scratch.size() <= i) scratch.emplace_back(new DevBuf);
+    return *scratch[i];
+  }
+  void activate() const { LG_CUDA(cudaSetDevice(device)); }
+  void check_launch() {
+    ++launches;
+    LG_CUDA(cudaGetLastError());
+  }
+  template <typename K>
+  void smem_attr(K kern, size_t bytes) {
+    const void* key = reinterpret_cast<const void*>(kern);
+    auto it = smem_set.find(key);
+    if (it != smem_set.end() && size_t(it->second) >= bytes) return;
+    if (bytes > 48 * 1024)
+      LG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+    smem_set[key] = int(bytes);
+  }
+};
+
+namespace {
+
+// ---- host <-> device staging with dtype conversion ------------------------
+template <typename A, typename B>
+void convert_dev(lithogpu_ctx* ctx, const A* in, B* out, size_t n) {
+  if (n == 0) return;
+  const int blocks = int(std::min<size_t>((n + 255) / 256, 148 * 16));
+  lg::k_convert<A, B><<<blocks, 256, 0, ctx->stream>>>(in, out, n);
+  ctx->check_launch();
+}
+
+template <typename B>
+void convert_from(lithogpu_ctx* ctx, const void* in, lithogpu_dtype dt, B* out, size_t n) {
+  switch (dt) {
+    case LITHOGPU_F32:
+      convert_dev(ctx, static_cast<const float*>(in), out, n);
+      break;
+    case LITHOGPU_F64:
+      convert_dev(ctx, static_cast<const double*>(in), out, n);
+      break;
+    case LITHOGPU_U8:
+      convert_dev(ctx, static_cast<const unsigned char*>(in), out, n);
+      break;
+  }
+}
+
+template <typename A>
+void convert_to(lithogpu_ctx* ctx, const A* in, void* out, lithogpu_dtype dt, size_t n) {
+  switch (dt) {
+    case LITHOGPU_F32:
+      convert_dev(ctx, in, static_cast<float*>(out), n);
+      break;
+    case LITHOGPU_F64:
+      convert_dev(ctx, in, static_cast<double*>(out), n);
+      break;
+    case LITHOGPU_U8:
+      convert_dev(ctx, in, static_cast<unsigned char*>(out), n);
+      break;
+  }
+}
+
+// Input of n elements of dtype dt at user pointer p -> device T array.
+// Uses scratch slots [s, s+1].
+template <typename T>
+const T* stage_in(lithogpu_ctx* ctx, const void* p, lithogpu_dtype dt, size_t n, int s) {
+  const bool dev = is_device_ptr(p);
+  const size_t bytes = n * dtype_size(dt);
+  const void* dsrc = p;
+  if (!dev) {
+    DevBuf& raw = ctx->slot(s);
+    raw.ensure(bytes);
+    LG_CUDA(cudaMemcpyAsync(raw.p, p, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    dsrc = raw.p;
+  }
+  const bool same = (sizeof(T) == 4 && dt == LITHOGPU_F32) || (sizeof(T) == 8 && dt == LITHOGPU_F64);
+  if (same) return static_cast<const T*>(dsrc);
+  DevBuf& cv = ctx->slot(s + 1);
+  cv.ensure(n * sizeof(T));
+  convert_from(ctx, dsrc, dt, cv.as<T>(), n);
+  return cv.as<T>();
+}
+
+// Output: returns a device T buffer to compute into; finish_out() moves it to p.
+template <typename T>
+struct OutStage {
+  lithogpu_ctx* ctx;
+  void* user;
+  lithogpu_dtype dt;
+  size_t n;
+  bool dev;
+  T* work = nullptr;
+  int slot;
+  OutStage(lithogpu_ctx* c, void* p, lithogpu_dtype d, size_t n_, int s)
+      : ctx(c), user(p), dt(d), n(n_), slot(s) {
+    if (!p) return;
+    dev = is_device_ptr(p);
+    const bool same = (sizeof(T) == 4 && dt == LITHOGPU_F32) || (sizeof(T) == 8 && dt == LITHOGPU_F64);
+    if (dev && same) {
+      work = static_cast<T*>(p);
+    } else {
+      DevBuf& b = ctx->slot(slot);
+      b.ensure(n * sizeof(T));
+      work = b.as<T>();
+    }
+  }
+  // returns true if a host copy was queued (caller must sync)
+  bool finish() {
+    if (!user) return false;
+    const bool same = (sizeof(T) == 4 && dt == LITHOGPU_F32) || (sizeof(T) == 8 && dt == LITHOGPU_F64);
+    if (dev) {
+      if (!same) convert_to(ctx, work, user, dt, n);
+      return false;
+    }
+    const void* src = work;
+    if (!same) {
+      DevBuf& b = ctx->slot(slot + 1);
+      b.ensure(n * dtype_size(dt));
+      convert_to(ctx, work, b.p, dt, n);
+      src = b.p;
+    }
+    LG_CUDA(cudaMemcpyAsync(user, src, n * dtype_size(dt), cudaMemcpyDeviceToHost, ctx->stream));
+    return true;
+  }
+};
+
+// ---- geometry --------------------------------------------------------------
+lg::AxisGeom make_axis(int N, int lo, int hi) {
+  lg::AxisGeom a{};
+  a.N = N;
+  a.lo = lo;
+  a.hi = hi;
+  a.B = hi - lo + 1;
+  a.Pm = std::max(-lo, hi);
+  const int P0 = a.B - 1;
+  int best = 0;
+  for (int d = N; d >= 1; --d) {
+    if (N % d) continue;
+    const int n = N / d;
+    if (n >= 2 * P0 + 1) {
+      best = d;
+      break;
+    }
+  }
+  if (best) {
+    a.d = best;
+    a.n = N / best;
+    a.full = 0;
+    a.P = P0;
+    a.nb2 = 2 * P0 + 1;
+  } else {
+    a.d = 1;
+    a.n = N;
+    a.full = 1;
+    a.P = N / 2;
+    a.nb2 = N;
+  }
+  return a;
+}
+
+// exp(-2 pi i m / L), m < L, fp64 then rounded
+template <typename T>
+void make_twiddles(int L, DevBuf& buf) {
+  std::vector<lg::cx<T>> h(L);
+  for (int m = 0; m < L; ++m) {
+    // reduce the angle exactly: m/L in [0,1)
+    const double a = 2.0 * M_PI * double(m) / double(L);
+    h[m].x = T(std::cos(a));
+    h[m].y = T(-std::sin(a));
+  }
+  buf.ensure(sizeof(lg::cx<T>) * L);
+  LG_CUDA(cudaMemcpy(buf.p, h.data(), sizeof(lg::cx<T>) * L, cudaMemcpyHostToDevice));
+}
+
+// 1-D DFT of the reference's truncated unit-sum Gaussian on an N-grid
+// (imaging.cpp:292-305: radius min(N/2, ceil(6 sigma_px)+1), unit sum; the
+// 2-D kernel is the product of the two axes' 1-D kernels).
+std::vector<double> gauss_taps(int N, double sigma_px, int& r) {
+  r = std::min(N / 2, int(std::ceil(6 * sigma_px)) + 1);
+  std::vector<double> g(2 * r + 1);
+  double s = 0;
+  for (int d = -r; d <= r; ++d) {
+    g[d + r] = std::exp(-0.5 * double(d) * double(d) / (sigma_px * sigma_px));
+    s += g[d + r];
+  }
+  for (auto& v : g) v /= s;
+  return g;
+}
+
+double gauss_hat(int N, const std::vector<double>& taps, int r, int p) {
+  double acc = 0;
+  for (int d = -r; d <= r; ++d) acc += taps[d + r] * std::cos(2.0 * M_PI * double(p) * d / N);
+  return acc;
+}
+
+struct Launch {
+  int G, RPC, block;
+  size_t smem;
+};
+
+template <typename T>
+Launch launch_cfg(int LA, int LB, int target = 256) {
+  Launch l;
+  l.G = lg::group_threads<T>(LA, LB);
+  l.RPC = std::max(1, target / l.G);
+  l.block = l.RPC * l.G;
+  l.smem = size_t(l.RPC) * lg::group_elems<T>(LA, LB) * sizeof(T);
+  return l;
+}
+
+int cdiv(long long a, long long b) { return int((a + b - 1) / b); }
+
+struct PlanBase {
+  virtual ~PlanBase() = default;
+};
+
+}  // namespace
+
+// ============================================================================
+// Plan: one tile geometry + F x K kernel stacks, templated on the real type
+// ============================================================================
+template <typename T>
+struct Plan : PlanBase {
+  using C = lg::cx<T>;
+  lithogpu_ctx* ctx;
+  lg::Geo<T> g{};
+  lithogpu_grid grid{};
+  int F = 0, K = 0;
+  DevBuf twNx, twNy, twnx, twny, H, wk;
+  // Gaussian transfer cache
+  double gsig = -1.0;
+  DevBuf gxh, gyb;
+  // work buffers (sized for `cap` tiles)
+  int cap = 0;
+  DevBuf Mr, Mhat, Tb, Ir, Ic, Rc, Dr, Wc, U, Acc, Gc, costrow, gmaxrow;
+  long long s_Mr, s_Mhat, s_T, s_Ir, s_C, s_Dr, s_Wc, s_U, s_Acc, s_Gc, s_cr, s_gm;
+
+  Plan(lithogpu_ctx* c, const lithogpu_grid& gr, int F_, int K_, const double* weights, int S,
+       const int32_t* support, const double* values)
+      : ctx(c), grid(gr), F(F_), K(K_) {
+    const int Nx = gr.nx, Ny = gr.ny;
+    // canonical signed support indices and band extent
+    std::vector<int> kx(S), ky(S);
+    int lox = 1 << 30, hix = -(1 << 30), loy = lox, hiy = hix;
+    for (int s = 0; s < S; ++s) {
+      int a = ((support[2 * s] % Nx) + Nx) % Nx, b = ((support[2 * s + 1] % Ny) + Ny) % Ny;
+      if (a > Nx / 2) a -= Nx;
+      if (b > Ny / 2) b -= Ny;
+      kx[s] = a;
+      ky[s] = b;
+      lox = std::min(lox, a);
+      hix = std::max(hix, a);
+      loy = std::min(loy, b);
+      hiy = std::max(hiy, b);
+    }
+    g.ax = make_axis(Nx, lox, hix);
+    g.ay = make_axis(Ny, loy, hiy);
+    g.F = F;
+    g.K = K;
+    auto tab = [&](int L, DevBuf& b) {
+      make_twiddles<T>(L, b);
+      lg::Tab<T> t;
+      t.tw = b.as<C>();
+      t.L = L;
+      t.log2L = lg::fast_len<T>(L) ? lg::ilog2(L) : -1;
+      return t;
+    };
+    g.tNx = tab(Nx, twNx);
+    g.tNy = tab(Ny, twNy);
+    g.tnx = tab(g.ax.n, twnx);
+    g.tny = tab(g.ay.n, twny);
+    // dense band kernels [F*K][By][Bx]
+    const int Bx = g.ax.B, By = g.ay.B;
+    std::vector<C> h(size_t(F) * K * By * Bx);
+    for (auto& v : h) v.x = v.y = T(0);
+    for (int fk = 0; fk < F * K; ++fk)
+      for (int s = 0; s < S; ++s) {
+        C& dst = h[(size_t(fk) * By + (ky[s] - loy)) * Bx + (kx[s] - lox)];
+        dst.x = T(values[2 * (size_t(fk) * S + s)]);
+        dst.y = T(values[2 * (size_t(fk) * S + s) + 1]);
+      }
+    H.ensure(h.size() * sizeof(C));
+    LG_CUDA(cudaMemcpy(H.p, h.data(), h.size() * sizeof(C), cudaMemcpyHostToDevice));
+    std::vector<T> w(size_t(F) * K);
+    for (size_t i = 0; i < w.size(); ++i) w[i] = T(weights[i]);
+    wk.ensure(w.size() * sizeof(T));
+    LG_CUDA(cudaMemcpy(wk.p, w.data(), w.size() * sizeof(T), cudaMemcpyHostToDevice));
+    // strides (elements)
+    const auto& ax = g.ax;
+    const auto& ay = g.ay;
+    s_Mr = (long long)(ax.Pm + 1) * Ny;
+    s_Mhat = (long long)By * Bx;
+    s_T = (long long)F * K * ay.n * Bx;
+    s_Ir = (long long)F * (ax.P + 1) * ay.n;
+    s_C = (long long)F * Ny * (ax.P + 1);
+    s_Dr = (long long)F * (ax.P + 1) * Ny;
+    s_Wc = (long long)F * ay.n * (ax.P + 1);
+    s_U = (long long)F * K * Bx * ay.n;
+    s_Acc = (long long)By * Bx;
+    s_Gc = (long long)Ny * (ax.Pm + 1);
+    s_cr = (long long)F * Ny;
+    s_gm = (long long)(Ny + 1) / 2;
+  }
+
+  void set_sigma(double sigma_nm) {
+    if (sigma_nm == gsig) return;
+    const auto& ax = g.ax;
+    const auto& ay = g.ay;
+    std::vector<T> hx(ax.P + 1), hy(ay.nb2);
+    if (sigma_nm == 0) {
+      std::fill(hx.begin(), hx.end(), T(1));
+      std::fill(hy.begin(), hy.end(), T(1));
+    } else {
+      const double sp = sigma_nm / grid.pitch_nm;
+      int rx, ry;
+      const auto tx = gauss_taps(ax.N, sp, rx);
+      const auto ty = gauss_taps(ay.N, sp, ry);
+      for (int p = 0; p <= ax.P; ++p) hx[p] = T(gauss_hat(ax.N, tx, rx, p));
+      for (int j = 0; j < ay.nb2; ++j) hy[j] = T(gauss_hat(ay.N, ty, ry, lg::band2_p(ay, j)));
+    }
+    gxh.ensure(hx.size() * sizeof(T));
+    gyb.ensure(hy.size() * sizeof(T));
+    LG_CUDA(cudaMemcpy(gxh.p, hx.data(), hx.size() * sizeof(T), cudaMemcpyHostToDevice));
+    LG_CUDA(cudaMemcpy(gyb.p, hy.data(), hy.size() * sizeof(T), cudaMemcpyHostToDevice));
+    gsig = sigma_nm;
+  }
+
+  void reserve(int tiles, bool adjoint) {
+    if (tiles > cap) {
+      Mr.release(); Mhat.release(); Tb.release(); Ir.release(); Ic.release(); Rc.release();
+      Dr.release(); Wc.release(); U.release(); Acc.release(); Gc.release();
+      costrow.release(); gmaxrow.release();
+      cap = tiles;
+    }
+    const size_t c = sizeof(C) * size_t(cap);
+    Mr.ensure(c * s_Mr);
+    Mhat.ensure(c * s_Mhat);
+    Tb.ensure(c * s_T);
+    Ir.ensure(c * s_Ir);
+    Rc.ensure(c * s_C);
+    if (!adjoint) {
+      Ic.ensure(c * s_C);
+      return;
+    }
+    Dr.ensure(c * s_Dr);
+    Wc.ensure(c * s_Wc);
+    U.ensure(c * s_U);
+    Acc.ensure(c * s_Acc);
+    Gc.ensure(c * s_Gc);
+    costrow.ensure(sizeof(double) * cap * s_cr);
+    gmaxrow.ensure(sizeof(double) * cap * s_gm);
+  }
+
+  template <typename Kern, typename... Args>
+  void go(Kern kern, const Launch& l, dim3 grd, Args... args) {
+    ctx->smem_attr(kern, l.smem);
+    kern<<<grd, l.block, l.smem, ctx->stream>>>(args...);
+    ctx->check_launch();
+  }
+
+  // ---- pipeline stages ------------------------------------------------------
+  // real images (tile-major, T) -> half-spectrum rows into out [Pout+1][Ny]
+  template <int MODE>
+  void real_rows_fwd(const T* src, long long src_ts, T steep, int Pout, C* out, long long out_ts,
+                     int tiles) {
+    const Launch l = launch_cfg<T>(g.ax.N, 0);
+    go(lg::k_real_rows_fwd<T, MODE>, l, dim3(cdiv((g.ay.N + 1) / 2, l.RPC), 1, tiles), g, src,
+       src_ts, steep, Pout, out, out_ts);
+  }
+  void mask_cols(int tiles) {
+    const Launch l = launch_cfg<T>(g.ay.N, 0);
+    go(lg::k_mask_cols<T>, l, dim3(cdiv(g.ax.Pm + 1, l.RPC), 1, tiles), g, Mr.as<C>(), s_Mr,
+       Mhat.as<C>(), s_Mhat);
+  }
+  void socs_cols(int tiles) {
+    const Launch l = launch_cfg<T>(g.ay.n, 0);
+    go(lg::k_socs_cols<T>, l, dim3(cdiv(g.ax.B, l.RPC), F * K, tiles), g, Mhat.as<C>(), s_Mhat,
+       H.as<C>(), Tb.as<C>(), s_T);
+  }
+  void socs_rows(T dose, int tiles) {
+    const Launch l = launch_cfg<T>(g.ax.n, 0);
+    go(lg::k_socs_rows<T>, l, dim3(cdiv(g.ay.n, l.RPC), F, tiles), g, Tb.as<C>(), s_T,
+       wk.as<T>(), dose, Ir.as<C>(), s_Ir, static_cast<T*>(nullptr), 0LL);
+  }
+  void isub_cols(bool want_i, bool want_r, int tiles) {
+    const Launch l = launch_cfg<T>(g.ay.n, g.ay.N);
+    const dim3 grd(cdiv(g.ax.P + 1, l.RPC), F, tiles);
+    if (want_i && want_r)
+      go(lg::k_isub_cols<T, true, true>, l, grd, g, Ir.as<C>(), s_Ir, gxh.as<T>(), gyb.as<T>(),
+         Ic.as<C>(), Rc.as<C>(), s_C);
+    else if (want_i)
+      go(lg::k_isub_cols<T, true, false>, l, grd, g, Ir.as<C>(), s_Ir, gxh.as<T>(), gyb.as<T>(),
+         Ic.as<C>(), Rc.as<C>(), s_C);
+    else
+      go(lg::k_isub_cols<T, false, true>, l, grd, g, Ir.as<C>(), s_Ir, gxh.as<T>(), gyb.as<T>(),
+         Ic.as<C>(), Rc.as<C>(), s_C);
+  }
+  template <typename OutT>
+  void out_rows(bool want_i, bool want_r, OutT* I, OutT* R, unsigned char* pr, long long o_ts,
+                T thr, int tiles) {
+    const Launch l = launch_cfg<T>(g.ax.N, 0);
+    go(lg::k_out_rows<T, OutT>, l, dim3(cdiv(g.ay.N, l.RPC), F, tiles), g,
+       want_i ? static_cast<const C*>(Ic.as<C>()) : nullptr,
+       want_r ? static_cast<const C*>(Rc.as<C>()) : nullptr, s_C, I, R, pr, o_ts, thr);
+  }
+  void resist_rows(const T* target, long long tg_ts, const T* cf, T beta, T thr, int tiles,
+                   T* zout = nullptr, long long z_ts = 0) {
+    const Launch l = launch_cfg<T>(g.ax.N, 0);
+    go(lg::k_resist_rows<T>, l, dim3(cdiv(g.ay.N, l.RPC), (F + 1) / 2, tiles), g, Rc.as<C>(),
+       s_C, target, tg_ts, cf, beta, thr, Dr.as<C>(), s_Dr, costrow.as<double>(), s_cr, zout,
+       z_ts);
+  }
+  void wlp_cols(bool gauss, int nf, int tiles) {
+    const Launch l = launch_cfg<T>(g.ay.N, g.ay.n);
+    const dim3 grd(cdiv(g.ax.P + 1, l.RPC), nf, tiles);
+    if (gauss)
+      go(lg::k_wlp_cols<T, true>, l, grd, g, Dr.as<C>(), s_Dr, gxh.as<T>(), gyb.as<T>(),
+         Wc.as<C>(), s_Wc);
+    else
+      go(lg::k_wlp_cols<T, false>, l, grd, g, Dr.as<C>(), s_Dr, gxh.as<T>(), gyb.as<T>(),
+         Wc.as<C>(), s_Wc);
+  }
+  void adj_rows(bool uniform, int nf, int tiles) {
+    const Launch l = launch_cfg<T>(g.ax.n, 0);
+    const dim3 grd(cdiv(g.ay.n, l.RPC), nf, tiles);
+    if (uniform)
+      go(lg::k_adj_rows<T, true>, l, grd, g, Tb.as<C>(), s_T, Wc.as<C>(), s_Wc, U.as<C>(), s_U);
+    else
+      go(lg::k_adj_rows<T, false>, l, grd, g, Tb.as<C>(), s_T, Wc.as<C>(), s_Wc, U.as<C>(), s_U);
+  }
+  void adj_cols(T dose, int tiles) {
+    const Launch l = launch_cfg<T>(g.ay.n, 0);
+    go(lg::k_adj_cols<T>, l, dim3(g.ax.B, 1, tiles), g, U.as<C>(), s_U, H.as<C>(), wk.as<T>(),
+       dose, Acc.as<C>(), s_Acc);
+  }
+  void grad_cols(int tiles, bool with_cost, double* cost_out, long long co_ts) {
+    const Launch l = launch_cfg<T>(g.ay.N, 0);
+    go(lg::k_grad_cols<T>, l, dim3(cdiv(g.ax.Pm + 1, l.RPC) + 1, 1, tiles), g, Acc.as<C>(),
+       s_Acc, Gc.as<C>(), s_Gc, static_cast<const double*>(costrow.as<double>()), s_cr,
+       with_cost ? int(F * g.ay.N) : 0, with_cost ? cost_out : nullptr, co_ts);
+  }
+  template <bool ILT, typename OutT>
+  void grad_rows(OutT* grad, long long gr_ts, T* theta, long long th_ts, T steep, T step,
+                 double* gm, int tiles) {
+    const Launch l = launch_cfg<T>(g.ax.N, 0);
+    go(lg::k_grad_rows<T, ILT, OutT>, l, dim3(cdiv((g.ay.N + 1) / 2, l.RPC), 1, tiles), g,
+       Gc.as<C>(), s_Gc, grad, gr_ts, theta, th_ts, steep, step, Mr.as<C>(), s_Mr, gm, s_gm);
+  }
+
+  // ---- composite operations ---------------------------------------------------
+  // Forward images for focus stacks (all F computed; caller picks one).
+  void forward(const T* mask, long long m_ts, int tiles, T dose, bool want_i, bool want_r) {
+    reserve(tiles, false);
+    real_rows_fwd<0>(mask, m_ts, T(0), g.ax.Pm, Mr.as<C>(), s_Mr, tiles);
+    mask_cols(tiles);
+    socs_cols(tiles);
+    socs_rows(dose, tiles);
+    isub_cols(want_i, want_r, tiles);
+  }
+
+  void gradient(const T* mask, const T* W, T dose, T* grad) {
+    reserve(1, true);
+    real_rows_fwd<0>(mask, 0, T(0), g.ax.Pm, Mr.as<C>(), s_Mr, 1);
+    mask_cols(1);
+    socs_cols(1);
+    if (W) {
+      real_rows_fwd<0>(W, 0, T(0), g.ax.P, Dr.as<C>(), s_Dr, 1);
+      wlp_cols(false, 1, 1);
+    }
+    adj_rows(W == nullptr, 1, 1);
+    adj_cols(dose, 1);
+    grad_cols(1, false, nullptr, 0);
+    grad_rows<false, T>(grad, 0, nullptr, 0, T(0), T(0), nullptr, 1);
+  }
+};
+
+struct lithogpu_kernels {
+  lithogpu_ctx* ctx;
+  lithogpu_dtype precision;
+  lithogpu_grid grid;
+  int F, K;
+  std::unique_ptr<PlanBase> plan;
+  template <typename T>
+  Plan<T>& p() {
+    return *static_cast<Plan<T>*>(plan.get());
+  }
+};
+
+// ============================================================================
+// ILT state
+// ============================================================================
+struct lithogpu_ilt {
+  lithogpu_kernels* ks;
+  lithogpu_ilt_params prm;
+  std::vector<double> cf;
+  int tiles;
+  DevBuf theta, target, cfd, cost, gmax;
+  bool primed = false;
+};
+
+template <typename T>
+static void ilt_run_impl(lithogpu_ilt* ilt, int iters, double* cost_user, double* gmax_user) {
+  using C = lg::cx<T>;
+  Plan<T>& P = ilt->ks->p<T>();
+  lithogpu_ctx* ctx = ilt->ks->ctx;
+  const int tiles = ilt->tiles;
+  const auto& prm = ilt->prm;
+  const long long NN = (long long)P.g.ax.N * P.g.ay.N;
+  P.reserve(tiles, true);
+  P.set_sigma(prm.resist_sigma_nm);
+  ilt->cost.ensure(sizeof(double) * size_t(std::max(iters, 1)) * tiles);
+  ilt->gmax.ensure(sizeof(double) * size_t(std::max(iters, 1)) * tiles);
+  T* theta = ilt->theta.as<T>();
+  const T a = T(prm.mask_steepness), step = T(prm.step), beta = T(prm.resist_beta),
+          thr = T(prm.threshold), dose = T(prm.dose);
+  // initial mask row pass (subsequent ones are fused into grad_rows)
+  P.template real_rows_fwd<1>(theta, NN, a, P.g.ax.Pm, P.Mr.template as<C>(), P.s_Mr, tiles);
+  for (int it = 0; it < iters; ++it) {
+    P.mask_cols(tiles);
+    P.socs_cols(tiles);
+    P.socs_rows(dose, tiles);
+    P.isub_cols(false, true, tiles);
+    P.resist_rows(ilt->target.as<T>(), NN, ilt->cfd.as<T>(), beta, thr, tiles);
+    P.wlp_cols(true, P.F, tiles);
+    P.adj_rows(false, P.F, tiles);
+    P.adj_cols(dose, tiles);
+    // cost of iteration `it` for each tile -> cost[it*tiles + tile]
+    P.grad_cols(tiles, true, ilt->cost.as<double>() + size_t(it) * tiles, 1);
+    P.template grad_rows<true, T>(static_cast<T*>(nullptr), 0, theta, NN, a, step,
+                                  P.gmaxrow.template as<double>(), tiles);
+    if (gmax_user) {
+      lg::k_reduce_max<<<tiles, 32, 0, ctx->stream>>>(
+          P.gmaxrow.template as<double>(), P.s_gm, int(P.s_gm),
+          ilt->gmax.as<double>() + size_t(it) * tiles);
+      ctx->check_launch();
+    }
+  }
+  if (cost_user) {
+    const size_t bytes = sizeof(double) * size_t(iters) * tiles;
+    LG_CUDA(cudaMemcpyAsync(cost_user, ilt->cost.p, bytes,
+                            is_device_ptr(cost_user) ? cudaMemcpyDeviceToDevice
+                                                     : cudaMemcpyDeviceToHost,
+                            ctx->stream));
+  }
+  if (gmax_user) {
+    const size_t bytes = sizeof(double) * size_t(iters) * tiles;
+    LG_CUDA(cudaMemcpyAsync(gmax_user, ilt->gmax.p, bytes,
+                            is_device_ptr(gmax_user) ? cudaMemcpyDeviceToDevice
+                                                     : cudaMemcpyDeviceToHost,
+                            ctx->stream));
+  }
+  LG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+const char* lithogpu_last_error(void) { return g_last_error.c_str(); }
+
+lithogpu_status lithogpu_ctx_create(int device, lithogpu_ctx** out) {
+  if (!out) {
+    g_last_error = "lithogpu_ctx_create: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    int n = 0;
+    LG_CUDA(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) throw UsageError("lithogpu_ctx_create: bad device index");
+    auto* c = new lithogpu_ctx;
+    c->device = device;
+    LG_CUDA(cudaSetDevice(device));
+    *out = c;
+  });
+}
+
+void lithogpu_ctx_destroy(lithogpu_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  delete ctx;
+}
+
+lithogpu_status lithogpu_ctx_set_stream(lithogpu_ctx* ctx, void* stream) {
+  if (!ctx) {
+    g_last_error = "lithogpu_ctx_set_stream: null context";
+    return LITHOGPU_ERR_USAGE;
+  }
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  g_last_error.clear();
+  return LITHOGPU_OK;
+}
+
+lithogpu_status lithogpu_ctx_synchronize(lithogpu_ctx* ctx) {
+  if (!ctx) {
+    g_last_error = "lithogpu_ctx_synchronize: null context";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    ctx->activate();
+    LG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+long long lithogpu_ctx_launch_count(const lithogpu_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+lithogpu_status lithogpu_rasterize(lithogpu_ctx* ctx, const lithogpu_grid* grid, const int64_t* xy,
+                                   const int64_t* poly_start, int n_poly, double dbu_per_nm,
+                                   double* out) {
+  if (!ctx || !grid || !out || (n_poly > 0 && (!xy || !poly_start)) || n_poly < 0) {
+    g_last_error = "lithogpu_rasterize: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    ctx->activate();
+    if (grid->pitch_nm <= 0) throw std::invalid_argument("rasterize_layer: nonpositive pitch");
+    if (grid->nx <= 0 || grid->ny <= 0) throw std::invalid_argument("rasterize_layer: empty grid");
+    if (!(dbu_per_nm > 0)) throw std::invalid_argument("rasterize_layer: nonpositive dbu_per_nm");
+    const int nx = grid->nx, ny = grid->ny;
+    const size_t npix = size_t(nx) * ny;
+    std::vector<int64_t> st(size_t(n_poly) + 1, 0);
+    if (n_poly > 0) {
+      if (is_device_ptr(poly_start))
+        LG_CUDA(cudaMemcpy(st.data(), poly_start, sizeof(int64_t) * (n_poly + 1), cudaMemcpyDeviceToHost));
+      else
+        std::memcpy(st.data(), poly_start, sizeof(int64_t) * (n_poly + 1));
+    }
+    const int64_t nv = st[n_poly];
+    const int nbx = (nx + lg::kRasterBin - 1) / lg::kRasterBin;
+    const int nby = (ny + lg::kRasterBin - 1) / lg::kRasterBin;
+    const int nbins = nbx * nby;
+    // device scratch
+    DevBuf dxy, dst, vx, vy, bb, cnt, off, tmp;
+    dxy.ensure(sizeof(int64_t) * 2 * std::max<int64_t>(nv, 1));
+    dst.ensure(sizeof(int64_t) * (n_poly + 1));
+    vx.ensure(sizeof(double) * std::max<int64_t>(nv, 1));
+    vy.ensure(sizeof(double) * std::max<int64_t>(nv, 1));
+    bb.ensure(sizeof(int4) * std::max(n_poly, 1));
+    cnt.ensure(sizeof(int) * (nbins + 1));
+    off.ensure(sizeof(int) * (nbins + 1));
+    if (nv > 0) LG_CUDA(cudaMemcpyAsync(dxy.p, xy, sizeof(int64_t) * 2 * nv, cudaMemcpyDefault, ctx->stream));
+    LG_CUDA(cudaMemcpyAsync(dst.p, st.data(), sizeof(int64_t) * (n_poly + 1), cudaMemcpyHostToDevice, ctx->stream));
+    if (n_poly > 0) {
+      lg::k_raster_prep<<<cdiv(n_poly, 128), 128, 0, ctx->stream>>>(
+          dxy.as<int64_t>(), dst.as<int64_t>(), n_poly, 1.0 / dbu_per_nm, grid->origin_x_nm,
+          grid->origin_y_nm, grid->pitch_nm, nx, ny, vx.as<double>(), vy.as<double>(), bb.as<int4>());
+      ctx->check_launch();
+    }
+    LG_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int) * (nbins + 1), ctx->stream));
+    lg::k_raster_bin<false><<<nbins, 256, 0, ctx->stream>>>(bb.as<int4>(), n_poly, nbx, cnt.as<int>(), nullptr, nullptr);
+    ctx->check_launch();
+    size_t tbytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tbytes, cnt.as<int>(), off.as<int>(), nbins + 1, ctx->stream);
+    tmp.ensure(std::max<size_t>(tbytes, 16));
+    cub::DeviceScan::ExclusiveSum(tmp.p, tbytes, cnt.as<int>(), off.as<int>(), nbins + 1, ctx->stream);
+    int total = 0;
+    LG_CUDA(cudaMemcpyAsync(&total, off.as<int>() + nbins, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    LG_CUDA(cudaStreamSynchronize(ctx->stream));
+    DevBuf lists;
+    lists.ensure(sizeof(int) * std::max(total, 1));
+    lg::k_raster_bin<true><<<nbins, 256, 0, ctx->stream>>>(bb.as<int4>(), n_poly, nbx, cnt.as<int>(), off.as<int>(), lists.as<int>());
+    ctx->check_launch();
+    const bool dev_out = is_device_ptr(out);
+    DevBuf obuf;
+    double* dout = out;
+    if (!dev_out) {
+      obuf.ensure(sizeof(double) * npix);
+      dout = obuf.as<double>();
+    }
+    dim3 blk(32, 8), grd(cdiv(nx, 32), cdiv(ny, 8));
+    lg::k_raster_pixels<<<grd, blk, 0, ctx->stream>>>(vx.as<double>(), vy.as<double>(), dst.as<int64_t>(), bb.as<int4>(), off.as<int>(), cnt.as<int>(), lists.as<int>(), nx, ny, nbx, dout);
+    ctx->check_launch();
+    if (!dev_out) LG_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * npix, cudaMemcpyDeviceToHost, ctx->stream));
+    LG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+lithogpu_status lithogpu_kernels_create(lithogpu_ctx* ctx, const lithogpu_grid* grid,
+                                        lithogpu_dtype precision, int n_focus, int order,
+                                        const double* weights, int n_support,
+                                        const int32_t* support, const double* values,
+                                        lithogpu_kernels** out) {
+  if (!ctx || !grid || !weights || !support || !values || !out) {
+    g_last_error = "lithogpu_kernels_create: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    require(precision == LITHOGPU_F32 || precision == LITHOGPU_F64,
+            "lithogpu_kernels_create: precision must be F32 or F64");
+    if (grid->nx <= 0 || grid->ny <= 0 || !(grid->pitch_nm > 0))
+      throw std::invalid_argument("lithogpu_kernels_create: bad grid");
+    if (n_focus <= 0 || order <= 0 || n_support <= 0)
+      throw std::invalid_argument("lithogpu_kernels_create: empty kernel stack");
+    for (int i = 0; i < n_focus * order; ++i)
+      if (!(weights[i] >= 0) || !std::isfinite(weights[i]))
+        throw std::invalid_argument("lithogpu_kernels_create: weights must be finite and >= 0");
+    ctx->activate();
+    auto* ks = new lithogpu_kernels;
+    ks->ctx = ctx;
+    ks->precision = precision;
+    ks->grid = *grid;
+    ks->F = n_focus;
+    ks->K = order;
+    try {
+      if (precision == LITHOGPU_F32)
+        ks->plan.reset(new Plan<float>(ctx, *grid, n_focus, order, weights, n_support, support, values));
+      else
+        ks->plan.reset(new Plan<double>(ctx, *grid, n_focus, order, weights, n_support, support, values));
+    } catch (...) {
+      delete ks;
+      throw;
+    }
+    *out = ks;
+  });
+}
+
+void lithogpu_kernels_destroy(lithogpu_kernels* ks) {
+  if (!ks) return;
+  cudaSetDevice(ks->ctx->device);
+  cudaStreamSynchronize(ks->ctx->stream);
+  delete ks;
+}
+
+lithogpu_status lithogpu_kernels_info(const lithogpu_kernels* ks, int* nx_sub, int* ny_sub,
+                                      int* band_x, int* band_y) {
+  if (!ks) {
+    g_last_error = "lithogpu_kernels_info: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    const lg::AxisGeom *ax, *ay;
+    if (ks->precision == LITHOGPU_F32) {
+      auto& p = const_cast<lithogpu_kernels*>(ks)->p<float>();
+      ax = &p.g.ax;
+      ay = &p.g.ay;
+    } else {
+      auto& p = const_cast<lithogpu_kernels*>(ks)->p<double>();
+      ax = &p.g.ax;
+      ay = &p.g.ay;
+    }
+    if (nx_sub) *nx_sub = ax->n;
+    if (ny_sub) *ny_sub = ay->n;
+    if (band_x) *band_x = ax->B;
+    if (band_y) *band_y = ay->B;
+  });
+}
+
+}  // extern "C"
+
+namespace {
+
+template <typename T>
+void image_impl(lithogpu_kernels* ks, int focus, const void* mask, lithogpu_dtype mdt, double dose,
+                double sigma, double thr, void* I, void* R, lithogpu_dtype odt, unsigned char* pr) {
+  Plan<T>& P = ks->p<T>();
+  lithogpu_ctx* ctx = ks->ctx;
+  const size_t n = size_t(P.g.ax.N) * P.g.ay.N;
+  const T* m = stage_in<T>(ctx, mask, mdt, n, 0);
+  const bool want_r = R || pr;
+  const bool want_i = I != nullptr;
+  P.set_sigma(want_r ? sigma : 0.0);
+  P.forward(m, 0, 1, T(dose), want_i || !want_r, want_r);
+  // all F foci are computed by forward(); output rows only for `focus`
+  OutStage<T> oi(ctx, I, odt, n, 2), orr(ctx, R, odt, n, 4);
+  DevBuf& fullI = ctx->slot(6);
+  DevBuf& fullR = ctx->slot(7);
+  DevBuf& fullP = ctx->slot(8);
+  const size_t Fn = size_t(P.F) * n;
+  fullI.ensure(sizeof(T) * Fn);
+  fullR.ensure(sizeof(T) * Fn);
+  if (pr) fullP.ensure(Fn);
+  P.template out_rows<T>(want_i, want_r, want_i ? fullI.as<T>() : nullptr,
+                         want_r ? fullR.as<T>() : nullptr, pr ? fullP.as<unsigned char>() : nullptr,
+                         0, T(thr), 1);
+  if (I)
+    LG_CUDA(cudaMemcpyAsync(oi.work, fullI.as<T>() + size_t(focus) * n, sizeof(T) * n,
+                            cudaMemcpyDeviceToDevice, ctx->stream));
+  if (R)
+    LG_CUDA(cudaMemcpyAsync(orr.work, fullR.as<T>() + size_t(focus) * n, sizeof(T) * n,
+                            cudaMemcpyDeviceToDevice, ctx->stream));
+  bool host = oi.finish();
+  host |= orr.finish();
+  if (pr) {
+    LG_CUDA(cudaMemcpyAsync(pr, fullP.as<unsigned char>() + size_t(focus) * n, n, cudaMemcpyDefault,
+                            ctx->stream));
+    host |= !is_device_ptr(pr);
+  }
+  if (host || !is_device_ptr(mask)) LG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+}  // namespace
+
+extern "C" {
+
+lithogpu_status lithogpu_image_resist(lithogpu_kernels* ks, int focus, const void* mask,
+                                      lithogpu_dtype mask_dtype, double dose, double sigma_nm,
+                                      double threshold, void* intensity, void* resist,
+                                      lithogpu_dtype out_dtype, unsigned char* print) {
+  if (!ks || !mask) {
+    g_last_error = "lithogpu_image_resist: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    if (focus < 0 || focus >= ks->F) throw UsageError("lithogpu_image: focus index out of range");
+    if (sigma_nm < 0) throw std::invalid_argument("gaussian_blur: negative sigma");
+    dtype_size(mask_dtype);
+    dtype_size(out_dtype);
+    ks->ctx->activate();
+    if (ks->precision == LITHOGPU_F32)
+      image_impl<float>(ks, focus, mask, mask_dtype, dose, sigma_nm, threshold, intensity, resist,
+                        out_dtype, print);
+    else
+      image_impl<double>(ks, focus, mask, mask_dtype, dose, sigma_nm, threshold, intensity, resist,
+                         out_dtype, print);
+  });
+}
+
+lithogpu_status lithogpu_image_socs(lithogpu_kernels* ks, int focus, const void* mask,
+                                    lithogpu_dtype mask_dtype, double dose, void* intensity,
+                                    lithogpu_dtype out_dtype) {
+  if (!intensity) {
+    g_last_error = "lithogpu_image_socs: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return lithogpu_image_resist(ks, focus, mask, mask_dtype, dose, 0.0, 0.0, intensity, nullptr,
+                               out_dtype, nullptr);
+}
+
+lithogpu_status lithogpu_intensity_gradient(lithogpu_kernels* ks, int focus, const void* mask,
+                                            lithogpu_dtype mask_dtype, const void* weight,
+                                            lithogpu_dtype weight_dtype, double dose, void* grad,
+                                            lithogpu_dtype grad_dtype) {
+  if (!ks || !mask || !grad) {
+    g_last_error = "lithogpu_intensity_gradient: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    if (focus < 0 || focus >= ks->F) throw UsageError("intensity_gradient: focus out of range");
+    ks->ctx->activate();
+    auto run = [&](auto tag) {
+      using T = decltype(tag);
+      Plan<T>& P = ks->p<T>();
+      lithogpu_ctx* ctx = ks->ctx;
+      const size_t n = size_t(P.g.ax.N) * P.g.ay.N;
+      const T* m = stage_in<T>(ctx, mask, mask_dtype, n, 0);
+      const T* w = weight ? stage_in<T>(ctx, weight, weight_dtype, n, 2) : nullptr;
+      OutStage<T> og(ctx, grad, grad_dtype, n, 4);
+      // single focus: temporarily view stack `focus` as a 1-stack plan
+      const int F0 = P.F;
+      lg::Geo<T> g0 = P.g;
+      DevBuf& Hf = ctx->slot(9);
+      DevBuf& wf = ctx->slot(10);
+      const size_t hsz = size_t(P.K) * P.g.ay.B * P.g.ax.B * sizeof(lg::cx<T>);
+      Hf.ensure(hsz);
+      wf.ensure(sizeof(T) * P.K);
+      LG_CUDA(cudaMemcpyAsync(Hf.p, P.H.template as<char>() + hsz * focus, hsz, cudaMemcpyDeviceToDevice, ctx->stream));
+      LG_CUDA(cudaMemcpyAsync(wf.p, P.wk.template as<T>() + size_t(P.K) * focus, sizeof(T) * P.K, cudaMemcpyDeviceToDevice, ctx->stream));
+      std::swap(P.H.p, Hf.p);
+      std::swap(P.wk.p, wf.p);
+      P.F = 1;
+      P.g.F = 1;
+      try {
+        P.gradient(m, w, T(dose), og.work);
+      } catch (...) {
+        std::swap(P.H.p, Hf.p);
+        std::swap(P.wk.p, wf.p);
+        P.F = F0;
+        P.g = g0;
+        throw;
+      }
+      std::swap(P.H.p, Hf.p);
+      std::swap(P.wk.p, wf.p);
+      P.F = F0;
+      P.g = g0;
+      const bool host = og.finish();
+      if (host || !is_device_ptr(mask)) LG_CUDA(cudaStreamSynchronize(ctx->stream));
+    };
+    if (ks->precision == LITHOGPU_F32)
+      run(float{});
+    else
+      run(double{});
+  });
+}
+
+lithogpu_status lithogpu_gaussian_blur(lithogpu_ctx* ctx, const lithogpu_grid* grid,
+                                       const void* in, lithogpu_dtype dtype, double sigma_nm,
+                                       void* out) {
+  if (!ctx || !grid || !in || !out) {
+    g_last_error = "lithogpu_gaussian_blur: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    if (sigma_nm < 0) throw std::invalid_argument("gaussian_blur: negative sigma");
+    require(dtype == LITHOGPU_F32 || dtype == LITHOGPU_F64, "gaussian_blur: dtype must be F32/F64");
+    ctx->activate();
+    const int nx = grid->nx, ny = grid->ny;
+    const size_t n = size_t(nx) * ny;
+    auto run = [&](auto tag) {
+      using T = decltype(tag);
+      const T* src = stage_in<T>(ctx, in, dtype, n, 0);
+      OutStage<T> o(ctx, out, dtype, n, 2);
+      if (sigma_nm == 0) {
+        LG_CUDA(cudaMemcpyAsync(o.work, src, sizeof(T) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+      } else {
+        const double sp = sigma_nm / grid->pitch_nm;
+        int rx, ry;
+        auto tx = gauss_taps(nx, sp, rx);
+        auto ty = gauss_taps(ny, sp, ry);
+        std::vector<T> hx(tx.begin(), tx.end()), hy(ty.begin(), ty.end());
+        DevBuf& dt = ctx->slot(11);
+        DevBuf& mid = ctx->slot(12);
+        dt.ensure(sizeof(T) * (hx.size() + hy.size()));
+        mid.ensure(sizeof(T) * n);
+        LG_CUDA(cudaMemcpyAsync(dt.p, hx.data(), sizeof(T) * hx.size(), cudaMemcpyHostToDevice, ctx->stream));
+        LG_CUDA(cudaMemcpyAsync(dt.as<T>() + hx.size(), hy.data(), sizeof(T) * hy.size(), cudaMemcpyHostToDevice, ctx->stream));
+        dim3 blk(32, 8), grd(cdiv(nx, 32), cdiv(ny, 8));
+        lg::k_blur_pass<T, 0><<<grd, blk, 0, ctx->stream>>>(src, mid.as<T>(), nx, ny, dt.as<T>(), rx);
+        ctx->check_launch();
+        lg::k_blur_pass<T, 1><<<grd, blk, 0, ctx->stream>>>(mid.as<T>(), o.work, nx, ny, dt.as<T>() + hx.size(), ry);
+        ctx->check_launch();
+        LG_CUDA(cudaStreamSynchronize(ctx->stream));  // host taps lifetime
+      }
+      const bool host = o.finish();
+      if (host) LG_CUDA(cudaStreamSynchronize(ctx->stream));
+    };
+    if (dtype == LITHOGPU_F32)
+      run(float{});
+    else
+      run(double{});
+  });
+}
+
+lithogpu_status lithogpu_threshold(lithogpu_ctx* ctx, size_t n, const void* in,
+                                   lithogpu_dtype in_dtype, double tau, void* out,
+                                   lithogpu_dtype out_dtype) {
+  if (!ctx || !in || !out) {
+    g_last_error = "lithogpu_threshold: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    dtype_size(in_dtype);
+    dtype_size(out_dtype);
+    ctx->activate();
+    const double* src = stage_in<double>(ctx, in, in_dtype, n, 0);
+    OutStage<double> o(ctx, out, out_dtype, n, 2);
+    const int blocks = int(std::min<size_t>((n + 255) / 256, 148 * 16));
+    if (n) {
+      lg::k_threshold<double, double><<<blocks, 256, 0, ctx->stream>>>(src, o.work, n, tau);
+      ctx->check_launch();
+    }
+    const bool host = o.finish();
+    if (host || !is_device_ptr(in)) LG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+lithogpu_status lithogpu_ilt_create(lithogpu_kernels* ks, const lithogpu_ilt_params* params,
+                                    int n_tiles, lithogpu_ilt** out) {
+  if (!ks || !params || !out || !params->focus_weights) {
+    g_last_error = "lithogpu_ilt_create: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    if (n_tiles <= 0) throw UsageError("lithogpu_ilt_create: n_tiles must be > 0");
+    if (params->resist_sigma_nm < 0) throw std::invalid_argument("ilt: negative resist sigma");
+    ks->ctx->activate();
+    auto* ilt = new lithogpu_ilt;
+    ilt->ks = ks;
+    ilt->prm = *params;
+    ilt->cf.assign(params->focus_weights, params->focus_weights + ks->F);
+    ilt->prm.focus_weights = ilt->cf.data();
+    ilt->tiles = n_tiles;
+    const size_t es = ks->precision == LITHOGPU_F32 ? 4 : 8;
+    const size_t n = size_t(ks->grid.nx) * ks->grid.ny * n_tiles;
+    try {
+      ilt->theta.ensure(es * n);
+      ilt->target.ensure(es * n);
+      ilt->cfd.ensure(es * ks->F);
+      if (es == 4) {
+        std::vector<float> c(ilt->cf.begin(), ilt->cf.end());
+        LG_CUDA(cudaMemcpy(ilt->cfd.p, c.data(), 4 * c.size(), cudaMemcpyHostToDevice));
+      } else {
+        LG_CUDA(cudaMemcpy(ilt->cfd.p, ilt->cf.data(), 8 * ilt->cf.size(), cudaMemcpyHostToDevice));
+      }
+      LG_CUDA(cudaMemset(ilt->theta.p, 0, es * n));
+      LG_CUDA(cudaMemset(ilt->target.p, 0, es * n));
+    } catch (...) {
+      delete ilt;
+      throw;
+    }
+    *out = ilt;
+  });
+}
+
+void lithogpu_ilt_destroy(lithogpu_ilt* ilt) {
+  if (!ilt) return;
+  cudaSetDevice(ilt->ks->ctx->device);
+  cudaStreamSynchronize(ilt->ks->ctx->stream);
+  delete ilt;
+}
+
+}  // extern "C"
+
+namespace {
+
+template <typename T>
+void ilt_set_impl(lithogpu_ilt* ilt, int tile0, int ntl, const void* target, const void* theta0,
+                  lithogpu_dtype dt) {
+  lithogpu_ctx* ctx = ilt->ks->ctx;
+  const size_t n1 = size_t(ilt->ks->grid.nx) * ilt->ks->grid.ny;
+  const size_t n = n1 * ntl;
+  const T* tg = stage_in<T>(ctx, target, dt, n, 0);
+  T* dtg = ilt->target.as<T>() + n1 * tile0;
+  T* dth = ilt->theta.as<T>() + n1 * tile0;
+  LG_CUDA(cudaMemcpyAsync(dtg, tg, sizeof(T) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (theta0) {
+    const T* th = stage_in<T>(ctx, theta0, dt, n, 2);
+    LG_CUDA(cudaMemcpyAsync(dth, th, sizeof(T) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  } else {
+    const int blocks = int(std::min<size_t>((n + 255) / 256, 148 * 16));
+    lg::k_theta_init<T><<<blocks, 256, 0, ctx->stream>>>(dtg, dth, n, T(2.0 / ilt->prm.mask_steepness));
+    ctx->check_launch();
+  }
+  if (!is_device_ptr(target) || (theta0 && !is_device_ptr(theta0)))
+    LG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+template <typename T>
+void ilt_get_impl(lithogpu_ilt* ilt, int tile0, int ntl, void* theta, void* mask, lithogpu_dtype dt) {
+  lithogpu_ctx* ctx = ilt->ks->ctx;
+  const size_t n1 = size_t(ilt->ks->grid.nx) * ilt->ks->grid.ny;
+  const size_t n = n1 * ntl;
+  const T* th = ilt->theta.as<T>() + n1 * tile0;
+  bool host = false;
+  if (theta) {
+    OutStage<T> o(ctx, theta, dt, n, 0);
+    LG_CUDA(cudaMemcpyAsync(o.work, th, sizeof(T) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    host |= o.finish();
+  }
+  if (mask) {
+    OutStage<T> o(ctx, mask, dt, n, 2);
+    const int blocks = int(std::min<size_t>((n + 255) / 256, 148 * 16));
+    lg::k_sigmoid<T><<<blocks, 256, 0, ctx->stream>>>(th, o.work, n, T(ilt->prm.mask_steepness));
+    ctx->check_launch();
+    host |= o.finish();
+  }
+  if (host) LG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+}  // namespace
+
+extern "C" {
+
+lithogpu_status lithogpu_ilt_set_tile(lithogpu_ilt* ilt, int tile, const void* target,
+                                      const void* theta0, lithogpu_dtype dtype) {
+  if (!ilt || !target) {
+    g_last_error = "lithogpu_ilt_set_tile: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    if (tile < 0 || tile >= ilt->tiles) throw UsageError("lithogpu_ilt_set_tile: tile out of range");
+    dtype_size(dtype);
+    ilt->ks->ctx->activate();
+    if (ilt->ks->precision == LITHOGPU_F32)
+      ilt_set_impl<float>(ilt, tile, 1, target, theta0, dtype);
+    else
+      ilt_set_impl<double>(ilt, tile, 1, target, theta0, dtype);
+  });
+}
+
+lithogpu_status lithogpu_ilt_set_tiles(lithogpu_ilt* ilt, const void* target, const void* theta0,
+                                       lithogpu_dtype dtype) {
+  if (!ilt || !target) {
+    g_last_error = "lithogpu_ilt_set_tiles: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    dtype_size(dtype);
+    ilt->ks->ctx->activate();
+    if (ilt->ks->precision == LITHOGPU_F32)
+      ilt_set_impl<float>(ilt, 0, ilt->tiles, target, theta0, dtype);
+    else
+      ilt_set_impl<double>(ilt, 0, ilt->tiles, target, theta0, dtype);
+  });
+}
+
+lithogpu_status lithogpu_ilt_run(lithogpu_ilt* ilt, int iterations, double* cost, double* gmax) {
+  if (!ilt) {
+    g_last_error = "lithogpu_ilt_run: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    if (iterations < 0) throw UsageError("lithogpu_ilt_run: negative iteration count");
+    ilt->ks->ctx->activate();
+    if (ilt->ks->precision == LITHOGPU_F32)
+      ilt_run_impl<float>(ilt, iterations, cost, gmax);
+    else
+      ilt_run_impl<double>(ilt, iterations, cost, gmax);
+  });
+}
+
+lithogpu_status lithogpu_ilt_get_tile(lithogpu_ilt* ilt, int tile, void* theta, void* mask,
+                                      lithogpu_dtype dtype) {
+  if (!ilt) {
+    g_last_error = "lithogpu_ilt_get_tile: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    if (tile < 0 || tile >= ilt->tiles) throw UsageError("lithogpu_ilt_get_tile: tile out of range");
+    dtype_size(dtype);
+    ilt->ks->ctx->activate();
+    if (ilt->ks->precision == LITHOGPU_F32)
+      ilt_get_impl<float>(ilt, tile, 1, theta, mask, dtype);
+    else
+      ilt_get_impl<double>(ilt, tile, 1, theta, mask, dtype);
+  });
+}
+
+lithogpu_status lithogpu_ilt_get_tiles(lithogpu_ilt* ilt, void* theta, void* mask,
+                                       lithogpu_dtype dtype) {
+  if (!ilt) {
+    g_last_error = "lithogpu_ilt_get_tiles: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    dtype_size(dtype);
+    ilt->ks->ctx->activate();
+    if (ilt->ks->precision == LITHOGPU_F32)
+      ilt_get_impl<float>(ilt, 0, ilt->tiles, theta, mask, dtype);
+    else
+      ilt_get_impl<double>(ilt, 0, ilt->tiles, theta, mask, dtype);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,332 @@
+// Device-side FFT building blocks for the SOCS imaging / ILT kernels (sm_100a).
+//
+// One "row group" of TPR threads transforms one length-L complex row held in
+// shared memory (split re/im arrays, one pad word per 128 B so the strided
+// Stockham stores stay bank-conflict free).  Power-of-two L >= 16 runs a
+// Stockham autosort FFT with radix-16 register butterflies (16 values per
+// thread, TPR = L/16, final radix 8/4/2 stage as needed); any other length
+// falls back to a direct O(L^2) DFT with an exact twiddle table (correctness
+// path for the reference's odd test grids, reference tests use 12/16/24 and
+// 74x49 windows).
+//
+// Conventions are the reference fft2 (proj/src/core/imaging.cpp:17-31):
+// SIGN = -1 forward exp(-2 pi i k x / L), SIGN = +1 backward, unnormalized.
+// Twiddle tables hold exp(-2 pi i m / L), m < L, rounded once from fp64.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace lg {
+
+template <typename T>
+struct alignas(2 * sizeof(T)) cx {
+  T x, y;
+};
+
+template <typename T>
+__device__ __forceinline__ cx<T> mk(T a, T b) {
+  cx<T> r;
+  r.x = a;
+  r.y = b;
+  return r;
+}
+template <typename T>
+__device__ __forceinline__ cx<T> add(cx<T> a, cx<T> b) {
+  return mk(a.x + b.x, a.y + b.y);
+}
+template <typename T>
+__device__ __forceinline__ cx<T> sub(cx<T> a, cx<T> b) {
+  return mk(a.x - b.x, a.y - b.y);
+}
+template <typename T>
+__device__ __forceinline__ cx<T> mul(cx<T> a, cx<T> b) {
+  return mk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// a * conj(b)
+template <typename T>
+__device__ __forceinline__ cx<T> mulc(cx<T> a, cx<T> b) {
+  return mk(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+template <typename T>
+__device__ __forceinline__ cx<T> conjg(cx<T> a) {
+  return mk(a.x, -a.y);
+}
+template <typename T>
+__device__ __forceinline__ cx<T> scale(cx<T> a, T s) {
+  return mk(a.x * s, a.y * s);
+}
+// read-only cached load of a complex value
+__device__ __forceinline__ cx<float> ldg_cx(const cx<float>* p) {
+  const float2 v = __ldg(reinterpret_cast<const float2*>(p));
+  return mk(v.x, v.y);
+}
+__device__ __forceinline__ cx<double> ldg_cx(const cx<double>* p) {
+  const double2 v = __ldg(reinterpret_cast<const double2*>(p));
+  return mk(v.x, v.y);
+}
+
+// a * (S * i)
+template <int S, typename T>
+__device__ __forceinline__ cx<T> mul_si(cx<T> a) {
+  return S < 0 ? mk(a.y, -a.x) : mk(-a.y, a.x);
+}
+
+// ---- shared-memory row layout -------------------------------------------
+template <typename T>
+__host__ __device__ constexpr int pad_shift() {
+  return sizeof(T) == 4 ? 5 : 4;  // one pad element per 128 bytes
+}
+template <typename T>
+__host__ __device__ __forceinline__ int pidx(int i) {
+  return i + (i >> pad_shift<T>());
+}
+template <typename T>
+__host__ __device__ constexpr int padded_len(int L) {
+  return L + (L >> pad_shift<T>()) + 1;
+}
+
+__host__ __device__ inline bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
+__host__ __device__ inline int ilog2(int n) {
+  int l = 0;
+  while ((1 << l) < n) ++l;
+  return l;
+}
+__host__ __device__ inline int next_pow2(int n) { return 1 << ilog2(n); }
+// threads per row group for a length-L transform
+__host__ __device__ inline int tpr_for(int L) {
+  const int t = next_pow2(L) / 16;
+  return t < 1 ? 1 : t;
+}
+
+// Row-group context: one length-L row in smem, processed by TPR threads.
+template <typename T>
+struct Row {
+  T* re;
+  T* im;
+  T* sre;  // scratch (generic DFT only), length L unpadded
+  T* sim;
+  int L;
+  int log2L;  // >= 0 iff fast pow2 path
+  int t;      // thread index in group
+  int TPR;
+  bool cta_sync;  // TPR > 32 -> group spans warps
+  bool active;
+  const cx<T>* tw;  // exp(-2 pi i m / L)
+
+  __device__ __forceinline__ void sync() const {
+    if (cta_sync)
+      __syncthreads();
+    else
+      __syncwarp();
+  }
+  __device__ __forceinline__ cx<T> ld(int i) const {
+    const int p = pidx<T>(i);
+    return mk(re[p], im[p]);
+  }
+  __device__ __forceinline__ void st(int i, cx<T> v) const {
+    const int p = pidx<T>(i);
+    re[p] = v.x;
+    im[p] = v.y;
+  }
+  __device__ __forceinline__ void zero() const {
+    if (!active) return;
+    for (int i = t; i < L; i += TPR) st(i, mk(T(0), T(0)));
+  }
+};
+
+// ---- radix-R DFT on registers, natural-order in and out -----------------
+template <int S, typename T>
+__device__ __forceinline__ void dft2(cx<T>& a, cx<T>& b) {
+  const cx<T> t = a;
+  a = add(t, b);
+  b = sub(t, b);
+}
+
+template <int S, typename T>
+__device__ __forceinline__ void dft4(cx<T>& v0, cx<T>& v1, cx<T>& v2, cx<T>& v3) {
+  const cx<T> t0 = add(v0, v2), t1 = sub(v0, v2), t2 = add(v1, v3);
+  const cx<T> t3 = mul_si<S>(sub(v1, v3));
+  v0 = add(t0, t2);
+  v2 = sub(t0, t2);
+  v1 = add(t1, t3);
+  v3 = sub(t1, t3);
+}
+
+// multiply by W_R^q = exp(S 2 pi i q / R) for R = 8, 16 with cheap special cases
+template <int R, int Q, int S, typename T>
+__device__ __forceinline__ cx<T> twc(cx<T> a) {
+  constexpr int q = Q % R;
+  if constexpr (q == 0) {
+    return a;
+  } else if constexpr (4 * q == R) {
+    return mul_si<S>(a);
+  } else if constexpr (8 * q == R) {  // (1 + S i)/sqrt2
+    const T c = T(0.70710678118654752440);
+    return S < 0 ? mk(c * (a.x + a.y), c * (a.y - a.x)) : mk(c * (a.x - a.y), c * (a.y + a.x));
+  } else if constexpr (8 * q == 3 * R) {  // (-1 + S i)/sqrt2
+    const T c = T(0.70710678118654752440);
+    return S < 0 ? mk(c * (a.y - a.x), -c * (a.x + a.y)) : mk(-c * (a.x + a.y), c * (a.x - a.y));
+  } else {
+    // generic: only R = 16, q in {1,3,5,7}
+    constexpr double C1 = 0.92387953251128675613, S1 = 0.38268343236508977173;
+    constexpr double cr = (q == 1) ? C1 : (q == 3) ? S1 : (q == 5) ? -S1 : -C1;
+    constexpr double si = (q == 1) ? S1 : (q == 3) ? C1 : (q == 5) ? C1 : S1;
+    const cx<T> w = mk(T(cr), T(S * si));
+    return mul(a, w);
+  }
+}
+
+template <int S, typename T>
+__device__ __forceinline__ void dft8(cx<T>* v) {
+  cx<T> e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
+  cx<T> o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
+  dft4<S>(e0, e1, e2, e3);
+  dft4<S>(o0, o1, o2, o3);
+  o1 = twc<8, 1, S>(o1);
+  o2 = twc<8, 2, S>(o2);
+  o3 = twc<8, 3, S>(o3);
+  v[0] = add(e0, o0);
+  v[4] = sub(e0, o0);
+  v[1] = add(e1, o1);
+  v[5] = sub(e1, o1);
+  v[2] = add(e2, o2);
+  v[6] = sub(e2, o2);
+  v[3] = add(e3, o3);
+  v[7] = sub(e3, o3);
+}
+
+template <int S, typename T>
+__device__ __forceinline__ void dft16(cx<T>* v) {
+  cx<T> e[8], o[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    e[i] = v[2 * i];
+    o[i] = v[2 * i + 1];
+  }
+  dft8<S>(e);
+  dft8<S>(o);
+  o[1] = twc<16, 1, S>(o[1]);
+  o[2] = twc<16, 2, S>(o[2]);
+  o[3] = twc<16, 3, S>(o[3]);
+  o[4] = twc<16, 4, S>(o[4]);
+  o[5] = twc<16, 5, S>(o[5]);
+  o[6] = twc<16, 6, S>(o[6]);
+  o[7] = twc<16, 7, S>(o[7]);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    v[i] = add(e[i], o[i]);
+    v[i + 8] = sub(e[i], o[i]);
+  }
+}
+
+template <int R, int S, typename T>
+__device__ __forceinline__ void dftR(cx<T>* v) {
+  if constexpr (R == 2) {
+    dft2<S>(v[0], v[1]);
+  } else if constexpr (R == 4) {
+    dft4<S>(v[0], v[1], v[2], v[3]);
+  } else if constexpr (R == 8) {
+    dft8<S>(v);
+  } else {
+    dft16<S>(v);
+  }
+}
+
+// One Stockham stage of radix R (Govindaraju et al. formulation): butterfly
+// j reads x[j + r L/R], twiddles by W_{Ns R}^{r (j mod Ns)}, transforms, and
+// writes to (j - j mod Ns) R + j mod Ns + r Ns.  Each thread owns 16/R
+// butterflies (j = t + b TPR), i.e. 16 values per stage.
+template <typename T, int R, int S>
+__device__ __forceinline__ void stockham_stage(const Row<T>& row, int Ns) {
+  constexpr int NB = 16 / R;
+  cx<T> v[NB][R];
+  const int LR = row.L / R;
+  if (row.active) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int j = row.t + b * row.TPR;
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[b][r] = row.ld(j + r * LR);
+    }
+  }
+  row.sync();
+  if (row.active) {
+    const int tstride = row.L / (Ns * R);
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int j = row.t + b * row.TPR;
+      const int k = j & (Ns - 1);
+      if (Ns > 1) {
+#pragma unroll
+        for (int r = 1; r < R; ++r) {
+          cx<T> w = ldg_cx(row.tw + r * k * tstride);
+          if (S > 0) w.y = -w.y;
+          v[b][r] = mul(v[b][r], w);
+        }
+      }
+      dftR<R, S>(v[b]);
+      const int base = (j - k) * R + k;
+#pragma unroll
+      for (int r = 0; r < R; ++r) row.st(base + r * Ns, v[b][r]);
+    }
+  }
+  row.sync();
+}
+
+template <typename T, int S>
+__device__ __forceinline__ void fft_pow2(const Row<T>& row) {
+  int Ns = 1;
+  int rem = row.log2L;
+  while (rem >= 4) {
+    stockham_stage<T, 16, S>(row, Ns);
+    Ns <<= 4;
+    rem -= 4;
+  }
+  if (rem == 3)
+    stockham_stage<T, 8, S>(row, Ns);
+  else if (rem == 2)
+    stockham_stage<T, 4, S>(row, Ns);
+  else if (rem == 1)
+    stockham_stage<T, 2, S>(row, Ns);
+}
+
+// direct DFT, any L (correctness path)
+template <typename T, int S>
+__device__ void dft_generic(const Row<T>& row) {
+  const int L = row.L;
+  if (row.active) {
+    for (int q = row.t; q < L; q += row.TPR) {
+      T ar = 0, ai = 0;
+      int m = 0;
+      for (int x = 0; x < L; ++x) {
+        const cx<T> v = row.ld(x);
+        cx<T> w = row.tw[m];
+        if (S > 0) w.y = -w.y;
+        ar += v.x * w.x - v.y * w.y;
+        ai += v.x * w.y + v.y * w.x;
+        m += q;
+        if (m >= L) m -= L;
+      }
+      row.sre[q] = ar;
+      row.sim[q] = ai;
+    }
+  }
+  row.sync();
+  if (row.active)
+    for (int q = row.t; q < L; q += row.TPR) row.st(q, mk(row.sre[q], row.sim[q]));
+  row.sync();
+}
+
+// In-place transform of the row; callers sync before (data written) and may
+// read the result right after (ends with a sync).
+template <typename T, int S>
+__device__ __forceinline__ void fft(const Row<T>& row) {
+  if (row.log2L >= 4)
+    fft_pow2<T, S>(row);
+  else
+    dft_generic<T, S>(row);
+}
+
+}  // namespace lg

@@ -1,0 +1,78 @@
+// Small elementwise / stencil kernels: dtype conversion, threshold resist,
+// direct separable Gaussian blur.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace lg {
+
+template <typename A, typename B>
+__global__ void k_convert(const A* __restrict__ in, B* __restrict__ out, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    out[i] = B(in[i]);
+}
+
+// z_print / ResistImage threshold (ai.cpp:90-92): v >= tau -> 1 else 0
+template <typename A, typename B>
+__global__ void k_threshold(const A* __restrict__ in, B* __restrict__ out, size_t n, double tau) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    out[i] = double(in[i]) >= tau ? B(1) : B(0);
+}
+
+// theta0 = (2 target - 1) * c
+template <typename T>
+__global__ void k_theta_init(const T* __restrict__ target, T* __restrict__ theta, size_t n, T c) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    theta[i] = (T(2) * target[i] - T(1)) * c;
+}
+
+template <typename T>
+__global__ void k_sigmoid(const T* __restrict__ theta, T* __restrict__ m, size_t n, T a) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    m[i] = T(1) / (T(1) + exp(-a * theta[i]));
+}
+
+// One separable pass of the cyclic truncated Gaussian (gaussian_blur,
+// imaging.cpp:287-314, is the same cyclic convolution done with 3 FFTs).
+// AXIS 0: along x (contiguous), AXIS 1: along y.  taps[d + r] = g(d)/sum g.
+template <typename T, int AXIS>
+__global__ void k_blur_pass(const T* __restrict__ in, T* __restrict__ out, int nx, int ny,
+                            const T* __restrict__ taps, int r) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= nx || y >= ny) return;
+  T acc = T(0);
+  if (AXIS == 0) {
+    const T* row = in + size_t(y) * nx;
+    for (int d = -r; d <= r; ++d) {
+      int xs = (x - d) % nx;
+      xs += xs < 0 ? nx : 0;
+      acc += taps[d + r] * row[xs];
+    }
+  } else {
+    for (int d = -r; d <= r; ++d) {
+      int ys = (y - d) % ny;
+      ys += ys < 0 ? ny : 0;
+      acc += taps[d + r] * in[size_t(ys) * nx + x];
+    }
+  }
+  out[size_t(y) * nx + x] = acc;
+}
+
+// per-tile max of n row partials, fixed order (deterministic); one block of 32 per tile
+__global__ void k_reduce_max(const double* __restrict__ rows, long long ts, int n,
+                             double* __restrict__ out) {
+  const double* r = rows + blockIdx.x * ts;
+  double m = 0;
+  for (int i = threadIdx.x; i < n; i += 32) m = fmax(m, r[i]);
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_down_sync(0xffffffffu, m, o));
+  if (threadIdx.x == 0) out[blockIdx.x] = m;
+}
+
+}  // namespace lg

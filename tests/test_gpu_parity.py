@@ -1,0 +1,170 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the CPU oracle
+(oracle/, itself pinned to the reference) and the committed golden vectors.
+
+Tolerances: fp32 path rel L-inf <= 1e-4 (north star); fp64 path at the
+reference's own test tolerances (test_imaging.cpp: 1e-6 .. 1e-10).
+Rasterization: bitwise.
+"""
+import numpy as np
+import pytest
+
+import paper_2602_15036_b200 as L
+from oracle import oracle as O
+from oracle import refpy as R
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_linf(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    s = np.abs(b).max()
+    return np.abs(a - b).max() / (s if s > 0 else 1.0)
+
+
+def euv(grid_n=7):
+    return L.OpticalModel(source=L.make_annular_source(0.4, 0.8, grid_n))
+
+
+def kernels_for(n, pitch, focus=(0.0,), k=0, floor=0.995, grid_n=7, ny=None):
+    g = L.Grid(n, ny or n, pitch)
+    return L.build_socs_kernels(euv(grid_n), g, list(focus), k_fixed=k, energy_floor=floor)
+
+
+# (nx, ny, pitch, K, grid_n): small generic-DFT grids, decimated pow2 grids, C1 scale
+IMG_CASES = [
+    (16, 16, 4.0, 0, 7),
+    (24, 24, 4.0, 0, 7),
+    (16, 12, 4.0, 0, 7),
+    (64, 64, 1.0, 8, 21),
+    (256, 256, 1.0, 8, 21),
+    (128, 256, 1.0, 12, 21),
+    (1024, 1024, 1.0, 8, 21),
+]
+
+
+@pytest.mark.parametrize("nx,ny,pitch,K,gn", IMG_CASES)
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_image_socs_vs_oracle(ctx, nx, ny, pitch, K, gn, prec):
+    rng = np.random.default_rng(nx * 7 + ny)
+    ks = kernels_for(nx, pitch, (30.0,), k=K, grid_n=gn, ny=ny)
+    mask = rng.random((ny, nx))
+    want = O.image_socs(mask, ks.weights[0], ks.support, ks.values[0], dose=1.3)
+    dk = L.DeviceKernels(ks, prec, ctx)
+    got = dk.image(mask, dose=1.3)["intensity"]
+    tol = 1e-4 if prec == "f32" else 1e-10
+    assert rel_linf(got, want) < tol, dk.info()
+
+
+@pytest.mark.parametrize("prec,tol", [("f32", 1e-4), ("f64", 1e-10)])
+def test_resist_image_vs_oracle(ctx, prec, tol):
+    rng = np.random.default_rng(3)
+    ks = kernels_for(256, 1.0, (0.0,), k=8, grid_n=21)
+    mask = (rng.random((256, 256)) > 0.6).astype(np.float64)
+    I = O.image_socs(mask, ks.weights[0], ks.support, ks.values[0])
+    Rr = O.gaussian_blur(I, 2.0, 1.0)
+    dk = L.DeviceKernels(ks, prec, ctx)
+    out = dk.image(mask, sigma_nm=2.0, threshold=0.25, want=("intensity", "resist", "print"))
+    assert rel_linf(out["intensity"], I) < tol
+    assert rel_linf(out["resist"], Rr) < tol
+    ref_print = O.threshold(Rr, 0.25)
+    guard = np.abs(Rr - 0.25) > 1e-4 * np.abs(Rr).max()
+    assert np.array_equal(out["print"][guard], ref_print[guard])
+
+
+def test_full_rank_equals_reference_hopkins(ctx):
+    """reference test_imaging.cpp:157-171 run through the drop-in (fp64)."""
+    rng = np.random.default_rng(41)
+    for n in (12, 16, 24):
+        for focus in (0.0, 30.0):
+            rk = R.RefKernels(n, n, 4.0, focus=focus, energy_floor=1.0, full_rank=True)
+            ks = L.SocsKernelSet(L.Grid(n, n, 4.0), [focus], rk.weights[None], rk.support, rk.values[None])
+            mask = rng.random((n, n))
+            got = L.image_socs(mask, ks, 1.0, precision="f64", ctx=ctx)
+            assert rel_linf(got, rk.hopkins(mask)) < 1e-6
+
+
+def test_clear_field_flat(ctx):
+    """reference test_imaging.cpp:186-195."""
+    rk = R.RefKernels(24, 24, 4.0, energy_floor=1.0, full_rank=True)
+    ks = L.SocsKernelSet(L.Grid(24, 24, 4.0), [0.0], rk.weights[None], rk.support, rk.values[None])
+    got = L.image_socs(np.ones((24, 24)), ks, 1.3, precision="f64", ctx=ctx)
+    assert np.abs(got - 1.3).max() < 1e-6
+
+
+@pytest.mark.parametrize("shape,pitch,sigma", [((12, 16), 2.0, 2.5), ((256, 256), 1.0, 2.0),
+                                               ((64, 128), 1.0, 3.0)])
+def test_gaussian_blur_vs_oracle(ctx, shape, pitch, sigma):
+    rng = np.random.default_rng(59)
+    v = rng.random(shape)
+    g = L.Grid(shape[1], shape[0], pitch)
+    got = L.gaussian_blur(g, v, sigma, ctx)
+    assert rel_linf(got, O.gaussian_blur(v, sigma, pitch)) < 1e-10
+    assert np.array_equal(L.gaussian_blur(g, v, 0.0, ctx), v)
+
+
+@pytest.mark.parametrize("n,pitch,K,gn", [(16, 4.0, 0, 5), (64, 1.0, 8, 21), (256, 1.0, 16, 21),
+                                          (512, 1.0, 16, 21)])
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("weighted", [False, True])
+def test_gradient_vs_oracle(ctx, n, pitch, K, gn, prec, weighted):
+    rng = np.random.default_rng(89 + n)
+    ks = kernels_for(n, pitch, (0.0,), k=K, grid_n=gn, floor=1.0 if K == 0 else 0.995)
+    mask = rng.random((n, n))
+    W = rng.standard_normal((n, n)) if weighted else None
+    want = O.weighted_gradient(mask, ks.weights[0], ks.support, ks.values[0], W, dose=1.3)
+    got = L.intensity_gradient(mask, ks, 1.3, weight=W, precision=prec, ctx=ctx)
+    tol = 1e-4 if prec == "f32" else 1e-9
+    assert rel_linf(got, want) < tol
+
+
+@pytest.mark.parametrize("n,F,K,prec,tol", [(64, 1, 8, "f64", 1e-9), (64, 3, 8, "f64", 1e-9),
+                                            (256, 1, 16, "f32", 1e-4), (256, 5, 8, "f32", 1e-4),
+                                            (24, 3, 0, "f64", 1e-9)])
+def test_ilt_step_vs_oracle(ctx, n, F, K, prec, tol):
+    rng = np.random.default_rng(7 * n + F)
+    pitch = 4.0 if n == 24 else 1.0
+    foci = [-40.0, -20.0, 0.0, 20.0, 40.0][:F] if F == 5 else ([-40.0, 0.0, 40.0][:F] if F == 3 else [0.0])
+    ks = kernels_for(n, pitch, foci, k=K, grid_n=7 if n == 24 else 21)
+    target = (rng.random((n, n)) > 0.5).astype(np.float64)
+    theta0 = rng.standard_normal((n, n)) * 0.5
+    prm = L.IltParams(mask_steepness=4.0, resist_beta=30.0, threshold=0.25, resist_sigma_nm=2.0,
+                      dose=1.0, step=0.05, focus_weights=[1.0 / F] * F)
+    solver = L.IltSolver(ks, prm, 1, prec, ctx)
+    solver.set_tiles(target[None], theta0[None])
+    cost = solver.run(1)
+    theta_gpu, _ = solver.get_tiles()
+    th = theta0.copy()
+    c_ref, g_ref = O.ilt_iteration(th, target, ks.weights, ks.support, ks.values, [1.0 / F] * F,
+                                   [4.0, 30.0, 0.25, 2.0, 1.0, 0.05], pitch)
+    assert abs(cost[0, 0] - c_ref) <= tol * abs(c_ref) * 10
+    # theta update = -step * grad: compare the gradients (rel L-inf on the step)
+    assert rel_linf(theta_gpu[0] - theta0, th - theta0) < tol * 10
+
+
+def test_rasterize_bit_exact_vs_reference(ctx):
+    rng = np.random.default_rng(5)
+    # random all-angle 8-vertex polygons (reference test_geometry.cpp:90-104), healed by the reference
+    for trial in range(6):
+        poly = [tuple(int(v) for v in rng.integers(5, 121, 2)) for _ in range(8)]
+        healed = R.heal([poly])
+        for (ox, oy, pitch, dbu) in [(0.0, 0.0, 1.0, 1.0), (-3.25, 1.5, 0.5, 2.0)]:
+            nx = ny = 300
+            want = R.rasterize([poly], nx, ny, pitch, ox, oy, dbu)
+            got = L.rasterize_layer(healed, L.Grid(nx, ny, pitch, ox, oy), dbu, ctx)
+            assert np.array_equal(got, want)
+
+
+def test_rasterize_known_answers(ctx):
+    """reference test_geometry.cpp:77-88."""
+    g = L.Grid(8, 8, 1.0)
+    r = L.rasterize_layer([[(2, 2), (6, 2), (6, 6), (2, 6)]], g, 1.0, ctx)
+    assert r[3, 3] == 1.0 and r[0, 0] == 0.0
+    r = L.rasterize_layer([[(0, 0), (9, 0), (9, 16), (0, 16)]], g, 2.0, ctx)
+    assert abs(r[3, 4] - 0.5) < 1e-12
+
+
+def test_threshold_semantics(ctx):
+    v = np.array([0.1, 0.25, 0.2500001, 0.3, 0.0])
+    out = L.threshold(v, 0.25, ctx)
+    assert out.tolist() == [0.0, 1.0, 1.0, 1.0, 0.0]
