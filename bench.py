@@ -1,0 +1,480 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native SOCS imaging / ILT hot path.
+
+Headline workload (BASELINE.json configs[1], "C2"): one 2048x2048 tile per
+GPU, K = 16 SOCS kernels, 1 focus plane, Gaussian-blur (sigma 2 nm) sigmoid
+resist, 50 ILT gradient iterations = one step.  Metric: ILT
+tile-iterations/s, whole job (weak scaling: one tile per rank, the global
+cost all-reduced over NCCL every iteration when N > 1).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+
+`value` is device-timed (CUDA events, inputs resident in HBM, L2 flushed
+between steps, max over ranks); `e2e` runs the same job through the public
+API from host buffers: polygon layout H2D -> GPU rasterization -> ILT -> mask
+D2H.  `--impl reference` times the reference's own CPU implementation
+(oracle/_ref: the unmodified reference sources, all host threads) on the
+same config.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (tile N, K, foci, iterations per step, description)
+    "c1": (1024, 8, [0.0], 0, "C1: single 1024x1024 tile forward aerial image + threshold resist, K=8, F=1"),
+    "c2": (2048, 16, [0.0], 50, "C2: 2048x2048 tile ILT, K=16, F=1, 50 iterations, Gaussian-blur resist"),
+    "c3": (2048, 16, [-40.0, -20.0, 0.0, 20.0, 40.0], 50, "C3: through-focus ILT 2048x2048, K=16, F=5"),
+    "c4": (4096, 32, [-40.0, 0.0, 40.0], 50, "C4: curvilinear ILT 4096x4096, K=32, F=3"),
+}
+ILT = dict(mask_steepness=4.0, resist_beta=30.0, threshold=0.25, resist_sigma_nm=2.0, dose=1.0, step=0.5)
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def make_problem(cfg_name, rank):
+    import paper_2602_15036_b200 as L
+    from paper_2602_15036_b200 import layouts as LY
+    N, K, foci, iters, desc = CONFIGS[cfg_name]
+    grid = L.Grid(N, N, 1.0, 0.0, 0.0)
+    gen = LY.curvilinear if cfg_name == "c4" else LY.line_space_contacts
+    polys = gen(N, N, seed=1000 + rank)
+    model = L.OpticalModel(source=L.make_annular_source(0.4, 0.8, 21))
+    ks = L.build_socs_kernels(model, grid, foci, k_fixed=K)
+    return grid, polys, ks, iters, desc
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 7:
+                rows.append(f)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = max(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        load = [v for v in sm if v > 0.5 * mx] or sm
+        return {"sm_mhz": float(np.median(load)), "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic model (implemented decimated-band algorithm)
+# ---------------------------------------------------------------------------
+def fft_flops(L):
+    return 5.0 * L * math.log2(L)
+
+
+def kernel_model(geo, F, K):
+    """Per-launch FFT flops and algorithmic HBM bytes of each kernel of one
+    ILT iteration on one tile (5 L log2 L per length-L complex transform)."""
+    Nx = Ny = geo["N"]
+    n = geo["n"]
+    B = geo["B"]
+    P = 2 * (B - 1) if False else B - 1  # intensity half extent
+    Pm = (B - 1) // 2
+    c = 8  # complex64 bytes
+    m = {}
+    m["mask_cols"] = ((Pm + 1) * fft_flops(Ny), (Pm + 1) * Ny * c + B * B * c)
+    m["socs_cols"] = (F * K * B * fft_flops(n), F * K * (B * B * c + n * B * c))
+    m["socs_rows"] = (F * n * (K + 1) * fft_flops(n), F * (K * n * B * c + (P + 1) * n * c))
+    m["isub_cols"] = (F * (P + 1) * (fft_flops(n) + fft_flops(Ny)), F * ((P + 1) * n * c + Ny * (P + 1) * c))
+    fp = (F + 1) // 2
+    m["resist_rows"] = (fp * Ny * 2 * fft_flops(Nx), F * Ny * (P + 1) * c * 2 + Nx * Ny * 4 * fp)
+    m["wlp_cols"] = (F * (P + 1) * (fft_flops(Ny) + fft_flops(n)), F * ((P + 1) * Ny * c + n * (P + 1) * c))
+    m["adj_rows"] = (F * n * (1 + 2 * K) * fft_flops(n), F * (n * (P + 1) * c + 2 * K * n * B * c))
+    m["adj_cols"] = (F * K * B * fft_flops(n), F * K * (B * n * c + B * B * c))
+    m["grad_cols"] = ((Pm + 1) * fft_flops(Ny), B * B * c + Ny * (Pm + 1) * c)
+    m["grad_rows"] = ((Ny // 2) * 2 * fft_flops(Nx), Ny * (Pm + 1) * c + Nx * Ny * 4 * 2 + (Pm + 1) * Ny * c)
+    return m
+
+
+def run_ours(args, world, rank, local):
+    import torch
+    import paper_2602_15036_b200 as L
+    from paper_2602_15036_b200 import layouts as LY
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream()
+    ctx = L.Context(local)
+    ctx.set_stream(stream.cuda_stream)
+
+    grid, polys, ks, iters, desc = make_problem(args.config, rank)
+    N = grid.nx
+    F, K = ks.weights.shape
+    dk = L.DeviceKernels(ks, "f32", ctx)
+    info = dk.info()
+    xy, starts = LY.polygon_arrays(polys)
+
+    # device-resident inputs: target raster (GPU rasterizer) and theta0
+    target = torch.empty((1, N, N), dtype=torch.float64, device=dev)
+    _raster_to(ctx, grid, xy, starts, target)
+    target32 = target.float()
+    theta0 = ((2 * target32 - 1) * (2.0 / ILT["mask_steepness"])).contiguous()
+    prm = L.IltParams(focus_weights=[1.0 / F] * F, **ILT)
+    solver = L.IltSolver(dk, prm, 1, "f32", ctx)
+    cost_dev = torch.zeros((iters, 1), dtype=torch.float64, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        solver.set_tiles(target32, theta0)
+        if world > 1:
+            import torch.distributed as dist
+            for it in range(iters):
+                solver.run_device(1, cost_dev[it])
+                dist.all_reduce(cost_dev[it])  # global ILT cost (sum over tiles / ranks)
+        else:
+            solver.run_device(iters, cost_dev)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier(device_ids=[local])
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    times = []
+    l0 = ctx.launch_count()
+    for _ in range(args.steps):
+        flush.fill_(1.0)  # L2 flush between steps (not timed)
+        barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    launches = ctx.launch_count() - l0
+    clk = clocks.stop()
+    total_ms = float(np.sum(times))
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * iters / (ms_per_step / 1e3)  # tile-iterations/s, whole job
+    final_cost = cost_dev[:, 0].cpu().numpy()
+
+    # ---- per-kernel CUDA-event profile (separate instrumented steps) ----
+    ctx.set_profiling(True)
+    ctx.profile_report(reset=True)
+    nprof = 2
+    for _ in range(nprof):
+        step()
+    torch.cuda.synchronize()
+    prof = ctx.profile_report(reset=True)
+    ctx.set_profiling(False)
+    peak_fp32 = ctx.fp32_peak_tflops()
+    geo = {"N": N, "n": info["nx_sub"], "B": info["band_x"]}
+    model = kernel_model(geo, F, K)
+    kernel_ms = {k: v[1] / v[0] for k, v in prof.items()}
+    top = max(prof, key=lambda k: prof[k][1])
+    top_flops, top_bytes = model.get(top, (0.0, 0.0))
+    top_ms = kernel_ms[top]
+    achieved = top_flops / (top_ms * 1e-3) / 1e12
+    iter_ms_prof = sum(v[1] for v in prof.values()) / (nprof * iters)
+    shares = {k: round(v[1] / sum(x[1] for x in prof.values()), 4) for k, v in prof.items()}
+
+    # ---- end to end through the public API from host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        mask_host = torch.empty((1, N, N), dtype=torch.float32).pin_memory()
+        cost_host = torch.empty((iters, 1), dtype=torch.float64).pin_memory()
+        xy_pin = torch.from_numpy(xy).pin_memory()
+        st_pin = torch.from_numpy(starts).pin_memory()
+        tgt_dev = torch.empty((1, N, N), dtype=torch.float64, device=dev)
+
+        def e2e_step():
+            _raster_to(ctx, grid, xy_pin.numpy(), st_pin.numpy(), tgt_dev)  # H2D polygons + GPU raster
+            solver.set_tiles(tgt_dev)                                         # theta0 from target
+            if world > 1:
+                import torch.distributed as dist
+                for it in range(iters):
+                    solver.run_device(1, cost_dev[it])
+                    dist.all_reduce(cost_dev[it])
+            else:
+                solver.run_device(iters, cost_dev)
+            cost_host.copy_(cost_dev, non_blocking=True)
+            _get_mask(solver, mask_host)                                      # D2H final mask
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        torch.cuda.synchronize()
+        et = []
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            e2e_step()
+            torch.cuda.synchronize()
+            et.append((time.perf_counter() - t0) * 1e3)
+        e_ms = float(np.sum(et))
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e_ms /= args.steps
+        e2e = {"value": world * iters / (e_ms / 1e3), "unit": "tile-iter/s",
+               "h2d_bytes_per_step": int(xy.nbytes + starts.nbytes),
+               "d2h_bytes_per_step": int(mask_host.numel() * 4 + cost_host.numel() * 8),
+               "ms_per_step": e_ms, "timer": "host perf_counter with device sync on both sides"}
+
+    # ---- secondary: C1 forward aerial-image throughput (Mpixel/s) ----
+    aerial = None
+    if rank == 0:
+        aerial = _c1_forward(ctx, stream)
+
+    result = None
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            cpu = _cpu_baseline(args.config)
+        result = {
+            "metric": f"ILT tile-iterations/s ({desc})",
+            "value": value,
+            "unit": "tile-iter/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_per_step,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic (seeded line/space+contact layout, GPU-rasterized; Abbe-SVD SOCS kernels)",
+            "config": {"workload": desc, "tile": N, "K": K, "F": F, "iterations_per_step": iters,
+                       "tiles_per_gpu": 1, "decimated_grid": info["nx_sub"], "kernel_band": info["band_x"],
+                       "ilt": ILT, "l2": "flushed between steps (256 MiB write, untimed)",
+                       "parallelism": f"tiles sharded over {world} rank(s), NCCL all-reduce of cost per iteration"},
+            "roofline": {"bound": "fp32", "kernel": top, "achieved": achieved, "peak": peak_fp32,
+                         "unit": "TFLOP/s", "frac": achieved / peak_fp32 if peak_fp32 else None,
+                         "traffic": None,
+                         "peak_source": "measured on-box FFMA microbenchmark (lithogpu_fp32_peak)",
+                         "flops_per_launch": top_flops, "algorithmic_bytes_per_launch": top_bytes,
+                         "kernel_ms": top_ms,
+                         "hbm_gbs_algorithmic": top_bytes / (top_ms * 1e-3) / 1e9,
+                         "hbm_peak_gbs": _peaks().get("hbm_gbs"),
+                         "kernel_share": shares, "kernel_ms_avg": kernel_ms,
+                         "instrumented_iter_ms": iter_ms_prof},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "final_cost": [float(final_cost[0]), float(final_cost[-1])] if len(final_cost) else None,
+            "aerial_c1": aerial,
+        }
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+    return result
+
+
+def _raster_to(ctx, grid, xy, starts, out_dev):
+    import ctypes as C
+    from paper_2602_15036_b200._lib import check, lib
+    g = grid.c()
+    check(lib().lithogpu_rasterize(ctx.handle, C.byref(g), xy.ctypes.data, starts.ctypes.data,
+                                   len(starts) - 1, 1.0, out_dev.data_ptr()))
+
+
+def _get_mask(solver, mask_host):
+    from paper_2602_15036_b200._lib import F32, check, lib
+    check(lib().lithogpu_ilt_get_tiles(solver._h, None, mask_host.data_ptr(), F32))
+
+
+def _c1_forward(ctx, stream):
+    """C1 (configs[0]): 1024^2 tile, K=8, forward aerial + blur + threshold;
+    device-resident, CUDA-event timed.  Mpixel/s."""
+    import torch
+    import paper_2602_15036_b200 as L
+    from paper_2602_15036_b200 import layouts as LY
+    grid, polys, ks, _, desc = make_problem("c1", 0)
+    dk = L.DeviceKernels(ks, "f32", ctx)
+    xy, starts = LY.polygon_arrays(polys)
+    dev = torch.device("cuda", ctx.device)
+    mask = torch.empty((grid.ny, grid.nx), dtype=torch.float64, device=dev)
+    _raster_to(ctx, grid, xy, starts, mask)
+    m32 = mask.float()
+    for _ in range(3):
+        dk.image(m32, sigma_nm=2.0, threshold=0.25, want=("intensity", "resist", "print"))
+    torch.cuda.synchronize()
+    reps = 50
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        dk.image(m32, sigma_nm=2.0, threshold=0.25, want=("intensity", "resist", "print"))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    return {"workload": desc, "ms_per_image": ms, "mpix_s": grid.nx * grid.ny / (ms * 1e-3) / 1e6,
+            "outputs": "aerial f32 + resist f32 + print u8", "l2": "warm (repeated image)"}
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def _ref_problem(cfg_name):
+    import paper_2602_15036_b200 as L
+    grid, polys, ks, iters, desc = make_problem(cfg_name, 0)
+    from oracle import refpy as R
+    target = R.rasterize(polys, grid.nx, grid.ny, grid.pitch_nm, grid.origin_x_nm, grid.origin_y_nm, 1.0)
+    return grid, ks, target, iters, desc
+
+
+def _cpu_baseline(cfg_name, n_iter=2):
+    """Reference CPU implementation (oracle/_ref) on a bounded sample."""
+    from oracle import refpy as R
+    if not R.available():
+        return {"value": None, "unit": "tile-iter/s", "cores": 0, "kind": "reference",
+                "sample": "unavailable: oracle/_ref not built"}
+    grid, ks, target, iters, desc = _ref_problem(cfg_name)
+    cores = os.cpu_count() or 1
+    R.set_threads(cores)
+    theta = ((2 * target - 1) * (2.0 / ILT["mask_steepness"])).copy()
+    F = ks.weights.shape[0]
+    prm = [ILT["mask_steepness"], ILT["resist_beta"], ILT["threshold"], ILT["resist_sigma_nm"], ILT["dose"],
+           ILT["step"]]
+    t0 = time.perf_counter()
+    for _ in range(n_iter):
+        R.ilt_iteration(theta, target, ks.weights, ks.support, ks.values, [1.0 / F] * F, prm, grid.pitch_nm)
+    dt = time.perf_counter() - t0
+    return {"value": n_iter / dt, "unit": "tile-iter/s", "cores": cores, "kind": "reference",
+            "sample": f"{n_iter} ILT iterations of the {grid.nx}x{grid.ny} tile (K={ks.weights.shape[1]}, F={F}) "
+                      f"through the unmodified reference image_socs/gaussian_blur/fft2 (fp64, FFT shim, "
+                      f"{cores} OpenMP threads), {dt:.1f} s"}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return None
+    from oracle import refpy as R
+    if not R.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libref_litho.so not built"}))
+        return None
+    grid, ks, target, iters, desc = _ref_problem(args.config)
+    cores = os.cpu_count() or 1
+    R.set_threads(cores)
+    F = ks.weights.shape[0]
+    prm = [ILT["mask_steepness"], ILT["resist_beta"], ILT["threshold"], ILT["resist_sigma_nm"], ILT["dose"],
+           ILT["step"]]
+    theta = ((2 * target - 1) * (2.0 / ILT["mask_steepness"])).copy()
+
+    def step():  # bounded sample: one ILT iteration of the tile per step
+        R.ilt_iteration(theta, target, ks.weights, ks.support, ks.values, [1.0 / F] * F, prm, grid.pitch_nm)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    ms = dt / args.steps * 1e3
+    value = 1.0 / (ms / 1e3)
+    res = {"impl": "reference", "metric": f"ILT tile-iterations/s ({desc})", "value": value,
+           "unit": "tile-iter/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f64", "data": "synthetic (same seeded layout and kernels as the GPU arm)",
+           "config": {"workload": desc, "tile": grid.nx, "K": int(ks.weights.shape[1]), "F": F,
+                      "iterations_per_step": 1, "note": "one ILT iteration per step (bounded CPU sample)"},
+           "cpu_baseline": {"value": value, "unit": "tile-iter/s", "cores": cores, "kind": "reference",
+                            "sample": "1 ILT iteration per step of the same tile, unmodified reference "
+                                      "sources (oracle/_ref), OpenMP FFT shim"},
+           "e2e": {"value": value, "unit": "tile-iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(res), flush=True)
+    return res
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -60,6 +60,14 @@ lithogpu_status lithogpu_ctx_synchronize(lithogpu_ctx* ctx);
 /* number of kernels this context launched so far (instrumentation) */
 long long lithogpu_ctx_launch_count(const lithogpu_ctx* ctx);
 
+/* Per-launch CUDA-event timing of every kernel this context launches
+ * (instrumentation for the roofline; adds one event pair per launch). */
+lithogpu_status lithogpu_ctx_set_profiling(lithogpu_ctx* ctx, int on);
+/* "name count total_ms" lines, aggregated since the last reset */
+lithogpu_status lithogpu_ctx_profile_report(lithogpu_ctx* ctx, char* buf, size_t len, int reset);
+/* FFMA-pipe peak of the context's GPU, TFLOP/s (microbenchmark, ~1 ms) */
+lithogpu_status lithogpu_fp32_peak(lithogpu_ctx* ctx, double* tflops);
+
 /* ---- rasterization ------------------------------------------------------
  * Exact area-weighted coverage in fp64, bit-exact with the reference
  * rasterize_layer (raster.cpp:53-95) on a HEALED layer: polygons must be the

@@ -47,6 +47,9 @@ _SIGS = {
     "lithogpu_ctx_set_stream": (C.c_int, [_vp, _vp]),
     "lithogpu_ctx_synchronize": (C.c_int, [_vp]),
     "lithogpu_ctx_launch_count": (C.c_longlong, [_vp]),
+    "lithogpu_ctx_set_profiling": (C.c_int, [_vp, C.c_int]),
+    "lithogpu_ctx_profile_report": (C.c_int, [_vp, C.c_char_p, C.c_size_t, C.c_int]),
+    "lithogpu_fp32_peak": (C.c_int, [_vp, C.POINTER(C.c_double)]),
     "lithogpu_rasterize": (C.c_int, [_vp, C.POINTER(Grid), _vp, _vp, C.c_int, C.c_double, _vp]),
     "lithogpu_kernels_create": (C.c_int, [_vp, C.POINTER(Grid), C.c_int, C.c_int, C.c_int, _vp,
                                           C.c_int, _vp, _vp, C.POINTER(_vp)]),

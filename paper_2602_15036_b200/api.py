@@ -200,6 +200,24 @@ class Context:
     def launch_count(self) -> int:
         return int(lib().lithogpu_ctx_launch_count(self._h))
 
+    def set_profiling(self, on: bool) -> None:
+        check(lib().lithogpu_ctx_set_profiling(self._h, int(bool(on))))
+
+    def profile_report(self, reset: bool = True) -> dict:
+        """{kernel name: (launches, total ms)} from per-launch CUDA events."""
+        buf = C.create_string_buffer(1 << 16)
+        check(lib().lithogpu_ctx_profile_report(self._h, buf, len(buf), int(reset)))
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, n, ms = line.split()
+            out[name] = (int(n), float(ms))
+        return out
+
+    def fp32_peak_tflops(self) -> float:
+        v = C.c_double()
+        check(lib().lithogpu_fp32_peak(self._h, C.byref(v)))
+        return v.value
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             lib().lithogpu_ctx_destroy(self._h)

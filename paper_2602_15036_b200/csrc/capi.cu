@@ -114,6 +114,61 @@ struct lithogpu_ctx {
   std::vector<std::unique_ptr<DevBuf>> scratch;  // staging pool (per call slots)
   DevBuf raster_tmp;
   std::unordered_map<const void*, int> smem_set;
+  // optional per-launch CUDA-event timing (lithogpu_ctx_set_profiling)
+  bool profiling = false;
+  struct Rec {
+    const char* name;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  struct Agg {
+    long long n = 0;
+    double ms = 0;
+  };
+  std::unordered_map<std::string, Agg> agg;
+
+  cudaEvent_t ev() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    LG_CUDA(cudaEventCreate(&e));
+    return e;
+  }
+  void prof_begin(const char* name) {
+    if (!profiling) return;
+    Rec r{name, ev(), ev()};
+    LG_CUDA(cudaEventRecord(r.a, stream));
+    recs.push_back(r);
+  }
+  void prof_end() {
+    if (!profiling || recs.empty()) return;
+    LG_CUDA(cudaEventRecord(recs.back().b, stream));
+  }
+  void prof_collect() {
+    if (recs.empty()) return;
+    LG_CUDA(cudaStreamSynchronize(stream));
+    for (auto& r : recs) {
+      float ms = 0;
+      LG_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+      Agg& g = agg[r.name];
+      g.n++;
+      g.ms += ms;
+      pool.push_back(r.a);
+      pool.push_back(r.b);
+    }
+    recs.clear();
+  }
+  ~lithogpu_ctx() {
+    for (auto& r : recs) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    for (auto e : pool) cudaEventDestroy(e);
+  }
 
   DevBuf& slot(size_t i) {
     while (scratch.size() <= i) scratch.emplace_back(new DevBuf);
@@ -349,6 +404,9 @@ struct Plan : PlanBase {
   // work buffers (sized for `cap` tiles)
   int cap = 0;
   DevBuf Mr, Mhat, Tb, Ir, Ic, Rc, Dr, Wc, U, Acc, Gc, costrow, gmaxrow;
+  // the ILT whose next-iteration mask rows currently sit in Mr (fused into
+  // grad_rows); any other producer of Mr clears it
+  const void* mr_owner = nullptr;
   long long s_Mr, s_Mhat, s_T, s_Ir, s_C, s_Dr, s_Wc, s_U, s_Acc, s_Gc, s_cr, s_gm;
 
   Plan(lithogpu_ctx* c, const lithogpu_grid& gr, int F_, int K_, const double* weights, int S,
@@ -468,9 +526,11 @@ struct Plan : PlanBase {
   }
 
   template <typename Kern, typename... Args>
-  void go(Kern kern, const Launch& l, dim3 grd, Args... args) {
+  void go(const char* name, Kern kern, const Launch& l, dim3 grd, Args... args) {
     ctx->smem_attr(kern, l.smem);
+    ctx->prof_begin(name);
     kern<<<grd, l.block, l.smem, ctx->stream>>>(args...);
+    ctx->prof_end();
     ctx->check_launch();
   }
 
@@ -480,49 +540,49 @@ struct Plan : PlanBase {
   void real_rows_fwd(const T* src, long long src_ts, T steep, int Pout, C* out, long long out_ts,
                      int tiles) {
     const Launch l = launch_cfg<T>(g.ax.N, 0);
-    go(lg::k_real_rows_fwd<T, MODE>, l, dim3(cdiv((g.ay.N + 1) / 2, l.RPC), 1, tiles), g, src,
+    go("real_rows_fwd", lg::k_real_rows_fwd<T, MODE>, l, dim3(cdiv((g.ay.N + 1) / 2, l.RPC), 1, tiles), g, src,
        src_ts, steep, Pout, out, out_ts);
   }
   void mask_cols(int tiles) {
     const Launch l = launch_cfg<T>(g.ay.N, 0);
-    go(lg::k_mask_cols<T>, l, dim3(cdiv(g.ax.Pm + 1, l.RPC), 1, tiles), g, Mr.as<C>(), s_Mr,
+    go("mask_cols", lg::k_mask_cols<T>, l, dim3(cdiv(g.ax.Pm + 1, l.RPC), 1, tiles), g, Mr.as<C>(), s_Mr,
        Mhat.as<C>(), s_Mhat);
   }
   void socs_cols(int tiles) {
     const Launch l = launch_cfg<T>(g.ay.n, 0);
-    go(lg::k_socs_cols<T>, l, dim3(cdiv(g.ax.B, l.RPC), F * K, tiles), g, Mhat.as<C>(), s_Mhat,
+    go("socs_cols", lg::k_socs_cols<T>, l, dim3(cdiv(g.ax.B, l.RPC), F * K, tiles), g, Mhat.as<C>(), s_Mhat,
        H.as<C>(), Tb.as<C>(), s_T);
   }
   void socs_rows(T dose, int tiles) {
     const Launch l = launch_cfg<T>(g.ax.n, 0);
-    go(lg::k_socs_rows<T>, l, dim3(cdiv(g.ay.n, l.RPC), F, tiles), g, Tb.as<C>(), s_T,
+    go("socs_rows", lg::k_socs_rows<T>, l, dim3(cdiv(g.ay.n, l.RPC), F, tiles), g, Tb.as<C>(), s_T,
        wk.as<T>(), dose, Ir.as<C>(), s_Ir, static_cast<T*>(nullptr), 0LL);
   }
   void isub_cols(bool want_i, bool want_r, int tiles) {
     const Launch l = launch_cfg<T>(g.ay.n, g.ay.N);
     const dim3 grd(cdiv(g.ax.P + 1, l.RPC), F, tiles);
     if (want_i && want_r)
-      go(lg::k_isub_cols<T, true, true>, l, grd, g, Ir.as<C>(), s_Ir, gxh.as<T>(), gyb.as<T>(),
+      go("isub_cols", lg::k_isub_cols<T, true, true>, l, grd, g, Ir.as<C>(), s_Ir, gxh.as<T>(), gyb.as<T>(),
          Ic.as<C>(), Rc.as<C>(), s_C);
     else if (want_i)
-      go(lg::k_isub_cols<T, true, false>, l, grd, g, Ir.as<C>(), s_Ir, gxh.as<T>(), gyb.as<T>(),
+      go("isub_cols", lg::k_isub_cols<T, true, false>, l, grd, g, Ir.as<C>(), s_Ir, gxh.as<T>(), gyb.as<T>(),
          Ic.as<C>(), Rc.as<C>(), s_C);
     else
-      go(lg::k_isub_cols<T, false, true>, l, grd, g, Ir.as<C>(), s_Ir, gxh.as<T>(), gyb.as<T>(),
+      go("isub_cols", lg::k_isub_cols<T, false, true>, l, grd, g, Ir.as<C>(), s_Ir, gxh.as<T>(), gyb.as<T>(),
          Ic.as<C>(), Rc.as<C>(), s_C);
   }
   template <typename OutT>
   void out_rows(bool want_i, bool want_r, OutT* I, OutT* R, unsigned char* pr, long long o_ts,
                 T thr, int tiles) {
     const Launch l = launch_cfg<T>(g.ax.N, 0);
-    go(lg::k_out_rows<T, OutT>, l, dim3(cdiv(g.ay.N, l.RPC), F, tiles), g,
+    go("out_rows", lg::k_out_rows<T, OutT>, l, dim3(cdiv(g.ay.N, l.RPC), F, tiles), g,
        want_i ? static_cast<const C*>(Ic.as<C>()) : nullptr,
        want_r ? static_cast<const C*>(Rc.as<C>()) : nullptr, s_C, I, R, pr, o_ts, thr);
   }
   void resist_rows(const T* target, long long tg_ts, const T* cf, T beta, T thr, int tiles,
                    T* zout = nullptr, long long z_ts = 0) {
     const Launch l = launch_cfg<T>(g.ax.N, 0);
-    go(lg::k_resist_rows<T>, l, dim3(cdiv(g.ay.N, l.RPC), (F + 1) / 2, tiles), g, Rc.as<C>(),
+    go("resist_rows", lg::k_resist_rows<T>, l, dim3(cdiv(g.ay.N, l.RPC), (F + 1) / 2, tiles), g, Rc.as<C>(),
        s_C, target, tg_ts, cf, beta, thr, Dr.as<C>(), s_Dr, costrow.as<double>(), s_cr, zout,
        z_ts);
   }
@@ -530,28 +590,28 @@ struct Plan : PlanBase {
     const Launch l = launch_cfg<T>(g.ay.N, g.ay.n);
     const dim3 grd(cdiv(g.ax.P + 1, l.RPC), nf, tiles);
     if (gauss)
-      go(lg::k_wlp_cols<T, true>, l, grd, g, Dr.as<C>(), s_Dr, gxh.as<T>(), gyb.as<T>(),
+      go("wlp_cols", lg::k_wlp_cols<T, true>, l, grd, g, Dr.as<C>(), s_Dr, gxh.as<T>(), gyb.as<T>(),
          Wc.as<C>(), s_Wc);
     else
-      go(lg::k_wlp_cols<T, false>, l, grd, g, Dr.as<C>(), s_Dr, gxh.as<T>(), gyb.as<T>(),
+      go("wlp_cols", lg::k_wlp_cols<T, false>, l, grd, g, Dr.as<C>(), s_Dr, gxh.as<T>(), gyb.as<T>(),
          Wc.as<C>(), s_Wc);
   }
   void adj_rows(bool uniform, int nf, int tiles) {
     const Launch l = launch_cfg<T>(g.ax.n, 0);
     const dim3 grd(cdiv(g.ay.n, l.RPC), nf, tiles);
     if (uniform)
-      go(lg::k_adj_rows<T, true>, l, grd, g, Tb.as<C>(), s_T, Wc.as<C>(), s_Wc, U.as<C>(), s_U);
+      go("adj_rows", lg::k_adj_rows<T, true>, l, grd, g, Tb.as<C>(), s_T, Wc.as<C>(), s_Wc, U.as<C>(), s_U);
     else
-      go(lg::k_adj_rows<T, false>, l, grd, g, Tb.as<C>(), s_T, Wc.as<C>(), s_Wc, U.as<C>(), s_U);
+      go("adj_rows", lg::k_adj_rows<T, false>, l, grd, g, Tb.as<C>(), s_T, Wc.as<C>(), s_Wc, U.as<C>(), s_U);
   }
   void adj_cols(T dose, int tiles) {
     const Launch l = launch_cfg<T>(g.ay.n, 0);
-    go(lg::k_adj_cols<T>, l, dim3(g.ax.B, 1, tiles), g, U.as<C>(), s_U, H.as<C>(), wk.as<T>(),
+    go("adj_cols", lg::k_adj_cols<T>, l, dim3(g.ax.B, 1, tiles), g, U.as<C>(), s_U, H.as<C>(), wk.as<T>(),
        dose, Acc.as<C>(), s_Acc);
   }
   void grad_cols(int tiles, bool with_cost, double* cost_out, long long co_ts) {
     const Launch l = launch_cfg<T>(g.ay.N, 0);
-    go(lg::k_grad_cols<T>, l, dim3(cdiv(g.ax.Pm + 1, l.RPC) + 1, 1, tiles), g, Acc.as<C>(),
+    go("grad_cols", lg::k_grad_cols<T>, l, dim3(cdiv(g.ax.Pm + 1, l.RPC) + 1, 1, tiles), g, Acc.as<C>(),
        s_Acc, Gc.as<C>(), s_Gc, static_cast<const double*>(costrow.as<double>()), s_cr,
        with_cost ? int(F * g.ay.N) : 0, with_cost ? cost_out : nullptr, co_ts);
   }
@@ -559,7 +619,7 @@ struct Plan : PlanBase {
   void grad_rows(OutT* grad, long long gr_ts, T* theta, long long th_ts, T steep, T step,
                  double* gm, int tiles) {
     const Launch l = launch_cfg<T>(g.ax.N, 0);
-    go(lg::k_grad_rows<T, ILT, OutT>, l, dim3(cdiv((g.ay.N + 1) / 2, l.RPC), 1, tiles), g,
+    go("grad_rows", lg::k_grad_rows<T, ILT, OutT>, l, dim3(cdiv((g.ay.N + 1) / 2, l.RPC), 1, tiles), g,
        Gc.as<C>(), s_Gc, grad, gr_ts, theta, th_ts, steep, step, Mr.as<C>(), s_Mr, gm, s_gm);
   }
 
@@ -567,6 +627,7 @@ struct Plan : PlanBase {
   // Forward images for focus stacks (all F computed; caller picks one).
   void forward(const T* mask, long long m_ts, int tiles, T dose, bool want_i, bool want_r) {
     reserve(tiles, false);
+    mr_owner = nullptr;
     real_rows_fwd<0>(mask, m_ts, T(0), g.ax.Pm, Mr.as<C>(), s_Mr, tiles);
     mask_cols(tiles);
     socs_cols(tiles);
@@ -576,6 +637,7 @@ struct Plan : PlanBase {
 
   void gradient(const T* mask, const T* W, T dose, T* grad) {
     reserve(1, true);
+    mr_owner = nullptr;
     real_rows_fwd<0>(mask, 0, T(0), g.ax.Pm, Mr.as<C>(), s_Mr, 1);
     mask_cols(1);
     socs_cols(1);
@@ -630,7 +692,12 @@ static void ilt_run_impl(lithogpu_ilt* ilt, int iters, double* cost_user, double
   const T a = T(prm.mask_steepness), step = T(prm.step), beta = T(prm.resist_beta),
           thr = T(prm.threshold), dose = T(prm.dose);
   // initial mask row pass (subsequent ones are fused into grad_rows)
-  P.template real_rows_fwd<1>(theta, NN, a, P.g.ax.Pm, P.Mr.template as<C>(), P.s_Mr, tiles);
+  if (!(ilt->primed && P.mr_owner == ilt))
+    P.template real_rows_fwd<1>(theta, NN, a, P.g.ax.Pm, P.Mr.template as<C>(), P.s_Mr, tiles);
+  if (iters > 0) {
+    ilt->primed = true;
+    P.mr_owner = ilt;
+  }
   for (int it = 0; it < iters; ++it) {
     P.mask_cols(tiles);
     P.socs_cols(tiles);
@@ -658,14 +725,17 @@ static void ilt_run_impl(lithogpu_ilt* ilt, int iters, double* cost_user, double
                                                      : cudaMemcpyDeviceToHost,
                             ctx->stream));
   }
+  bool host = false;
   if (gmax_user) {
     const size_t bytes = sizeof(double) * size_t(iters) * tiles;
+    const bool dev = is_device_ptr(gmax_user);
+    host |= !dev;
     LG_CUDA(cudaMemcpyAsync(gmax_user, ilt->gmax.p, bytes,
-                            is_device_ptr(gmax_user) ? cudaMemcpyDeviceToDevice
-                                                     : cudaMemcpyDeviceToHost,
-                            ctx->stream));
+                            dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->stream));
   }
-  LG_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (cost_user) host |= !is_device_ptr(cost_user);
+  // stream-ordered unless results go to host memory
+  if (host) LG_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
 // ============================================================================
@@ -720,6 +790,70 @@ lithogpu_status lithogpu_ctx_synchronize(lithogpu_ctx* ctx) {
 }
 
 long long lithogpu_ctx_launch_count(const lithogpu_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+lithogpu_status lithogpu_ctx_set_profiling(lithogpu_ctx* ctx, int on) {
+  if (!ctx) {
+    g_last_error = "lithogpu_ctx_set_profiling: null context";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    ctx->activate();
+    ctx->prof_collect();
+    ctx->profiling = on != 0;
+  });
+}
+
+lithogpu_status lithogpu_ctx_profile_report(lithogpu_ctx* ctx, char* buf, size_t len, int reset) {
+  if (!ctx || !buf || len == 0) {
+    g_last_error = "lithogpu_ctx_profile_report: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    ctx->activate();
+    ctx->prof_collect();
+    std::string out;
+    char line[256];
+    for (const auto& kv : ctx->agg) {
+      std::snprintf(line, sizeof line, "%s %lld %.9f\n", kv.first.c_str(), kv.second.n, kv.second.ms);
+      out += line;
+    }
+    std::snprintf(buf, len, "%s", out.c_str());
+    if (reset) ctx->agg.clear();
+  });
+}
+
+lithogpu_status lithogpu_fp32_peak(lithogpu_ctx* ctx, double* tflops) {
+  if (!ctx || !tflops) {
+    g_last_error = "lithogpu_fp32_peak: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    ctx->activate();
+    int dev = 0, sms = 0;
+    LG_CUDA(cudaGetDevice(&dev));
+    LG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    DevBuf o;
+    o.ensure(16);
+    cudaEvent_t a, b;
+    LG_CUDA(cudaEventCreate(&a));
+    LG_CUDA(cudaEventCreate(&b));
+    const int blocks = sms * 8, threads = 256, iters = 4096;
+    float best = 1e30f;
+    for (int rep = 0; rep < 4; ++rep) {
+      LG_CUDA(cudaEventRecord(a, ctx->stream));
+      lg::k_ffma_peak<<<blocks, threads, 0, ctx->stream>>>(o.as<float>(), iters, 0.999f, 0.001f);
+      LG_CUDA(cudaEventRecord(b, ctx->stream));
+      LG_CUDA(cudaEventSynchronize(b));
+      float ms = 0;
+      LG_CUDA(cudaEventElapsedTime(&ms, a, b));
+      if (rep > 0) best = std::min(best, ms);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    const double flops = 2.0 * 8 * 16 * double(iters) * blocks * threads;
+    *tflops = flops / (best * 1e-3) / 1e12;
+  });
+}
 
 lithogpu_status lithogpu_rasterize(lithogpu_ctx* ctx, const lithogpu_grid* grid, const int64_t* xy,
                                    const int64_t* poly_start, int n_poly, double dbu_per_nm,
@@ -1177,6 +1311,7 @@ lithogpu_status lithogpu_ilt_set_tile(lithogpu_ilt* ilt, int tile, const void* t
     if (tile < 0 || tile >= ilt->tiles) throw UsageError("lithogpu_ilt_set_tile: tile out of range");
     dtype_size(dtype);
     ilt->ks->ctx->activate();
+    ilt->primed = false;
     if (ilt->ks->precision == LITHOGPU_F32)
       ilt_set_impl<float>(ilt, tile, 1, target, theta0, dtype);
     else
@@ -1193,6 +1328,7 @@ lithogpu_status lithogpu_ilt_set_tiles(lithogpu_ilt* ilt, const void* target, co
   return guarded([&] {
     dtype_size(dtype);
     ilt->ks->ctx->activate();
+    ilt->primed = false;
     if (ilt->ks->precision == LITHOGPU_F32)
       ilt_set_impl<float>(ilt, 0, ilt->tiles, target, theta0, dtype);
     else

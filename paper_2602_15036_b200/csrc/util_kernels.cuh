@@ -75,4 +75,25 @@ __global__ void k_reduce_max(const double* __restrict__ rows, long long ts, int 
   if (threadIdx.x == 0) out[blockIdx.x] = m;
 }
 
+// FP32 FMA-pipe peak microbenchmark: 8 independent FFMA chains per thread.
+__global__ void k_ffma_peak(float* out, int iters, float b, float c) {
+  float a0 = threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5,
+        a6 = a0 + 6, a7 = a0 + 7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      a0 = fmaf(a0, b, c);
+      a1 = fmaf(a1, b, c);
+      a2 = fmaf(a2, b, c);
+      a3 = fmaf(a3, b, c);
+      a4 = fmaf(a4, b, c);
+      a5 = fmaf(a5, b, c);
+      a6 = fmaf(a6, b, c);
+      a7 = fmaf(a7, b, c);
+    }
+  }
+  const float r = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  if (r == 1234.5f) out[0] = r;  // keep the chains live
+}
+
 }  // namespace lg
