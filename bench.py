@@ -164,7 +164,8 @@ def run_ours(args, world, rank, local):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream(device=dev)  # non-default stream: ILT loop is graph-captured
+    torch.cuda.set_stream(stream)
     ctx = L.Context(local)
     ctx.set_stream(stream.cuda_stream)
 

@@ -18,10 +18,11 @@ OBJ = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU_SOURCES = ["csrc/capi.cu"]
+CU_SOURCES = ["csrc/capi.cu", "csrc/fast_rows.cu", "csrc/fast_cols.cu"]
 CPP_SOURCES = ["host/socs_kernels.cpp"]
 DEPS = ["csrc/fft.cuh", "csrc/geom.h", "csrc/socs_kernels.cuh", "csrc/raster_kernels.cuh",
-        "csrc/util_kernels.cuh", "../include/lithogpu.h"]
+        "csrc/util_kernels.cuh", "csrc/fftr.cuh", "csrc/socs_fast.h", "csrc/socs_fast.cuh",
+        "csrc/fast_common.cuh", "../include/lithogpu.h"]
 
 
 def _newer(target, sources):
@@ -55,7 +56,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if force or _newer(obj, [src, "../include/lithogpu.h"]):
             jobs.append(["g++", "-O2", "-std=c++17", "-fPIC", "-fopenmp", "-ffp-contract=off",
                          "-c", src, "-o", obj])
-    with ThreadPoolExecutor(max_workers=4) as ex:
+    with ThreadPoolExecutor(max_workers=8) as ex:
         for r in ex.map(_run, jobs):
             if verbose:
                 sys.stderr.write(r.stderr)

@@ -18,6 +18,9 @@
 #include "raster_kernels.cuh"
 #include "socs_kernels.cuh"
 #include "util_kernels.cuh"
+#include "socs_fast.h"
+#include <cstdlib>
+#include <type_traits>
 
 namespace {
 
@@ -296,6 +299,9 @@ struct OutStage {
 };
 
 // ---- geometry --------------------------------------------------------------
+// Decimation d: the largest divisor of N whose grid n = N/d still holds the
+// intensity band without aliasing (n >= 2P+1) and keeps n >= 32 (fast-path
+// transform range).  No such d -> full band on the N grid.
 lg::AxisGeom make_axis(int N, int lo, int hi) {
   lg::AxisGeom a{};
   a.N = N;
@@ -308,7 +314,7 @@ lg::AxisGeom make_axis(int N, int lo, int hi) {
   for (int d = N; d >= 1; --d) {
     if (N % d) continue;
     const int n = N / d;
-    if (n >= 2 * P0 + 1) {
+    if (n >= 2 * P0 + 1 && n >= std::min(N, 32)) {
       best = d;
       break;
     }
@@ -407,7 +413,13 @@ struct Plan : PlanBase {
   // the ILT whose next-iteration mask rows currently sit in Mr (fused into
   // grad_rows); any other producer of Mr clears it
   const void* mr_owner = nullptr;
+  long long gen = 0;  // bumped whenever work buffers are reallocated
   long long s_Mr, s_Mhat, s_T, s_Ir, s_C, s_Dr, s_Wc, s_U, s_Acc, s_Gc, s_cr, s_gm;
+  // fp32 fast path (power-of-two tiles, register FFT kernels of socs_fast.cuh)
+  bool fast = false;
+  lg::FGeo fg{};
+  DevBuf ftNx, ftNy, ftnx, ftny, Wsub, Ih, Rh, Wh;
+  long long s_Wsub = 0, s_band = 0;
 
   Plan(lithogpu_ctx* c, const lithogpu_grid& gr, int F_, int K_, const double* weights, int S,
        const int32_t* support, const double* values)
@@ -474,6 +486,45 @@ struct Plan : PlanBase {
     s_Gc = (long long)Ny * (ax.Pm + 1);
     s_cr = (long long)F * Ny;
     s_gm = (long long)(Ny + 1) / 2;
+    if constexpr (std::is_same<T, float>::value) {
+      auto ok = [](int L) { return lg::is_pow2(L) && lg::fast_log2_ok(lg::ilog2(L)); };
+      fast = ok(Nx) && ok(Ny) && ok(ax.n) && ok(ay.n) && !std::getenv("LITHOGPU_GENERIC");
+      if (fast) {
+        fg.ax = ax;
+        fg.ay = ay;
+        fg.F = F;
+        fg.K = K;
+        fg.lgNx = lg::ilog2(Nx);
+        fg.lgNy = lg::ilog2(Ny);
+        fg.lgnx = lg::ilog2(ax.n);
+        fg.lgny = lg::ilog2(ay.n);
+        auto table = [](int lgL, DevBuf& b) {
+          std::vector<lg::C32> h(std::max(1, lg::fast_tw_len(lgL)));
+          lg::fast_fill_twiddles(lgL, h.data());
+          b.ensure(h.size() * sizeof(lg::C32));
+          LG_CUDA(cudaMemcpy(b.p, h.data(), h.size() * sizeof(lg::C32), cudaMemcpyHostToDevice));
+          return b.as<lg::C32>();
+        };
+        fg.twNx = table(fg.lgNx, ftNx);
+        fg.twNy = table(fg.lgNy, ftNy);
+        fg.twnx = table(fg.lgnx, ftnx);
+        fg.twny = table(fg.lgny, ftny);
+        s_Wsub = (long long)F * ay.n * ax.n;
+        s_band = (long long)F * ay.nb2 * (ax.P + 1);
+        const long long npairs = (Ny + 1) / 2;
+        const long long wpg = std::max(1, lg::fast_tpr(fg.lgNx) / 32);
+        s_cr = std::max(s_cr, F * npairs * wpg);
+        s_gm = std::max(s_gm, npairs * wpg);
+      }
+    }
+  }
+
+  template <typename Fn>
+  void fl(const char* name, Fn&& fn) {
+    ctx->prof_begin(name);
+    fn();
+    ctx->prof_end();
+    ctx->check_launch();
   }
 
   void set_sigma(double sigma_nm) {
@@ -501,12 +552,21 @@ struct Plan : PlanBase {
 
   void reserve(int tiles, bool adjoint) {
     if (tiles > cap) {
+      ++gen;
       Mr.release(); Mhat.release(); Tb.release(); Ir.release(); Ic.release(); Rc.release();
       Dr.release(); Wc.release(); U.release(); Acc.release(); Gc.release();
       costrow.release(); gmaxrow.release();
       cap = tiles;
     }
     const size_t c = sizeof(C) * size_t(cap);
+    if (fast) {
+      Rh.ensure(c * s_band);
+      Ih.ensure(c * s_band);
+      if (adjoint) {
+        Wh.ensure(c * s_band);
+        Wsub.ensure(sizeof(T) * size_t(cap) * s_Wsub);
+      }
+    }
     Mr.ensure(c * s_Mr);
     Mhat.ensure(c * s_Mhat);
     Tb.ensure(c * s_T);
@@ -574,6 +634,15 @@ struct Plan : PlanBase {
   template <typename OutT>
   void out_rows(bool want_i, bool want_r, OutT* I, OutT* R, unsigned char* pr, long long o_ts,
                 T thr, int tiles) {
+    if constexpr (std::is_same<T, float>::value && std::is_same<OutT, float>::value) {
+      if (fast) {
+        fl("out_rows", [&] {
+          lg::fl_out_rows(fg, ctx->stream, tiles, want_i ? Ic.as<C>() : nullptr, want_r ? Rc.as<C>() : nullptr,
+                          s_C, I, R, pr, o_ts, thr);
+        });
+        return;
+      }
+    }
     const Launch l = launch_cfg<T>(g.ax.N, 0);
     go("out_rows", lg::k_out_rows<T, OutT>, l, dim3(cdiv(g.ay.N, l.RPC), F, tiles), g,
        want_i ? static_cast<const C*>(Ic.as<C>()) : nullptr,
@@ -628,6 +697,24 @@ struct Plan : PlanBase {
   void forward(const T* mask, long long m_ts, int tiles, T dose, bool want_i, bool want_r) {
     reserve(tiles, false);
     mr_owner = nullptr;
+    if constexpr (std::is_same<T, float>::value) {
+      if (fast) {
+        cudaStream_t s = ctx->stream;
+        fl("real_rows_fwd", [&] { lg::fl_real_rows_fwd(fg, s, tiles, 0, mask, m_ts, 0.f, g.ax.Pm, Mr.as<C>(), s_Mr); });
+        fl("mask_cols", [&] { lg::fl_mask_cols(fg, s, tiles, Mr.as<C>(), s_Mr, Mhat.as<C>(), s_Mhat); });
+        fl("socs_cols", [&] { lg::fl_socs_cols(fg, s, tiles, Mhat.as<C>(), s_Mhat, H.as<C>(), Tb.as<C>(), s_T); });
+        fl("socs_rows", [&] { lg::fl_socs_rows(fg, s, tiles, Tb.as<C>(), s_T, wk.as<T>(), dose, Ir.as<C>(), s_Ir); });
+        fl("isub_colfwd", [&] {
+          lg::fl_band_colfwd(fg, s, tiles, F, true, Ir.as<C>(), s_Ir, gxh.as<T>(), gyb.as<T>(),
+                             want_r ? Rh.as<C>() : nullptr, want_i ? Ih.as<C>() : nullptr, s_band);
+        });
+        if (want_i)
+          fl("isub_colinv", [&] { lg::fl_band_colinv(fg, s, tiles, F, false, Ih.as<C>(), s_band, Ic.as<C>(), s_C); });
+        if (want_r)
+          fl("isub_colinv", [&] { lg::fl_band_colinv(fg, s, tiles, F, false, Rh.as<C>(), s_band, Rc.as<C>(), s_C); });
+        return;
+      }
+    }
     real_rows_fwd<0>(mask, m_ts, T(0), g.ax.Pm, Mr.as<C>(), s_Mr, tiles);
     mask_cols(tiles);
     socs_cols(tiles);
@@ -638,6 +725,34 @@ struct Plan : PlanBase {
   void gradient(const T* mask, const T* W, T dose, T* grad) {
     reserve(1, true);
     mr_owner = nullptr;
+    if constexpr (std::is_same<T, float>::value) {
+      if (fast) {
+        cudaStream_t s = ctx->stream;
+        fl("real_rows_fwd", [&] { lg::fl_real_rows_fwd(fg, s, 1, 0, mask, 0, 0.f, g.ax.Pm, Mr.as<C>(), s_Mr); });
+        fl("mask_cols", [&] { lg::fl_mask_cols(fg, s, 1, Mr.as<C>(), s_Mr, Mhat.as<C>(), s_Mhat); });
+        fl("socs_cols", [&] { lg::fl_socs_cols(fg, s, 1, Mhat.as<C>(), s_Mhat, H.as<C>(), Tb.as<C>(), s_T); });
+        if (W) {
+          fl("real_rows_fwd", [&] { lg::fl_real_rows_fwd(fg, s, 1, 0, W, 0, 0.f, g.ax.P, Dr.as<C>(), s_Dr); });
+          fl("wlp_colfwd", [&] {
+            lg::fl_band_colfwd(fg, s, 1, 1, false, Dr.as<C>(), s_Dr, nullptr, nullptr, Wh.as<C>(), nullptr, s_band);
+          });
+          fl("wlp_colinv", [&] { lg::fl_band_colinv(fg, s, 1, 1, true, Wh.as<C>(), s_band, Wc.as<C>(), s_Wc); });
+          fl("wlp_rows", [&] { lg::fl_wlp_rows(fg, s, 1, 1, Wc.as<C>(), s_Wc, Wsub.as<T>(), s_Wsub); });
+        }
+        fl("adj_rows", [&] {
+          lg::fl_adj_rows(fg, s, 1, 1, W == nullptr, Tb.as<C>(), s_T, Wsub.as<T>(), s_Wsub, U.as<C>(), s_U);
+        });
+        fl("adj_cols", [&] { lg::fl_adj_cols(fg, s, 1, U.as<C>(), s_U, H.as<C>(), wk.as<T>(), dose, Acc.as<C>(), s_Acc); });
+        fl("grad_cols", [&] {
+          lg::fl_grad_cols(fg, s, 1, Acc.as<C>(), s_Acc, Gc.as<C>(), s_Gc, nullptr, 0, 0, nullptr, 0);
+        });
+        fl("grad_rows", [&] {
+          lg::fl_grad_rows(fg, s, 1, false, Gc.as<C>(), s_Gc, grad, 0, nullptr, 0, 0.f, 0.f, Mr.as<C>(), s_Mr,
+                           nullptr, 0);
+        });
+        return;
+      }
+    }
     real_rows_fwd<0>(mask, 0, T(0), g.ax.Pm, Mr.as<C>(), s_Mr, 1);
     mask_cols(1);
     socs_cols(1);
@@ -674,6 +789,32 @@ struct lithogpu_ilt {
   int tiles;
   DevBuf theta, target, cfd, cost, gmax;
   bool primed = false;
+  // captured launch sequences (see ilt_run_impl)
+  struct GraphKey {
+    int iters;
+    bool gmax, prime;
+    long long gen;
+    const void *cost, *gmaxp;
+    bool operator==(const GraphKey& o) const {
+      return iters == o.iters && gmax == o.gmax && prime == o.prime && gen == o.gen &&
+             cost == o.cost && gmaxp == o.gmaxp;
+    }
+  };
+  struct GraphEntry {
+    GraphKey key;
+    cudaGraphExec_t exec;
+    long long nk;  // kernels per replay
+  };
+  std::vector<GraphEntry> graphs;
+  std::vector<GraphKey> warm;
+  bool warm_key(const GraphKey& k) const {
+    for (const auto& w : warm)
+      if (w == k) return true;
+    return false;
+  }
+  ~lithogpu_ilt() {
+    for (auto& e : graphs) cudaGraphExecDestroy(e.exec);
+  }
 };
 
 template <typename T>
@@ -692,12 +833,68 @@ static void ilt_run_impl(lithogpu_ilt* ilt, int iters, double* cost_user, double
   const T a = T(prm.mask_steepness), step = T(prm.step), beta = T(prm.resist_beta),
           thr = T(prm.threshold), dose = T(prm.dose);
   // initial mask row pass (subsequent ones are fused into grad_rows)
-  if (!(ilt->primed && P.mr_owner == ilt))
-    P.template real_rows_fwd<1>(theta, NN, a, P.g.ax.Pm, P.Mr.template as<C>(), P.s_Mr, tiles);
+  const bool need_prime = !(ilt->primed && P.mr_owner == ilt);
   if (iters > 0) {
     ilt->primed = true;
     P.mr_owner = ilt;
   }
+  auto enqueue = [&]() {
+  if constexpr (std::is_same<T, float>::value) {
+    if (P.fast) {
+      cudaStream_t s = ctx->stream;
+      const lg::FGeo& fg = P.fg;
+      const int F = P.F;
+      if (need_prime)
+        P.fl("real_rows_fwd", [&] { lg::fl_real_rows_fwd(fg, s, tiles, 1, theta, NN, a, P.g.ax.Pm, P.Mr.template as<C>(), P.s_Mr); });
+      for (int it = 0; it < iters; ++it) {
+        P.fl("mask_cols", [&] { lg::fl_mask_cols(fg, s, tiles, P.Mr.template as<C>(), P.s_Mr, P.Mhat.template as<C>(), P.s_Mhat); });
+        P.fl("socs_cols", [&] { lg::fl_socs_cols(fg, s, tiles, P.Mhat.template as<C>(), P.s_Mhat, P.H.template as<C>(), P.Tb.template as<C>(), P.s_T); });
+        P.fl("socs_rows", [&] { lg::fl_socs_rows(fg, s, tiles, P.Tb.template as<C>(), P.s_T, P.wk.template as<T>(), dose, P.Ir.template as<C>(), P.s_Ir); });
+        P.fl("isub_colfwd", [&] {
+          lg::fl_band_colfwd(fg, s, tiles, F, true, P.Ir.template as<C>(), P.s_Ir, P.gxh.template as<T>(),
+                             P.gyb.template as<T>(), P.Rh.template as<C>(), nullptr, P.s_band);
+        });
+        P.fl("isub_colinv", [&] { lg::fl_band_colinv(fg, s, tiles, F, false, P.Rh.template as<C>(), P.s_band, P.Rc.template as<C>(), P.s_C); });
+        P.fl("resist_rows", [&] {
+          lg::fl_resist_rows(fg, s, tiles, P.Rc.template as<C>(), P.s_C, ilt->target.as<T>(), NN, ilt->cfd.as<T>(), beta, thr,
+                             P.Dr.template as<C>(), P.s_Dr, P.costrow.template as<double>(), P.s_cr);
+        });
+        P.fl("wlp_colfwd", [&] {
+          lg::fl_band_colfwd(fg, s, tiles, F, false, P.Dr.template as<C>(), P.s_Dr, P.gxh.template as<T>(),
+                             P.gyb.template as<T>(), P.Wh.template as<C>(), nullptr, P.s_band);
+        });
+        P.fl("wlp_colinv", [&] { lg::fl_band_colinv(fg, s, tiles, F, true, P.Wh.template as<C>(), P.s_band, P.Wc.template as<C>(), P.s_Wc); });
+        P.fl("wlp_rows", [&] { lg::fl_wlp_rows(fg, s, tiles, F, P.Wc.template as<C>(), P.s_Wc, P.Wsub.template as<T>(), P.s_Wsub); });
+        P.fl("adj_rows", [&] {
+          lg::fl_adj_rows(fg, s, tiles, F, false, P.Tb.template as<C>(), P.s_T, P.Wsub.template as<T>(), P.s_Wsub,
+                          P.U.template as<C>(), P.s_U);
+        });
+        P.fl("adj_cols", [&] {
+          lg::fl_adj_cols(fg, s, tiles, P.U.template as<C>(), P.s_U, P.H.template as<C>(), P.wk.template as<T>(), dose,
+                          P.Acc.template as<C>(), P.s_Acc);
+        });
+        const long long npairs = (P.g.ay.N + 1) / 2;
+        const int ncost = int(std::min<long long>(P.s_cr, F * npairs * std::max(1, lg::fast_tpr(fg.lgNx) / 32)));
+        P.fl("grad_cols", [&] {
+          lg::fl_grad_cols(fg, s, tiles, P.Acc.template as<C>(), P.s_Acc, P.Gc.template as<C>(), P.s_Gc,
+                           P.costrow.template as<double>(), P.s_cr, ncost, ilt->cost.as<double>() + size_t(it) * tiles, 1);
+        });
+        P.fl("grad_rows", [&] {
+          lg::fl_grad_rows(fg, s, tiles, true, P.Gc.template as<C>(), P.s_Gc, nullptr, 0, theta, NN, a, step,
+                           P.Mr.template as<C>(), P.s_Mr, P.gmaxrow.template as<double>(), P.s_gm);
+        });
+        if (gmax_user) {
+          const int ngm = int(npairs * std::max(1, lg::fast_tpr(fg.lgNx) / 32));
+          lg::k_reduce_max<<<tiles, 32, 0, ctx->stream>>>(P.gmaxrow.template as<double>(), P.s_gm, ngm,
+                                                         ilt->gmax.as<double>() + size_t(it) * tiles);
+          ctx->check_launch();
+        }
+      }
+      return;
+    }
+  }
+  if (need_prime)
+    P.template real_rows_fwd<1>(theta, NN, a, P.g.ax.Pm, P.Mr.template as<C>(), P.s_Mr, tiles);
   for (int it = 0; it < iters; ++it) {
     P.mask_cols(tiles);
     P.socs_cols(tiles);
@@ -718,6 +915,49 @@ static void ilt_run_impl(lithogpu_ilt* ilt, int iters, double* cost_user, double
       ctx->check_launch();
     }
   }
+  };  // enqueue
+
+  // CUDA graph of the whole `iters`-iteration launch sequence: captured on the
+  // second call with an identical configuration, replayed afterwards.
+  const bool graphable = ctx->stream != nullptr && !ctx->profiling && iters > 0 &&
+                         !std::getenv("LITHOGPU_NO_GRAPH");
+  if (!graphable) {
+    enqueue();
+  } else {
+    const lithogpu_ilt::GraphKey key{iters, gmax_user != nullptr, need_prime, P.gen, ilt->cost.p,
+                                     ilt->gmax.p};
+    lithogpu_ilt::GraphEntry* hit = nullptr;
+    for (auto& e : ilt->graphs)
+      if (e.key == key) hit = &e;
+    if (!hit && ilt->warm_key(key)) {
+      const long long l0 = ctx->launches;
+      LG_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+      cudaGraph_t graph = nullptr;
+      try {
+        enqueue();
+      } catch (...) {
+        cudaStreamEndCapture(ctx->stream, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+      }
+      LG_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
+      cudaGraphExec_t exec = nullptr;
+      const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      LG_CUDA(ie);
+      ilt->graphs.push_back({key, exec, ctx->launches - l0});
+      ctx->launches = l0;
+      hit = &ilt->graphs.back();
+    }
+    if (hit) {
+      LG_CUDA(cudaGraphLaunch(hit->exec, ctx->stream));
+      ctx->launches += hit->nk;
+    } else {
+      enqueue();
+      ilt->warm.push_back(key);
+    }
+  }
+
   if (cost_user) {
     const size_t bytes = sizeof(double) * size_t(iters) * tiles;
     LG_CUDA(cudaMemcpyAsync(cost_user, ilt->cost.p, bytes,

@@ -67,6 +67,16 @@ __device__ __forceinline__ cx<double> ldg_cx(const cx<double>* p) {
   return mk(v.x, v.y);
 }
 
+// Hermitian split of a packed real pair: Z = FFT(a + i b) ->
+//   A(p) = (Z(p) + conj Z(-p))/2,  B(p) = (Z(p) - conj Z(-p))/(2i)
+template <typename T>
+__device__ __forceinline__ void split_pair(cx<T> X, cx<T> Ym, cx<T>& A, cx<T>& Bv) {
+  const cx<T> Yc = conjg(Ym);
+  A = scale(add(X, Yc), T(0.5));
+  const cx<T> D = sub(X, Yc);
+  Bv = mk(T(0.5) * D.y, T(-0.5) * D.x);
+}
+
 // a * (S * i)
 template <int S, typename T>
 __device__ __forceinline__ cx<T> mul_si(cx<T> a) {

@@ -1,0 +1,251 @@
+// Register-resident, compile-time-planned Stockham FFT (fp32 fast path).
+//
+// A row group of TPR = L/E threads transforms one length-L row.  Thread t
+// holds the row in the NATURAL distribution v[e] = x[t + e*TPR] (coalesced
+// global loads/stores, band gathers/scatters straight from registers).  The
+// first Stockham stage reads its butterflies from that distribution and the
+// last one writes its outputs back into it, so an S-stage plan needs only
+// S-1 shared-memory exchanges (float2, one pad per 16 elements: conflict free
+// for every plan below except L = 512, 1.25 wavefronts).
+// Stage twiddles come from per-stage tables laid out [r-1][k] (k fastest) so a
+// warp's twiddle loads are contiguous; they are issued before the exchange
+// barrier so their latency hides behind it.
+//
+// Conventions: reference fft2 (proj/src/core/imaging.cpp:17-31), SIGN -1
+// forward, +1 backward, unnormalized.
+#pragma once
+
+#include "fft.cuh"
+
+namespace lg {
+
+template <int LOG2>
+struct RPlan;
+
+#define LG_RPLAN(LG, EE, ...)                            \
+  template <>                                            \
+  struct RPlan<LG> {                                     \
+    static constexpr int L = 1 << LG;                    \
+    static constexpr int E = EE;                         \
+    static constexpr int TPR = L / EE;                   \
+    static constexpr int R[] = {__VA_ARGS__};            \
+    static constexpr int NS = sizeof(R) / sizeof(int);   \
+  };
+
+LG_RPLAN(5, 8, 8, 4)
+LG_RPLAN(6, 8, 8, 8)
+LG_RPLAN(7, 16, 16, 8)
+LG_RPLAN(8, 16, 16, 16)
+LG_RPLAN(9, 8, 8, 8, 8)
+LG_RPLAN(10, 16, 16, 8, 8)
+LG_RPLAN(11, 16, 16, 16, 8)
+LG_RPLAN(12, 16, 16, 16, 16)
+LG_RPLAN(13, 16, 16, 16, 16, 2)
+#undef LG_RPLAN
+
+template <int LOG2, int S>
+struct Stg {
+  static constexpr int R = RPlan<LOG2>::R[S];
+  static constexpr int Ns = Stg<LOG2, S - 1>::Ns * Stg<LOG2, S - 1>::R;
+  static constexpr int tw_off = Stg<LOG2, S - 1>::tw_off + Stg<LOG2, S - 1>::tw_len;
+  static constexpr int tw_len = (R - 1) * Ns;
+};
+template <int LOG2>
+struct Stg<LOG2, 0> {
+  static constexpr int R = RPlan<LOG2>::R[0];
+  static constexpr int Ns = 1;
+  static constexpr int tw_off = 0;
+  static constexpr int tw_len = 0;
+};
+
+template <int LOG2>
+struct TwLen {
+  static constexpr int value =
+      Stg<LOG2, RPlan<LOG2>::NS - 1>::tw_off + Stg<LOG2, RPlan<LOG2>::NS - 1>::tw_len;
+};
+
+// Shared-memory exchange layouts (policy): where element i of a row lives.
+//   Xch2<SW>: one float2 array;  XchS<SW>: split re / im float arrays.
+// SW: 0 = i + (i>>4) padding, 1 = i ^ ((i>>3)&15), 2 = i ^ ((i>>4)&31),
+//     3 = i ^ ((i>>3)&31), 4 = i + (i>>5) padding.
+template <int SW>
+__host__ __device__ __forceinline__ int swz(int i) {
+  if constexpr (SW == 0) return i + (i >> 4);
+  else if constexpr (SW == 1) return i ^ ((i >> 3) & 15);
+  else if constexpr (SW == 2) return i ^ ((i >> 4) & 31);
+  else if constexpr (SW == 3) return i ^ ((i >> 3) & 31);
+  else return i + (i >> 5);
+}
+template <int SW>
+__host__ __device__ constexpr int swz_len(int L) {
+  return (SW == 0) ? L + (L >> 4) + 1 : (SW == 4) ? L + (L >> 5) + 1 : L;
+}
+
+template <int SW>
+struct Xch2 {  // float2 cells
+  static constexpr bool soa = false;
+  template <int LOG2>
+  __host__ __device__ static constexpr int bytes() { return swz_len<SW>(1 << LOG2) * 8; }
+  template <typename T>
+  static __device__ __forceinline__ void st(void* sm, int L, int i, cx<T> v) {
+    reinterpret_cast<cx<T>*>(sm)[swz<SW>(i)] = v;
+  }
+  template <typename T>
+  static __device__ __forceinline__ cx<T> ld(const void* sm, int L, int i) {
+    return reinterpret_cast<const cx<T>*>(sm)[swz<SW>(i)];
+  }
+};
+template <int SW>
+struct XchS {  // split re / im
+  static constexpr bool soa = true;
+  template <int LOG2>
+  __host__ __device__ static constexpr int bytes() { return 2 * swz_len<SW>(1 << LOG2) * 4; }
+  template <typename T>
+  static __device__ __forceinline__ void st(void* sm, int L, int i, cx<T> v) {
+    T* r = reinterpret_cast<T*>(sm);
+    const int p = swz<SW>(i);
+    r[p] = v.x;
+    r[swz_len<SW>(L) + p] = v.y;
+  }
+  template <typename T>
+  static __device__ __forceinline__ cx<T> ld(const void* sm, int L, int i) {
+    const T* r = reinterpret_cast<const T*>(sm);
+    const int p = swz<SW>(i);
+    return mk(r[p], r[swz_len<SW>(L) + p]);
+  }
+};
+
+// default exchange layout per plan (chosen by the on-GPU sweep)
+template <int LOG2>
+struct XchOf {
+  using type = Xch2<0>;
+};
+template <>
+struct XchOf<9> {  // [8,8,8] plan: XOR swizzle measured 29.6 vs 26.1 TFLOP/s for padding
+  using type = Xch2<1>;
+};
+
+// smem bytes of one row buffer for the default layout (>= L float2)
+template <int LOG2>
+__host__ __device__ constexpr int rsm_len() {
+  return (XchOf<LOG2>::type::template bytes<LOG2>() + 7) / 8 > (1 << LOG2) + ((1 << LOG2) >> 4) + 1
+             ? (XchOf<LOG2>::type::template bytes<LOG2>() + 7) / 8
+             : (1 << LOG2) + ((1 << LOG2) >> 4) + 1;
+}
+__device__ __forceinline__ int rpad(int i) { return i + (i >> 4); }
+
+// Barrier of one row group: warp-level when the group fits a warp, else a
+// named barrier per group (id 1 + gid, <= 15 groups) or the CTA barrier.
+struct GSync {
+  int id;  // 0: __syncwarp; >0: bar.sync id; <0: __syncthreads
+  int n;
+  __device__ __forceinline__ void operator()() const {
+    if (id == 0)
+      __syncwarp();
+    else if (id > 0)
+      asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+    else
+      __syncthreads();
+  }
+};
+
+template <int LOG2>
+__device__ __forceinline__ GSync make_gsync(int gid, int groups) {
+  constexpr int TPR = RPlan<LOG2>::TPR;
+  GSync s;
+  s.n = TPR;
+  if (TPR <= 32)
+    s.id = 0;
+  else if (groups <= 15)
+    s.id = 1 + gid;
+  else
+    s.id = -1;
+  return s;
+}
+
+template <typename T, int LOG2, int SIGN, int S, typename X>
+__device__ __forceinline__ void fftr_stage(cx<T> (&v)[RPlan<LOG2>::E], cx<T>* sm,
+                                           const cx<T>* __restrict__ tw, int t, const GSync& sync) {
+  using P = RPlan<LOG2>;
+  using G = Stg<LOG2, S>;
+  constexpr int E = P::E, R = G::R, NB = E / R, L = P::L, TPR = P::TPR, Ns = G::Ns;
+  constexpr bool FIRST = S == 0, LAST = S == P::NS - 1;
+  cx<T> x[NB][R];
+  cx<T> w[NB][R];
+  if constexpr (Ns > 1) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int k = (t + b * TPR) & (Ns - 1);
+#pragma unroll
+      for (int r = 1; r < R; ++r) w[b][r] = ldg_cx(tw + G::tw_off + (r - 1) * Ns + k);
+    }
+  }
+  if constexpr (FIRST) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[b][r] = v[b + r * NB];
+  } else {
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[b][r] = X::template ld<T>(sm, L, t + b * TPR + r * (L / R));
+  }
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    if constexpr (Ns > 1) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        cx<T> ww = w[b][r];
+        if (SIGN > 0) ww.y = -ww.y;
+        x[b][r] = mul(x[b][r], ww);
+      }
+    }
+    dftR<R, SIGN>(x[b]);
+  }
+  if constexpr (LAST) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[b + r * NB] = x[b][r];
+  } else {
+    sync();  // every thread finished reading sm (previous stage / previous use)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int j = t + b * TPR;
+      const int k = j & (Ns - 1);
+      const int base = (j - k) * R + k;
+#pragma unroll
+      for (int r = 0; r < R; ++r) X::template st<T>(sm, L, base + r * Ns, x[b][r]);
+    }
+    sync();
+    fftr_stage<T, LOG2, SIGN, S + 1, X>(v, sm, tw, t, sync);
+  }
+}
+
+// In-register FFT of the row held in the natural distribution.
+template <typename T, int LOG2, int SIGN, typename X = typename XchOf<LOG2>::type>
+__device__ __forceinline__ void fftr(cx<T> (&v)[RPlan<LOG2>::E], cx<T>* sm,
+                                     const cx<T>* __restrict__ tw, int t, const GSync& sync) {
+  fftr_stage<T, LOG2, SIGN, 0, X>(v, sm, tw, t, sync);
+}
+
+// Store the natural-distribution row into sm (padded) so any element can be
+// read by any thread of the group (callers sync before reading).
+template <typename T, int LOG2>
+__device__ __forceinline__ void to_smem(const cx<T> (&v)[RPlan<LOG2>::E], cx<T>* sm, int t) {
+  constexpr int E = RPlan<LOG2>::E, TPR = RPlan<LOG2>::TPR;
+#pragma unroll
+  for (int e = 0; e < E; ++e) sm[rpad(t + e * TPR)] = v[e];
+}
+
+// Host helper: per-stage twiddle table (exp(-2 pi i r k / (Ns R)), [r-1][k])
+template <int LOG2, int S = 0, typename F>
+void fill_rtwiddles(F&& put) {
+  using G = Stg<LOG2, S>;
+  for (int r = 1; r < G::R; ++r)
+    for (int k = 0; k < G::Ns; ++k) put(G::tw_off + (r - 1) * G::Ns + k, r * k, G::Ns * G::R);
+  if constexpr (S + 1 < RPlan<LOG2>::NS) fill_rtwiddles<LOG2, S + 1>(put);
+}
+
+}  // namespace lg

@@ -1,0 +1,672 @@
+// fp32 fast-path kernels for power-of-two tiles, built on the register FFT
+// (fftr.cuh).  Same data flow and reference anchors as socs_kernels.cuh (the
+// generic runtime-length path kept for odd grids and the fp64 mode); here
+// every transform length is a template parameter, band gathers/scatters go
+// straight between global memory and registers, and the per-kernel work is
+// spread over (row, kernel) so a 2048^2 tile fills all 148 SMs.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <type_traits>
+
+#include "fftr.cuh"
+#include "socs_fast.h"
+
+namespace lg {
+
+template <int LG>
+struct FGroup {
+  static constexpr int TPR = RPlan<LG>::TPR;
+  static constexpr int E = RPlan<LG>::E;
+  int gid, t, groups;
+  C32* sm;
+  GSync sync;
+  __device__ __forceinline__ FGroup() {
+    extern __shared__ __align__(16) unsigned char fsm_raw[];
+    groups = blockDim.x / TPR;
+    gid = threadIdx.x / TPR;
+    t = threadIdx.x % TPR;
+    sm = reinterpret_cast<C32*>(fsm_raw) + gid * rsm_len<LG>();
+    sync = make_gsync<LG>(gid, groups);
+  }
+  __device__ __forceinline__ int idx(int e) const { return t + e * TPR; }
+};
+
+__device__ __forceinline__ float fsig(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
+
+// kernel-band slot of residue i mod L, or -1
+__device__ __forceinline__ int kslot(int i, int lo, int hi, int L) {
+  const int q = lo + ((i - lo) & (L - 1));
+  return q <= hi ? q - lo : -1;
+}
+// intensity-band slot of residue i mod L (band2 layout of geom.h), or -1
+__device__ __forceinline__ int islot(const AxisGeom& a, int i, int L) {
+  if (a.full) return i;  // full band: L == n == N, slot j = residue
+  const int q = -a.P + ((i + a.P) & (L - 1));
+  return q <= a.P ? q + a.P : -1;
+}
+
+// Build Z = A + iB for the row held in the natural distribution from the
+// half spectra a[0..P], b[0..P] of two real signals (b may be null).
+template <int LG>
+__device__ __forceinline__ void load_herm_pair(C32 (&v)[RPlan<LG>::E], const FGroup<LG>& g,
+                                               const C32* a, const C32* b, int P) {
+  constexpr int L = 1 << LG;
+#pragma unroll
+  for (int e = 0; e < RPlan<LG>::E; ++e) {
+    const int i = g.idx(e);
+    const int m = (L - i) & (L - 1);
+    C32 A = mk(0.f, 0.f), Bv = mk(0.f, 0.f);
+    if (i <= P) {
+      A = a[i];
+      if (b) Bv = b[i];
+      if (m == i) {
+        A.y = 0.f;
+        Bv.y = 0.f;
+      }
+    } else if (m <= P) {
+      A = conjg(a[m]);
+      if (b) Bv = conjg(b[m]);
+    }
+    v[e] = mk(A.x - Bv.y, A.y + Bv.x);
+  }
+}
+
+// warp-partial (deterministic) reduction: lane 0 of each warp-slice writes
+__device__ __forceinline__ float warp_sum(float v, int width) {
+  for (int o = width / 2; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o, width);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v, int width) {
+  for (int o = width / 2; o > 0; o >>= 1) v = fmaxf(v, __shfl_down_sync(0xffffffffu, v, o, width));
+  return v;
+}
+
+// ===========================================================================
+// real row pairs -> half spectra [Pout+1][Ny] (MODE 0 raw, 1 sigmoid(steep x))
+// ===========================================================================
+template <int LG, int MODE>
+__global__ void __launch_bounds__(256) fk_real_rows_fwd(FGeo g, const float* __restrict__ src,
+                                                        long long src_ts, float steep, int Pout,
+                                                        C32* __restrict__ out, long long out_ts) {
+  FGroup<LG> G;
+  constexpr int L = 1 << LG, E = RPlan<LG>::E;
+  const int Ny = g.ay.N, npairs = (Ny + 1) / 2;
+  const int pair0 = blockIdx.x * G.groups + G.gid;
+  const bool act = pair0 < npairs;
+  const int pair = act ? pair0 : npairs - 1;
+  const int y0 = 2 * pair, y1 = y0 + 1;
+  const bool has1 = y1 < Ny;
+  const float* s = src + blockIdx.z * src_ts;
+  C32 v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = G.idx(e);
+    float a = s[size_t(y0) * L + i];
+    float b = has1 ? s[size_t(y1) * L + i] : 0.f;
+    if (MODE == 1) {
+      a = fsig(steep * a);
+      b = has1 ? fsig(steep * b) : 0.f;
+    }
+    v[e] = mk(a, b);
+  }
+  fftr<float, LG, -1>(v, G.sm, g.twNx, G.t, G.sync);
+  G.sync();
+  to_smem<float, LG>(v, G.sm, G.t);
+  G.sync();
+  if (!act) return;
+  C32* o = out + blockIdx.z * out_ts;
+  for (int px = G.t; px <= Pout; px += G.TPR) {
+    C32 A, Bv;
+    split_pair(G.sm[rpad(px)], G.sm[rpad((L - px) & (L - 1))], A, Bv);
+    o[size_t(px) * Ny + y0] = A;
+    if (has1) o[size_t(px) * Ny + y1] = Bv;
+  }
+}
+
+// ===========================================================================
+// per-kernel rows: I_sub(sy,.) = dose sum_k w_k |IFFT_nx(T_fk[sy])|^2, the K
+// kernels spread over the CTA's row groups, reduced in fixed order, then the
+// FFT of the real intensity row -> Ir[f][px][sy], px in [0, P].
+// grid (ny, F, tiles), block = groups * TPR
+// ===========================================================================
+template <int LG>
+__global__ void __launch_bounds__(512) fk_socs_rows(FGeo g, const C32* __restrict__ T,
+                                                    long long t_ts, const float* __restrict__ wk,
+                                                    float dose, C32* __restrict__ Ir,
+                                                    long long ir_ts) {
+  FGroup<LG> G;
+  constexpr int L = 1 << LG, E = RPlan<LG>::E;
+  const int sy = blockIdx.x, f = blockIdx.y, K = g.K, Bx = g.ax.B, ny = g.ay.n;
+  const int lo = g.ax.lo, hi = g.ax.hi;
+  float acc[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) acc[e] = 0.f;
+  int slot[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) slot[e] = kslot(G.idx(e), lo, hi, L);
+  for (int k = G.gid; k < K; k += G.groups) {
+    const C32* src = T + blockIdx.z * t_ts + (size_t(f) * K + k) * ny * Bx + size_t(sy) * Bx;
+    C32 v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = slot[e] >= 0 ? src[slot[e]] : mk(0.f, 0.f);
+    fftr<float, LG, +1>(v, G.sm, g.twnx, G.t, G.sync);
+    const float w = wk[f * K + k] * dose;
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] += w * (v[e].x * v[e].x + v[e].y * v[e].y);
+  }
+  // fixed-order cross-group reduction through shared memory
+  G.sync();
+  float* mine = reinterpret_cast<float*>(G.sm);
+#pragma unroll
+  for (int e = 0; e < E; ++e) mine[G.idx(e)] = acc[e];
+  __syncthreads();
+  if (G.gid != 0) return;
+  C32 v[E];
+  const float* base = reinterpret_cast<const float*>(G.sm);  // group 0 buffer
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    float s = 0.f;
+    for (int q = 0; q < G.groups; ++q)
+      s += reinterpret_cast<const float*>(base + size_t(q) * 2 * rsm_len<LG>())[G.idx(e)];
+    v[e] = mk(s, 0.f);
+  }
+  fftr<float, LG, -1>(v, G.sm, g.twnx, G.t, G.sync);
+  C32* o = Ir + blockIdx.z * ir_ts + size_t(f) * (g.ax.P + 1) * ny;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = G.idx(e);
+    if (i <= g.ax.P) o[size_t(i) * ny + sy] = v[e];
+  }
+}
+
+// ===========================================================================
+// ILT resist rows (row pair y0, y0+1 of focus f): R = IFFT_Nx(R^ half rows),
+// Z = sig(beta (R - thr)), cost partial, D = 2 c_f (Z - Zt) beta Z (1 - Z),
+// FFT_Nx(D pair) -> Dr[f][px][y].  grid (ceil(Ny/2/groups), F, tiles)
+// ===========================================================================
+template <int LG>
+__global__ void __launch_bounds__(256) fk_resist_rows(FGeo g, const C32* __restrict__ Rc,
+                                                      long long c_ts, const float* __restrict__ target,
+                                                      long long tg_ts, const float* __restrict__ cf,
+                                                      float beta, float thr, C32* __restrict__ Dr,
+                                                      long long d_ts, double* __restrict__ costp,
+                                                      long long cp_ts) {
+  FGroup<LG> G;
+  constexpr int L = 1 << LG, E = RPlan<LG>::E, TPR = RPlan<LG>::TPR;
+  constexpr int WPG = TPR >= 32 ? TPR / 32 : 1;
+  const int Ny = g.ay.N, Px = g.ax.P, f = blockIdx.y, npairs = (Ny + 1) / 2;
+  const int pair0 = blockIdx.x * G.groups + G.gid;
+  const bool act = pair0 < npairs;
+  const int pair = act ? pair0 : npairs - 1;
+  const int y0 = 2 * pair, y1 = y0 + 1;
+  const bool has1 = y1 < Ny;
+  const C32* rc = Rc + blockIdx.z * c_ts + size_t(f) * Ny * (Px + 1);
+  // target rows prefetched before the transform (latency hidden behind it)
+  const float* tg = target + blockIdx.z * tg_ts;
+  float t0v[E], t1v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    t0v[e] = __ldg(tg + size_t(y0) * L + G.idx(e));
+    t1v[e] = has1 ? __ldg(tg + size_t(y1) * L + G.idx(e)) : 0.f;
+  }
+  C32 v[E];
+  load_herm_pair<LG>(v, G, rc + size_t(y0) * (Px + 1), has1 ? rc + size_t(y1) * (Px + 1) : nullptr, Px);
+  fftr<float, LG, +1>(v, G.sm, g.twNx, G.t, G.sync);
+  const float w = cf[f];
+  float c = 0.f;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const float z0 = fsig(beta * (v[e].x - thr));
+    const float e0 = z0 - t0v[e];
+    float d1 = 0.f;
+    c += e0 * e0;
+    if (has1) {
+      const float z1 = fsig(beta * (v[e].y - thr));
+      const float e1 = z1 - t1v[e];
+      c += e1 * e1;
+      d1 = 2.f * w * e1 * beta * z1 * (1.f - z1);
+    }
+    v[e] = mk(2.f * w * e0 * beta * z0 * (1.f - z0), d1);
+  }
+  c = warp_sum(c * w, TPR < 32 ? TPR : 32);
+  if (act && (G.t & 31) == 0)
+    costp[blockIdx.z * cp_ts + (size_t(f) * npairs + pair) * WPG + (G.t >> 5)] = double(c);
+  fftr<float, LG, -1>(v, G.sm, g.twNx, G.t, G.sync);
+  G.sync();
+  to_smem<float, LG>(v, G.sm, G.t);
+  G.sync();
+  if (!act) return;
+  C32* d = Dr + blockIdx.z * d_ts + size_t(f) * (Px + 1) * Ny;
+  for (int px = G.t; px <= Px; px += TPR) {
+    C32 A, Bv;
+    split_pair(G.sm[rpad(px)], G.sm[rpad((L - px) & (L - 1))], A, Bv);
+    d[size_t(px) * Ny + y0] = A;
+    if (has1) d[size_t(px) * Ny + y1] = Bv;
+  }
+}
+
+// ===========================================================================
+// forward output rows: I = Re, R = Im of IFFT_Nx(I^ + i R^), print = R >= thr
+// grid (ceil(Ny/groups), F, tiles)
+// ===========================================================================
+template <int LG>
+__global__ void __launch_bounds__(256) fk_out_rows(FGeo g, const C32* __restrict__ Ic,
+                                                   const C32* __restrict__ Rc, long long c_ts,
+                                                   float* __restrict__ Iout, float* __restrict__ Rout,
+                                                   unsigned char* __restrict__ print, long long o_ts,
+                                                   float thr) {
+  FGroup<LG> G;
+  constexpr int L = 1 << LG, E = RPlan<LG>::E;
+  const int Ny = g.ay.N, Px = g.ax.P, f = blockIdx.y;
+  const int y0 = blockIdx.x * G.groups + G.gid;
+  const bool act = y0 < Ny;
+  const int y = act ? y0 : Ny - 1;
+  const size_t cb = blockIdx.z * c_ts + (size_t(f) * Ny + y) * (Px + 1);
+  C32 v[E];
+  load_herm_pair<LG>(v, G, Ic ? Ic + cb : Rc + cb, (Ic && Rc) ? Rc + cb : nullptr, Px);
+  fftr<float, LG, +1>(v, G.sm, g.twNx, G.t, G.sync);
+  if (!act) return;
+  const size_t ob = blockIdx.z * o_ts + (size_t(f) * Ny + y) * L;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = G.idx(e);
+    const float Iv = v[e].x;
+    const float Rv = Ic ? v[e].y : v[e].x;  // R alone sits in the real slot
+    if (Iout && Ic) Iout[ob + i] = Iv;
+    if (Rout && Rc) Rout[ob + i] = Rv;
+    if (print && Rc) print[ob + i] = Rv >= thr ? 1 : 0;
+  }
+}
+
+// ===========================================================================
+// W_lp on the decimated grid: Wsub[f][sy] = IFFT_nx(Hermitian Wc[f][sy]) for
+// row pairs.  grid (ceil(ny/2/groups), nf, tiles)
+// ===========================================================================
+template <int LG>
+__global__ void __launch_bounds__(256) fk_wlp_rows(FGeo g, const C32* __restrict__ Wc,
+                                                   long long w_ts, float* __restrict__ Wsub,
+                                                   long long ws_ts) {
+  FGroup<LG> G;
+  constexpr int L = 1 << LG, E = RPlan<LG>::E;
+  const int ny = g.ay.n, Px = g.ax.P, f = blockIdx.y, npairs = (ny + 1) / 2;
+  const int pair0 = blockIdx.x * G.groups + G.gid;
+  const bool act = pair0 < npairs;
+  const int pair = act ? pair0 : npairs - 1;
+  const int y0 = 2 * pair, y1 = y0 + 1;
+  const bool has1 = y1 < ny;
+  const C32* wc = Wc + blockIdx.z * w_ts + size_t(f) * ny * (Px + 1);
+  C32 v[E];
+  load_herm_pair<LG>(v, G, wc + size_t(y0) * (Px + 1), has1 ? wc + size_t(y1) * (Px + 1) : nullptr, Px);
+  fftr<float, LG, +1>(v, G.sm, g.twnx, G.t, G.sync);
+  if (!act) return;
+  float* o = Wsub + blockIdx.z * ws_ts + size_t(f) * ny * L;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = G.idx(e);
+    o[size_t(y0) * L + i] = v[e].x;
+    if (has1) o[size_t(y1) * L + i] = v[e].y;
+  }
+}
+
+// ===========================================================================
+// adjoint rows, one (sy, f*K+k) per group:
+//   U_fk[qx][sy] = FFT_nx(W_lp(sy,.) . IFFT_nx(T_fk[sy]))(qx), qx in band
+// grid (ceil(ny/groups), F*K, tiles)
+// ===========================================================================
+template <int LG, bool UNIFORM>
+__global__ void __launch_bounds__(256) fk_adj_rows(FGeo g, const C32* __restrict__ T,
+                                                   long long t_ts, const float* __restrict__ Wsub,
+                                                   long long ws_ts, C32* __restrict__ U,
+                                                   long long u_ts) {
+  FGroup<LG> G;
+  constexpr int L = 1 << LG, E = RPlan<LG>::E;
+  const int ny = g.ay.n, Bx = g.ax.B, K = g.K, lo = g.ax.lo, hi = g.ax.hi;
+  const int fk = blockIdx.y, f = fk / K;
+  const int sy0 = blockIdx.x * G.groups + G.gid;
+  const bool act = sy0 < ny;
+  const int sy = act ? sy0 : ny - 1;
+  int slot[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) slot[e] = kslot(G.idx(e), lo, hi, L);
+  const C32* src = T + blockIdx.z * t_ts + size_t(fk) * ny * Bx + size_t(sy) * Bx;
+  C32 v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) v[e] = slot[e] >= 0 ? src[slot[e]] : mk(0.f, 0.f);
+  float wv[E];
+  if (!UNIFORM) {
+    const float* w = Wsub + blockIdx.z * ws_ts + (size_t(f) * ny + sy) * L;
+#pragma unroll
+    for (int e = 0; e < E; ++e) wv[e] = w[G.idx(e)];
+  }
+  fftr<float, LG, +1>(v, G.sm, g.twnx, G.t, G.sync);
+  if (!UNIFORM) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = scale(v[e], wv[e]);
+  }
+  fftr<float, LG, -1>(v, G.sm, g.twnx, G.t, G.sync);
+  if (!act) return;
+  C32* o = U + blockIdx.z * u_ts + size_t(fk) * Bx * ny;
+#pragma unroll
+  for (int e = 0; e < E; ++e)
+    if (slot[e] >= 0) o[size_t(slot[e]) * ny + sy] = v[e];
+}
+
+// ===========================================================================
+// gradient rows (pair y0, y0+1): g = IFFT_Nx(Hermitian Gc rows) = dL/dM;
+// !ILT: write grad; ILT: theta update, then next iteration's mask rows.
+// grid (ceil(Ny/2/groups), 1, tiles)
+// ===========================================================================
+template <int LG, bool ILT>
+__global__ void __launch_bounds__(256) fk_grad_rows(FGeo g, const C32* __restrict__ Gc,
+                                                    long long g_ts, float* __restrict__ grad,
+                                                    long long gr_ts, float* __restrict__ theta,
+                                                    long long th_ts, float steep, float step,
+                                                    C32* __restrict__ Mr, long long mr_ts,
+                                                    double* __restrict__ gmaxp, long long gm_ts) {
+  FGroup<LG> G;
+  constexpr int L = 1 << LG, E = RPlan<LG>::E, TPR = RPlan<LG>::TPR;
+  constexpr int WPG = TPR >= 32 ? TPR / 32 : 1;
+  const int Ny = g.ay.N, Pm = g.ax.Pm, npairs = (Ny + 1) / 2;
+  const int pair0 = blockIdx.x * G.groups + G.gid;
+  const bool act = pair0 < npairs;
+  const int pair = act ? pair0 : npairs - 1;
+  const int y0 = 2 * pair, y1 = y0 + 1;
+  const bool has1 = y1 < Ny;
+  const C32* gc = Gc + blockIdx.z * g_ts;
+  float* th = theta + blockIdx.z * th_ts;
+  float t0v[E], t1v[E];  // theta rows prefetched before the transform
+  if (ILT) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      t0v[e] = th[size_t(y0) * L + G.idx(e)];
+      t1v[e] = has1 ? th[size_t(y1) * L + G.idx(e)] : 0.f;
+    }
+  }
+  C32 v[E];
+  load_herm_pair<LG>(v, G, gc + size_t(y0) * (Pm + 1), has1 ? gc + size_t(y1) * (Pm + 1) : nullptr, Pm);
+  fftr<float, LG, +1>(v, G.sm, g.twNx, G.t, G.sync);
+  if (!ILT) {
+    if (!act) return;
+    float* o = grad + blockIdx.z * gr_ts;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = G.idx(e);
+      o[size_t(y0) * L + i] = v[e].x;
+      if (has1) o[size_t(y1) * L + i] = v[e].y;
+    }
+    return;
+  }
+  float gm = 0.f;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = G.idx(e);
+    const float t0 = t0v[e];
+    const float m0 = fsig(steep * t0);
+    const float g0 = v[e].x * steep * m0 * (1.f - m0);
+    const float n0 = t0 - step * g0;
+    gm = fmaxf(gm, fabsf(g0));
+    float n1v = 0.f;
+    if (has1) {
+      const float t1 = t1v[e];
+      const float m1 = fsig(steep * t1);
+      const float g1 = v[e].y * steep * m1 * (1.f - m1);
+      const float n1 = t1 - step * g1;
+      gm = fmaxf(gm, fabsf(g1));
+      if (act) th[size_t(y1) * L + i] = n1;
+      n1v = fsig(steep * n1);
+    }
+    if (act) th[size_t(y0) * L + i] = n0;
+    v[e] = mk(fsig(steep * n0), n1v);
+  }
+  gm = warp_max(gm, TPR < 32 ? TPR : 32);
+  if (act && gmaxp && (G.t & 31) == 0) gmaxp[blockIdx.z * gm_ts + size_t(pair) * WPG + (G.t >> 5)] = gm;
+  fftr<float, LG, -1>(v, G.sm, g.twNx, G.t, G.sync);
+  G.sync();
+  to_smem<float, LG>(v, G.sm, G.t);
+  G.sync();
+  if (!act) return;
+  C32* o = Mr + blockIdx.z * mr_ts;
+  for (int px = G.t; px <= Pm; px += TPR) {
+    C32 A, Bv;
+    split_pair(G.sm[rpad(px)], G.sm[rpad((L - px) & (L - 1))], A, Bv);
+    o[size_t(px) * Ny + y0] = A;
+    if (has1) o[size_t(px) * Ny + y1] = Bv;
+  }
+}
+
+// ===========================================================================
+// mask half-spectrum columns -> kernel band M^ (Hermitian mirror for qx < 0)
+// grid (ceil((Pmx+1)/groups), 1, tiles)
+// ===========================================================================
+template <int LG>
+__global__ void __launch_bounds__(256) fk_mask_cols(FGeo g, const C32* __restrict__ Mr,
+                                                    long long mr_ts, C32* __restrict__ Mhat,
+                                                    long long mh_ts) {
+  FGroup<LG> G;
+  constexpr int L = 1 << LG, E = RPlan<LG>::E;
+  const int Pm = g.ax.Pm;
+  const int px0 = blockIdx.x * G.groups + G.gid;
+  const bool act = px0 <= Pm;
+  const int px = act ? px0 : Pm;
+  const C32* src = Mr + blockIdx.z * mr_ts + size_t(px) * L;
+  C32 v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) v[e] = src[G.idx(e)];
+  fftr<float, LG, -1>(v, G.sm, g.twNy, G.t, G.sync);
+  if (!act) return;
+  const float inv = 1.0f / (float(g.ax.N) * float(L));
+  C32* mh = Mhat + blockIdx.z * mh_ts;
+  const int Bx = g.ax.B;
+  const int sp = band_slot(g.ax, px);
+  const int sn = px > 0 ? band_slot(g.ax, -px) : -1;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = G.idx(e);
+    if (sp >= 0) {
+      const int jy = kslot(i, g.ay.lo, g.ay.hi, L);
+      if (jy >= 0) mh[size_t(jy) * Bx + sp] = scale(v[e], inv);
+    }
+    if (sn >= 0 && sn != sp) {
+      const int jy = kslot((L - i) & (L - 1), g.ay.lo, g.ay.hi, L);
+      if (jy >= 0) mh[size_t(jy) * Bx + sn] = scale(conjg(v[e]), inv);
+    }
+  }
+}
+
+// ===========================================================================
+// per-kernel columns on the decimated grid: T_fk[sy][cx] = IFFT_ny(M^ H_fk)
+// grid (ceil(Bx/groups), F*K, tiles)
+// ===========================================================================
+template <int LG>
+__global__ void __launch_bounds__(256) fk_socs_cols(FGeo g, const C32* __restrict__ Mhat,
+                                                    long long mh_ts, const C32* __restrict__ H,
+                                                    C32* __restrict__ T, long long t_ts) {
+  FGroup<LG> G;
+  constexpr int L = 1 << LG, E = RPlan<LG>::E;
+  const int Bx = g.ax.B, By = g.ay.B, fk = blockIdx.y;
+  const int c0 = blockIdx.x * G.groups + G.gid;
+  const bool act = c0 < Bx;
+  const int cx_ = act ? c0 : Bx - 1;
+  const C32* mh = Mhat + blockIdx.z * mh_ts;
+  const C32* h = H + size_t(fk) * By * Bx;
+  C32 v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int jy = kslot(G.idx(e), g.ay.lo, g.ay.hi, L);
+    v[e] = jy >= 0 ? mul(mh[size_t(jy) * Bx + cx_], ldg_cx(h + size_t(jy) * Bx + cx_)) : mk(0.f, 0.f);
+  }
+  fftr<float, LG, +1>(v, G.sm, g.twny, G.t, G.sync);
+  if (!act) return;
+  C32* o = T + blockIdx.z * t_ts + size_t(fk) * L * Bx;
+#pragma unroll
+  for (int e = 0; e < E; ++e) o[size_t(G.idx(e)) * Bx + cx_] = v[e];
+}
+
+// ===========================================================================
+// column FFT -> intensity band: out[f][j][px] = FFT_L(in[f][px])(p_j) s(j,px)
+// grid (ceil((Px+1)/groups), nf, tiles).  inv = 1/(Lx L) (grid normalisation)
+// ===========================================================================
+template <int LG>
+__global__ void __launch_bounds__(256) fk_band_colfwd(FGeo g, const C32* __restrict__ in,
+                                                      long long in_ts, float inv,
+                                                      const float* __restrict__ gxh,
+                                                      const float* __restrict__ gyb,
+                                                      C32* __restrict__ outR, C32* __restrict__ outI,
+                                                      long long o_ts) {
+  FGroup<LG> G;
+  constexpr int L = 1 << LG, E = RPlan<LG>::E;
+  const int Px = g.ax.P, f = blockIdx.y, nb2 = g.ay.nb2;
+  const int px0 = blockIdx.x * G.groups + G.gid;
+  const bool act = px0 <= Px;
+  const int px = act ? px0 : Px;
+  const C32* src = in + blockIdx.z * in_ts + (size_t(f) * (Px + 1) + px) * L;
+  C32 v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) v[e] = src[G.idx(e)];
+  fftr<float, LG, -1>(v, G.sm, L == g.ay.N ? g.twNy : g.twny, G.t, G.sync);
+  if (!act) return;
+  const float gx = gxh ? gxh[px] : 1.f;
+  const size_t ob = blockIdx.z * o_ts + size_t(f) * nb2 * (Px + 1);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int j = islot(g.ay, G.idx(e), L);
+    if (j < 0) continue;
+    const C32 c = scale(v[e], inv);
+    if (outI) outI[ob + size_t(j) * (Px + 1) + px] = c;
+    if (outR) outR[ob + size_t(j) * (Px + 1) + px] = gyb ? scale(c, gx * gyb[j]) : c;
+  }
+}
+
+// ===========================================================================
+// intensity band -> column IFFT of length L: out[f][y][px]
+// grid (ceil((Px+1)/groups), nf, tiles)
+// ===========================================================================
+template <int LG>
+__global__ void __launch_bounds__(256) fk_band_colinv(FGeo g, const C32* __restrict__ band,
+                                                      long long b_ts, C32* __restrict__ out,
+                                                      long long o_ts) {
+  FGroup<LG> G;
+  constexpr int L = 1 << LG, E = RPlan<LG>::E;
+  const int Px = g.ax.P, f = blockIdx.y, nb2 = g.ay.nb2;
+  const int px0 = blockIdx.x * G.groups + G.gid;
+  const bool act = px0 <= Px;
+  const int px = act ? px0 : Px;
+  const C32* b = band + blockIdx.z * b_ts + size_t(f) * nb2 * (Px + 1);
+  C32 v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int j = islot(g.ay, G.idx(e), L);
+    v[e] = j >= 0 ? b[size_t(j) * (Px + 1) + px] : mk(0.f, 0.f);
+  }
+  fftr<float, LG, +1>(v, G.sm, L == g.ay.N ? g.twNy : g.twny, G.t, G.sync);
+  if (!act) return;
+  C32* o = out + blockIdx.z * o_ts + size_t(f) * L * (Px + 1);
+#pragma unroll
+  for (int e = 0; e < E; ++e) o[size_t(G.idx(e)) * (Px + 1) + px] = v[e];
+}
+
+// ===========================================================================
+// adjoint columns: Acc(qy,cx) = sum_fk FFT_ny(U_fk[cx])(qy) conj(H_fk) 2 dose
+// w_fk dx dy/(Nx Ny); (f,k) spread over the CTA's groups, fixed-order
+// reduction.  grid (Bx, 1, tiles)
+// ===========================================================================
+template <int LG>
+__global__ void __launch_bounds__(512) fk_adj_cols(FGeo g, const C32* __restrict__ U,
+                                                   long long u_ts, const C32* __restrict__ H,
+                                                   const float* __restrict__ wk, float dose,
+                                                   C32* __restrict__ Acc, long long a_ts) {
+  FGroup<LG> G;
+  constexpr int L = 1 << LG, E = RPlan<LG>::E;
+  const int Bx = g.ax.B, By = g.ay.B, FK = g.F * g.K, cx_ = blockIdx.x;
+  const float sc = float(2.0 * double(g.ax.d) * double(g.ay.d) / (double(g.ax.N) * double(g.ay.N)));
+  int slot[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) slot[e] = kslot(G.idx(e), g.ay.lo, g.ay.hi, L);
+  C32 acc[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) acc[e] = mk(0.f, 0.f);
+  for (int fk = G.gid; fk < FK; fk += G.groups) {
+    const C32* src = U + blockIdx.z * u_ts + (size_t(fk) * Bx + cx_) * L;
+    C32 v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = src[G.idx(e)];
+    fftr<float, LG, -1>(v, G.sm, g.twny, G.t, G.sync);
+    const float w = wk[fk] * dose * sc;
+    const C32* h = H + size_t(fk) * By * Bx;
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      if (slot[e] >= 0) acc[e] = add(acc[e], scale(mulc(v[e], ldg_cx(h + size_t(slot[e]) * Bx + cx_)), w));
+  }
+  G.sync();
+#pragma unroll
+  for (int e = 0; e < E; ++e) G.sm[G.idx(e)] = acc[e];
+  __syncthreads();
+  if (G.gid != 0) return;
+  C32* o = Acc + blockIdx.z * a_ts;
+  const C32* base = G.sm;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    if (slot[e] < 0) continue;
+    C32 s = mk(0.f, 0.f);
+    for (int q = 0; q < G.groups; ++q) s = add(s, base[size_t(q) * rsm_len<LG>() + G.idx(e)]);
+    o[size_t(slot[e]) * Bx + cx_] = s;
+  }
+}
+
+// ===========================================================================
+// gradient columns: Hermitian part of Acc, IFFT_Ny -> Gc[y][px], px in [0,Pmx];
+// the last CTA reduces this iteration's cost partials (fixed order).
+// grid (ceil((Pmx+1)/groups) + 1, 1, tiles)
+// ===========================================================================
+template <int LG>
+__global__ void __launch_bounds__(256) fk_grad_cols(FGeo g, const C32* __restrict__ Acc,
+                                                    long long a_ts, C32* __restrict__ Gc,
+                                                    long long g_ts, const double* __restrict__ costp,
+                                                    long long cp_ts, int ncost,
+                                                    double* __restrict__ cost_out, long long co_ts) {
+  FGroup<LG> G;
+  constexpr int L = 1 << LG, E = RPlan<LG>::E;
+  if (blockIdx.x == gridDim.x - 1) {
+    if (cost_out) {  // fixed-order (deterministic) parallel sum of the cost partials
+      __shared__ double red[256];
+      const double* c = costp + blockIdx.z * cp_ts;
+      double s = 0;
+      if (threadIdx.x < 256)
+        for (int i = threadIdx.x; i < ncost; i += 256) s += c[i];
+      if (threadIdx.x < 256) red[threadIdx.x] = s;
+      __syncthreads();
+      for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) cost_out[blockIdx.z * co_ts] = red[0];
+    }
+    return;
+  }
+  const int Pm = g.ax.Pm, Bx = g.ax.B;
+  const int px0 = blockIdx.x * G.groups + G.gid;
+  const bool act = px0 <= Pm;
+  const int px = act ? px0 : Pm;
+  const C32* a = Acc + blockIdx.z * a_ts;
+  const int sp = band_slot(g.ax, px), sn = band_slot(g.ax, -px);
+  C32 v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = G.idx(e);
+    const int jp = kslot(i, g.ay.lo, g.ay.hi, L);
+    const int jn = kslot((L - i) & (L - 1), g.ay.lo, g.ay.hi, L);
+    C32 s = mk(0.f, 0.f);
+    if (sp >= 0 && jp >= 0) s = add(s, a[size_t(jp) * Bx + sp]);
+    if (sn >= 0 && jn >= 0) s = add(s, conjg(a[size_t(jn) * Bx + sn]));
+    v[e] = scale(s, 0.5f);
+  }
+  fftr<float, LG, +1>(v, G.sm, g.twNy, G.t, G.sync);
+  if (!act) return;
+  C32* o = Gc + blockIdx.z * g_ts;
+#pragma unroll
+  for (int e = 0; e < E; ++e) o[size_t(G.idx(e)) * (Pm + 1) + px] = v[e];
+}
+
+}  // namespace lg

@@ -1,0 +1,69 @@
+// Host-side interface of the fp32 fast path (power-of-two tiles): one
+// launcher per kernel, each enqueues exactly one kernel on `s`.
+// Kernels live in socs_fast.cuh; launchers are split over fast_rows.cu /
+// fast_cols.cu so the template instantiations compile in parallel.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "fft.cuh"
+#include "geom.h"
+
+namespace lg {
+
+struct FGeo {
+  AxisGeom ax, ay;
+  int F, K;
+  int lgNx, lgNy, lgnx, lgny;
+  // per-stage twiddle tables (fftr.cuh layout) for Nx, Ny, nx, ny
+  const cx<float>* twNx;
+  const cx<float>* twNy;
+  const cx<float>* twnx;
+  const cx<float>* twny;
+};
+
+using C32 = cx<float>;
+
+inline bool fast_log2_ok(int lg) { return lg >= 5 && lg <= 13; }
+int fast_tw_len(int lg);
+int fast_tpr(int lg);  // threads per row group of the length-2^lg plan
+void fast_fill_twiddles(int lg, C32* host_out);  // fftr per-stage layout
+
+// ---- row kernels (fast_rows.cu) ----
+void fl_real_rows_fwd(const FGeo& g, cudaStream_t s, int tiles, int mode, const float* src,
+                      long long src_ts, float steep, int Pout, C32* out, long long out_ts);
+void fl_socs_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* T, long long t_ts,
+                  const float* wk, float dose, C32* Ir, long long ir_ts);
+void fl_resist_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* Rc, long long c_ts,
+                    const float* target, long long tg_ts, const float* cf, float beta, float thr,
+                    C32* Dr, long long d_ts, double* costp, long long cp_ts);
+void fl_out_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* Ic, const C32* Rc,
+                 long long c_ts, float* Iout, float* Rout, unsigned char* print, long long o_ts,
+                 float thr);
+void fl_wlp_rows(const FGeo& g, cudaStream_t s, int tiles, int nf, const C32* Wc, long long w_ts,
+                 float* Wsub, long long ws_ts);
+void fl_adj_rows(const FGeo& g, cudaStream_t s, int tiles, int nf, bool uniform, const C32* T,
+                 long long t_ts, const float* Wsub, long long ws_ts, C32* U, long long u_ts);
+void fl_grad_rows(const FGeo& g, cudaStream_t s, int tiles, bool ilt, const C32* Gc, long long g_ts,
+                  float* grad, long long gr_ts, float* theta, long long th_ts, float steep,
+                  float step, C32* Mr, long long mr_ts, double* gmaxp, long long gm_ts);
+
+// ---- column kernels (fast_cols.cu) ----
+void fl_mask_cols(const FGeo& g, cudaStream_t s, int tiles, const C32* Mr, long long mr_ts,
+                  C32* Mhat, long long mh_ts);
+void fl_socs_cols(const FGeo& g, cudaStream_t s, int tiles, const C32* Mhat, long long mh_ts,
+                  const C32* H, C32* T, long long t_ts);
+// column FFT of length Ly (ny or Ny) -> intensity band (optionally x Gaussian)
+void fl_band_colfwd(const FGeo& g, cudaStream_t s, int tiles, int nf, bool sub, const C32* in,
+                    long long in_ts, const float* gxh, const float* gyb, C32* outR, C32* outI,
+                    long long o_ts);
+// intensity band -> column IFFT of length Ly (Ny if !sub else ny)
+void fl_band_colinv(const FGeo& g, cudaStream_t s, int tiles, int nf, bool sub, const C32* band,
+                    long long b_ts, C32* out, long long o_ts);
+void fl_adj_cols(const FGeo& g, cudaStream_t s, int tiles, const C32* U, long long u_ts,
+                 const C32* H, const float* wk, float dose, C32* Acc, long long a_ts);
+void fl_grad_cols(const FGeo& g, cudaStream_t s, int tiles, const C32* Acc, long long a_ts, C32* Gc,
+                  long long g_ts, const double* costp, long long cp_ts, int ncost,
+                  double* cost_out, long long co_ts);
+
+}  // namespace lg

@@ -139,15 +139,6 @@ __device__ __forceinline__ float sigm<float>(float x) {
   return 1.0f / (1.0f + __expf(-x));
 }
 
-// Hermitian split of a packed real pair: Z = FFT(a + i b) ->
-//   A(p) = (Z(p) + conj Z(-p))/2,  B(p) = (Z(p) - conj Z(-p))/(2i)
-template <typename T>
-__device__ __forceinline__ void split_pair(cx<T> X, cx<T> Ym, cx<T>& A, cx<T>& Bv) {
-  const cx<T> Yc = conjg(Ym);
-  A = scale(add(X, Yc), T(0.5));
-  const cx<T> D = sub(X, Yc);
-  Bv = mk(T(0.5) * D.y, T(-0.5) * D.x);
-}
 
 // ===========================================================================
 // Full-grid real row pairs -> half spectra px in [0, Pout] (column-major out)

@@ -40,6 +40,7 @@ IMG_CASES = [
     (256, 256, 1.0, 8, 21),
     (128, 256, 1.0, 12, 21),
     (1024, 1024, 1.0, 8, 21),
+    (2048, 2048, 1.0, 16, 21),
 ]
 
 
@@ -120,7 +121,8 @@ def test_gradient_vs_oracle(ctx, n, pitch, K, gn, prec, weighted):
 
 @pytest.mark.parametrize("n,F,K,prec,tol", [(64, 1, 8, "f64", 1e-9), (64, 3, 8, "f64", 1e-9),
                                             (256, 1, 16, "f32", 1e-4), (256, 5, 8, "f32", 1e-4),
-                                            (24, 3, 0, "f64", 1e-9)])
+                                            (24, 3, 0, "f64", 1e-9), (2048, 1, 16, "f32", 1e-4),
+                                            (512, 3, 16, "f32", 1e-4)])
 def test_ilt_step_vs_oracle(ctx, n, F, K, prec, tol):
     rng = np.random.default_rng(7 * n + F)
     pitch = 4.0 if n == 24 else 1.0
