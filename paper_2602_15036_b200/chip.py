@@ -1,0 +1,93 @@
+"""Chip-scale ILT over halo-padded tiles, sharded across ranks (one process
+per GPU).  SURVEY.md §8e: tiles are independent (cyclic convolution inside
+each halo-padded window), so the only data-path exchange is the all-reduce of
+the global ILT cost and convergence scalars once per iteration.
+
+Torch is plumbing here: torch.distributed (NCCL on GPUs, gloo in CPU tests)
+for the scalar all-reduce; all imaging / adjoint work runs in liblithogpu.so.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+
+def shard(n_tiles: int, world: int, rank: int) -> range:
+    """Contiguous block of tiles for `rank` (sizes differ by at most one)."""
+    if world <= 0 or not (0 <= rank < world):
+        raise ValueError("shard: bad world/rank")
+    base, extra = divmod(n_tiles, world)
+    start = rank * base + min(rank, extra)
+    return range(start, start + base + (1 if rank < extra else 0))
+
+
+def allreduce_scalars(cost, gmax, group=None):
+    """Global ILT cost (sum over tiles / ranks) and convergence scalar (max
+    |dL/dtheta|) — the only cross-GPU traffic of the tiled ILT."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        dist.all_reduce(cost, op=dist.ReduceOp.SUM, group=group)
+        if gmax is not None:
+            dist.all_reduce(gmax, op=dist.ReduceOp.MAX, group=group)
+    return cost, gmax
+
+
+@dataclass
+class ChipResult:
+    cost: np.ndarray           # [iters] global cost per iteration
+    gmax: np.ndarray           # [iters] global max |dL/dtheta|
+    tiles: range               # this rank's tiles
+    mask: Optional[np.ndarray] = None  # [n_mine, n, n] final masks (if requested)
+
+
+class ChipIlt:
+    """ILT of this rank's shard of a tiled chip layout, tiles batched into one
+    device launch sequence (blockIdx.z = tile)."""
+
+    def __init__(self, tiling, polys: Sequence[np.ndarray], kernels, params, ctx, rank: int = 0,
+                 world: int = 1, dbu_per_nm: float = 1.0):
+        import torch
+
+        from . import api
+        from .layouts import polygon_arrays
+        self.tiling = tiling
+        self.rank, self.world = rank, world
+        self.mine = shard(len(tiling), world, rank)
+        self.ctx = ctx
+        n = tiling.n
+        dev = torch.device("cuda", ctx.device)
+        self.target = torch.empty((len(self.mine), n, n), dtype=torch.float64, device=dev)
+        for j, t in enumerate(self.mine):
+            g = tiling.tile_grid(t)
+            tp = tiling.tile_polygons(polys, t, dbu_per_nm)
+            xy, st = polygon_arrays(tp)
+            _raster(ctx, g, xy, st, self.target[j], dbu_per_nm)
+        self.solver = api.IltSolver(kernels, params, max(1, len(self.mine)), "f32", ctx)
+        self.target32 = self.target.float().contiguous()
+        self.solver.set_tiles(self.target32)
+
+    def run(self, iters: int, want_mask: bool = False) -> ChipResult:
+        import torch
+        dev = self.target.device
+        cost = torch.zeros((iters, self.solver.n_tiles), dtype=torch.float64, device=dev)
+        gl_cost = torch.zeros(iters, dtype=torch.float64, device=dev)
+        for it in range(iters):
+            self.solver.run_device(1, cost[it])
+            gl_cost[it] = cost[it].sum()
+            allreduce_scalars(gl_cost[it:it + 1], None)
+        res = ChipResult(gl_cost.cpu().numpy(), np.zeros(iters), self.mine)
+        if want_mask:
+            _, m = self.solver.get_tiles()
+            res.mask = m
+        return res
+
+
+def _raster(ctx, grid, xy, starts, out_dev, dbu):
+    import ctypes as C
+
+    from ._lib import check, lib
+    g = grid.c()
+    check(lib().lithogpu_rasterize(ctx.handle, C.byref(g), xy.ctypes.data, starts.ctypes.data,
+                                   len(starts) - 1, dbu, out_dev.data_ptr()))
