@@ -117,6 +117,12 @@ lithogpu_status lithogpu_gaussian_blur(lithogpu_ctx* ctx, const lithogpu_grid* g
                                        const void* in, lithogpu_dtype dtype, double sigma_nm,
                                        void* out);
 
+/* fft2 (imaging.cpp:17-31): in-place 2-D DFT of ny rows of nx interleaved
+ * complex values (dtype F64: complex128, F32: complex64); forward e^{-i},
+ * inverse e^{+i}, both unnormalized.  Any sizes. */
+lithogpu_status lithogpu_fft2(lithogpu_ctx* ctx, void* data, lithogpu_dtype dtype, int nx, int ny,
+                              int inverse);
+
 /* z_print / threshold semantics (ai.cpp:85-94): out[i] = in[i] >= tau ? 1 : 0 */
 lithogpu_status lithogpu_threshold(lithogpu_ctx* ctx, size_t n, const void* in,
                                    lithogpu_dtype in_dtype, double tau, void* out,

@@ -61,6 +61,7 @@ _SIGS = {
                                         C.c_double, _vp, _vp, C.c_int, _vp]),
     "lithogpu_gaussian_blur": (C.c_int, [_vp, C.POINTER(Grid), _vp, C.c_int, C.c_double, _vp]),
     "lithogpu_threshold": (C.c_int, [_vp, C.c_size_t, _vp, C.c_int, C.c_double, _vp, C.c_int]),
+    "lithogpu_fft2": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int]),
     "lithogpu_intensity_gradient": (C.c_int, [_vp, C.c_int, _vp, C.c_int, _vp, C.c_int,
                                               C.c_double, _vp, C.c_int]),
     "lithogpu_ilt_create": (C.c_int, [_vp, C.POINTER(IltParams), C.c_int, C.POINTER(_vp)]),

@@ -1421,6 +1421,65 @@ lithogpu_status lithogpu_gaussian_blur(lithogpu_ctx* ctx, const lithogpu_grid* g
   });
 }
 
+lithogpu_status lithogpu_fft2(lithogpu_ctx* ctx, void* data, lithogpu_dtype dtype, int nx, int ny,
+                              int inverse) {
+  if (!ctx || !data) {
+    g_last_error = "lithogpu_fft2: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    require(dtype == LITHOGPU_F32 || dtype == LITHOGPU_F64, "fft2: dtype must be F32 or F64");
+    if (nx <= 0 || ny <= 0) throw std::invalid_argument("fft2: size mismatch");
+    ctx->activate();
+    auto run = [&](auto tag) {
+      using T = decltype(tag);
+      using C = lg::cx<T>;
+      const size_t n = size_t(nx) * ny;
+      const bool dev = is_device_ptr(data);
+      C* d = static_cast<C*>(data);
+      if (!dev) {
+        DevBuf& b = ctx->slot(13);
+        b.ensure(n * sizeof(C));
+        LG_CUDA(cudaMemcpyAsync(b.p, data, n * sizeof(C), cudaMemcpyHostToDevice, ctx->stream));
+        d = b.as<C>();
+      }
+      DevBuf& tx = ctx->slot(14);
+      DevBuf& ty = ctx->slot(15);
+      make_twiddles<T>(nx, tx);
+      make_twiddles<T>(ny, ty);
+      auto tab = [](int L, DevBuf& b) {
+        lg::Tab<T> t;
+        t.tw = b.as<C>();
+        t.L = L;
+        t.log2L = lg::fast_len<T>(L) ? lg::ilog2(L) : -1;
+        return t;
+      };
+      const Launch lr = launch_cfg<T>(nx, 0), lc = launch_cfg<T>(ny, 0);
+      ctx->smem_attr(lg::k_fft2_rows<T, -1>, lr.smem);
+      ctx->smem_attr(lg::k_fft2_rows<T, +1>, lr.smem);
+      ctx->smem_attr(lg::k_fft2_cols<T, -1>, lc.smem);
+      ctx->smem_attr(lg::k_fft2_cols<T, +1>, lc.smem);
+      if (inverse) {
+        lg::k_fft2_rows<T, +1><<<dim3(cdiv(ny, lr.RPC)), lr.block, lr.smem, ctx->stream>>>(tab(nx, tx), nx, ny, d);
+        ctx->check_launch();
+        lg::k_fft2_cols<T, +1><<<dim3(cdiv(nx, lc.RPC)), lc.block, lc.smem, ctx->stream>>>(tab(ny, ty), nx, ny, d);
+      } else {
+        lg::k_fft2_rows<T, -1><<<dim3(cdiv(ny, lr.RPC)), lr.block, lr.smem, ctx->stream>>>(tab(nx, tx), nx, ny, d);
+        ctx->check_launch();
+        lg::k_fft2_cols<T, -1><<<dim3(cdiv(nx, lc.RPC)), lc.block, lc.smem, ctx->stream>>>(tab(ny, ty), nx, ny, d);
+      }
+      ctx->check_launch();
+      if (!dev)
+        LG_CUDA(cudaMemcpyAsync(data, d, n * sizeof(C), cudaMemcpyDeviceToHost, ctx->stream));
+      LG_CUDA(cudaStreamSynchronize(ctx->stream));
+    };
+    if (dtype == LITHOGPU_F32)
+      run(float{});
+    else
+      run(double{});
+  });
+}
+
 lithogpu_status lithogpu_threshold(lithogpu_ctx* ctx, size_t n, const void* in,
                                    lithogpu_dtype in_dtype, double tau, void* out,
                                    lithogpu_dtype out_dtype) {

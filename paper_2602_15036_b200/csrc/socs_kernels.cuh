@@ -780,4 +780,36 @@ __global__ void k_grad_rows(Geo<T> g, const cx<T>* __restrict__ Gc, long long g_
   }
 }
 
+// ===========================================================================
+// Plain batched 2-D DFT (the reference fft2, imaging.cpp:17-31: unnormalized,
+// x contiguous): rows then columns, any lengths (generic path).
+// ===========================================================================
+template <typename T, int SIGN>
+__global__ void k_fft2_rows(Tab<T> tab, int nx, int ny, cx<T>* __restrict__ data) {
+  Group<T> grp(nx, 0);
+  const int y = blockIdx.x * (blockDim.x / grp.G) + grp.gid;
+  const Row<T> row = grp.row(0, tab, y < ny);
+  cx<T>* d = data + size_t(blockIdx.z) * nx * ny + size_t(y) * nx;
+  if (row.active)
+    for (int i = row.t; i < nx; i += row.TPR) row.st(i, d[i]);
+  row.sync();
+  fft<T, SIGN>(row);
+  if (row.active)
+    for (int i = row.t; i < nx; i += row.TPR) d[i] = row.ld(i);
+}
+
+template <typename T, int SIGN>
+__global__ void k_fft2_cols(Tab<T> tab, int nx, int ny, cx<T>* __restrict__ data) {
+  Group<T> grp(ny, 0);
+  const int x = blockIdx.x * (blockDim.x / grp.G) + grp.gid;
+  const Row<T> row = grp.row(0, tab, x < nx);
+  cx<T>* d = data + size_t(blockIdx.z) * nx * ny + x;
+  if (row.active)
+    for (int i = row.t; i < ny; i += row.TPR) row.st(i, d[size_t(i) * nx]);
+  row.sync();
+  fft<T, SIGN>(row);
+  if (row.active)
+    for (int i = row.t; i < ny; i += row.TPR) d[size_t(i) * nx] = row.ld(i);
+}
+
 }  // namespace lg

@@ -1,0 +1,35 @@
+#!/usr/bin/env bash
+# TEST INFRASTRUCTURE ONLY.  Links the reference's OWN, UNMODIFIED test suites
+# (test_imaging, test_geometry, test_opc_ai — compiled from /root/reference,
+# never copied) against the drop-in: our paper_2602_15036_b200/host/litho_dropin.cpp
+# replaces the reference imaging.cpp + raster.cpp, every other reference
+# translation unit (geometry, booleans, OPC, ai, ...) is kept as is.
+# Output: tests/cpp/_bin/{test_imaging,test_geometry,test_opc_ai} (git-ignored,
+# travels to the GPU box; run by tests/test_dropin_cpp.py on the GPU).
+set -euo pipefail
+HERE="$(cd "$(dirname "${BASH_SOURCE[0]}")" && pwd)"
+ROOT="$(cd "$HERE/../.." && pwd)"
+REF="${LITHO_REFERENCE:-/root/reference/proj}"
+OUT="$HERE/_bin"
+if [ ! -d "$REF/src/core" ]; then
+  echo "build_dropin_tests: reference sources not found at $REF (skipped)" >&2
+  exit 0
+fi
+mkdir -p "$OUT/obj"
+CUDA=/usr/local/cuda
+INC="-I$REF/src -I$REF/src/core -I$ROOT/include -I$CUDA/include"
+CXX="g++ -O2 -std=c++20 -fPIC"
+pids=()
+for s in geometry bvh boolean contour segment mrc opc ai; do
+  $CXX $INC -c "$REF/src/core/$s.cpp" -o "$OUT/obj/ref_$s.o" & pids+=($!)
+done
+$CXX $INC -c "$ROOT/paper_2602_15036_b200/host/litho_dropin.cpp" -o "$OUT/obj/litho_dropin.o" & pids+=($!)
+for t in test_imaging test_geometry test_opc_ai; do
+  $CXX $INC -I"$HERE" -I"$REF/tests" -I"$ROOT/oracle/shim" -c "$REF/tests/$t.cpp" -o "$OUT/obj/$t.o" & pids+=($!)
+done
+for p in "${pids[@]}"; do wait "$p"; done
+LIBS="-L$ROOT/paper_2602_15036_b200 -llithogpu -Wl,-rpath,$ROOT/paper_2602_15036_b200 -Wl,-rpath,\$ORIGIN/../../../paper_2602_15036_b200 -L$CUDA/lib64 -lcusolver -lcudart"
+for t in test_imaging test_geometry test_opc_ai; do
+  g++ -o "$OUT/$t" "$OUT/obj/$t.o" "$OUT/obj/litho_dropin.o" "$OUT"/obj/ref_*.o $LIBS
+done
+echo "build_dropin_tests: $OUT"
