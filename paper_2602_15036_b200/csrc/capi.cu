@@ -302,7 +302,7 @@ struct OutStage {
 // Decimation d: the largest divisor of N whose grid n = N/d still holds the
 // intensity band without aliasing (n >= 2P+1) and keeps n >= 32 (fast-path
 // transform range).  No such d -> full band on the N grid.
-lg::AxisGeom make_axis(int N, int lo, int hi) {
+lg::AxisGeom make_axis(int N, int lo, int hi, bool mixed = false) {
   lg::AxisGeom a{};
   a.N = N;
   a.lo = lo;
@@ -310,6 +310,23 @@ lg::AxisGeom make_axis(int N, int lo, int hi) {
   a.B = hi - lo + 1;
   a.Pm = std::max(-lo, hi);
   const int P0 = a.B - 1;
+  if (mixed) {
+    // fp32 fast path: any supported FFT length n >= 2P+1 works (the samples
+    // s N/n of the trigonometric polynomial need not be integer pixels)
+    const bool pow2_only = std::getenv("LITHOGPU_POW2_SUBGRID") != nullptr;
+    for (int n : lg::kFastLens) {
+      if (n > N) break;
+      if (pow2_only && !lg::is_pow2(n)) continue;
+      if (n >= 2 * P0 + 1 && n >= std::min(N, 32)) {
+        a.d = N % n == 0 ? N / n : 0;  // informational (0: fractional decimation)
+        a.n = n;
+        a.full = 0;
+        a.P = P0;
+        a.nb2 = 2 * P0 + 1;
+        return a;
+      }
+    }
+  }
   int best = 0;
   for (int d = N; d >= 1; --d) {
     if (N % d) continue;
@@ -418,8 +435,8 @@ struct Plan : PlanBase {
   // fp32 fast path (power-of-two tiles, register FFT kernels of socs_fast.cuh)
   bool fast = false;
   lg::FGeo fg{};
-  DevBuf ftNx, ftNy, ftnx, ftny, Wsub, Ih, Rh, Wh;
-  long long s_Wsub = 0, s_band = 0;
+  DevBuf ftNx, ftNy, ftnx, ftny, Wsub, Ih, Rh, Wh, Ip, AccS;
+  long long s_Wsub = 0, s_band = 0, s_Ip = 0, s_AccS = 0;
 
   Plan(lithogpu_ctx* c, const lithogpu_grid& gr, int F_, int K_, const double* weights, int S,
        const int32_t* support, const double* values)
@@ -439,8 +456,10 @@ struct Plan : PlanBase {
       loy = std::min(loy, b);
       hiy = std::max(hiy, b);
     }
-    g.ax = make_axis(Nx, lox, hix);
-    g.ay = make_axis(Ny, loy, hiy);
+    const bool mixed = std::is_same<T, float>::value && lg::fast_len_ok(Nx) && lg::fast_len_ok(Ny) &&
+                       !std::getenv("LITHOGPU_GENERIC");
+    g.ax = make_axis(Nx, lox, hix, mixed);
+    g.ay = make_axis(Ny, loy, hiy, mixed);
     g.F = F;
     g.K = K;
     auto tab = [&](int L, DevBuf& b) {
@@ -482,37 +501,35 @@ struct Plan : PlanBase {
     s_Dr = (long long)F * (ax.P + 1) * Ny;
     s_Wc = (long long)F * ay.n * (ax.P + 1);
     s_U = (long long)F * K * Bx * ay.n;
-    s_Acc = (long long)By * Bx;
+    s_Acc = (long long)F * K * By * Bx;  // fast path keeps per-(f,k) partials
     s_Gc = (long long)Ny * (ax.Pm + 1);
     s_cr = (long long)F * Ny;
     s_gm = (long long)(Ny + 1) / 2;
     if constexpr (std::is_same<T, float>::value) {
-      auto ok = [](int L) { return lg::is_pow2(L) && lg::fast_log2_ok(lg::ilog2(L)); };
+      auto ok = [](int L) { return lg::fast_len_ok(L); };
       fast = ok(Nx) && ok(Ny) && ok(ax.n) && ok(ay.n) && !std::getenv("LITHOGPU_GENERIC");
       if (fast) {
         fg.ax = ax;
         fg.ay = ay;
         fg.F = F;
         fg.K = K;
-        fg.lgNx = lg::ilog2(Nx);
-        fg.lgNy = lg::ilog2(Ny);
-        fg.lgnx = lg::ilog2(ax.n);
-        fg.lgny = lg::ilog2(ay.n);
-        auto table = [](int lgL, DevBuf& b) {
-          std::vector<lg::C32> h(std::max(1, lg::fast_tw_len(lgL)));
-          lg::fast_fill_twiddles(lgL, h.data());
+        auto table = [](int len, DevBuf& b) {
+          std::vector<lg::C32> h(std::max(1, lg::fast_tw_len(len)));
+          lg::fast_fill_twiddles(len, h.data());
           b.ensure(h.size() * sizeof(lg::C32));
           LG_CUDA(cudaMemcpy(b.p, h.data(), h.size() * sizeof(lg::C32), cudaMemcpyHostToDevice));
           return b.as<lg::C32>();
         };
-        fg.twNx = table(fg.lgNx, ftNx);
-        fg.twNy = table(fg.lgNy, ftNy);
-        fg.twnx = table(fg.lgnx, ftnx);
-        fg.twny = table(fg.lgny, ftny);
+        fg.twNx = table(Nx, ftNx);
+        fg.twNy = table(Ny, ftNy);
+        fg.twnx = table(ax.n, ftnx);
+        fg.twny = table(ay.n, ftny);
         s_Wsub = (long long)F * ay.n * ax.n;
         s_band = (long long)F * ay.nb2 * (ax.P + 1);
+        s_Ip = (long long)F * K * ay.n * ax.n;
+        s_AccS = (long long)By * Bx;
         const long long npairs = (Ny + 1) / 2;
-        const long long wpg = std::max(1, lg::fast_tpr(fg.lgNx) / 32);
+        const long long wpg = std::max(1, lg::fast_tpr(Nx) / 32);
         s_cr = std::max(s_cr, F * npairs * wpg);
         s_gm = std::max(s_gm, npairs * wpg);
       }
@@ -562,10 +579,10 @@ struct Plan : PlanBase {
     if (fast) {
       Rh.ensure(c * s_band);
       Ih.ensure(c * s_band);
-      if (adjoint) {
-        Wh.ensure(c * s_band);
-        Wsub.ensure(sizeof(T) * size_t(cap) * s_Wsub);
-      }
+      Ip.ensure(sizeof(T) * size_t(cap) * s_Ip);
+      if (adjoint) AccS.ensure(c * s_AccS);
+      Wsub.ensure(sizeof(T) * size_t(cap) * s_Wsub);  // W_lp (adjoint) / I_sub (forward) scratch
+      if (adjoint) Wh.ensure(c * s_band);
     }
     Mr.ensure(c * s_Mr);
     Mhat.ensure(c * s_Mhat);
@@ -700,10 +717,13 @@ struct Plan : PlanBase {
     if constexpr (std::is_same<T, float>::value) {
       if (fast) {
         cudaStream_t s = ctx->stream;
+        lg::fast_set_pdl(true);
         fl("real_rows_fwd", [&] { lg::fl_real_rows_fwd(fg, s, tiles, 0, mask, m_ts, 0.f, g.ax.Pm, Mr.as<C>(), s_Mr); });
         fl("mask_cols", [&] { lg::fl_mask_cols(fg, s, tiles, Mr.as<C>(), s_Mr, Mhat.as<C>(), s_Mhat); });
         fl("socs_cols", [&] { lg::fl_socs_cols(fg, s, tiles, Mhat.as<C>(), s_Mhat, H.as<C>(), Tb.as<C>(), s_T); });
-        fl("socs_rows", [&] { lg::fl_socs_rows(fg, s, tiles, Tb.as<C>(), s_T, wk.as<T>(), dose, Ir.as<C>(), s_Ir); });
+        fl("socs_rows", [&] { lg::fl_socs_rows(fg, s, tiles, Tb.as<C>(), s_T, wk.as<T>(), dose, Ip.as<T>(), s_Ip); });
+        fl("ip_sum", [&] { lg::fl_ip_sum(fg, s, tiles, Ip.as<T>(), s_Ip, Wsub.as<T>(), s_Wsub); });
+        fl("isub_rows", [&] { lg::fl_isub_rows(fg, s, tiles, Wsub.as<T>(), s_Wsub, Ir.as<C>(), s_Ir); });
         fl("isub_colfwd", [&] {
           lg::fl_band_colfwd(fg, s, tiles, F, true, Ir.as<C>(), s_Ir, gxh.as<T>(), gyb.as<T>(),
                              want_r ? Rh.as<C>() : nullptr, want_i ? Ih.as<C>() : nullptr, s_band);
@@ -743,8 +763,9 @@ struct Plan : PlanBase {
           lg::fl_adj_rows(fg, s, 1, 1, W == nullptr, Tb.as<C>(), s_T, Wsub.as<T>(), s_Wsub, U.as<C>(), s_U);
         });
         fl("adj_cols", [&] { lg::fl_adj_cols(fg, s, 1, U.as<C>(), s_U, H.as<C>(), wk.as<T>(), dose, Acc.as<C>(), s_Acc); });
+        fl("acc_sum", [&] { lg::fl_acc_sum(fg, s, 1, Acc.as<C>(), AccS.as<C>(), s_AccS); });
         fl("grad_cols", [&] {
-          lg::fl_grad_cols(fg, s, 1, Acc.as<C>(), s_Acc, Gc.as<C>(), s_Gc, nullptr, 0, 0, nullptr, 0);
+          lg::fl_grad_cols(fg, s, 1, AccS.as<C>(), s_AccS, Gc.as<C>(), s_Gc, nullptr, 0, 0, nullptr, 0);
         });
         fl("grad_rows", [&] {
           lg::fl_grad_rows(fg, s, 1, false, Gc.as<C>(), s_Gc, grad, 0, nullptr, 0, 0.f, 0.f, Mr.as<C>(), s_Mr,
@@ -843,13 +864,16 @@ static void ilt_run_impl(lithogpu_ilt* ilt, int iters, double* cost_user, double
     if (P.fast) {
       cudaStream_t s = ctx->stream;
       const lg::FGeo& fg = P.fg;
+      lg::fast_set_pdl(false);  // PDL slows the graph-replayed ILT loop
       const int F = P.F;
       if (need_prime)
         P.fl("real_rows_fwd", [&] { lg::fl_real_rows_fwd(fg, s, tiles, 1, theta, NN, a, P.g.ax.Pm, P.Mr.template as<C>(), P.s_Mr); });
       for (int it = 0; it < iters; ++it) {
         P.fl("mask_cols", [&] { lg::fl_mask_cols(fg, s, tiles, P.Mr.template as<C>(), P.s_Mr, P.Mhat.template as<C>(), P.s_Mhat); });
         P.fl("socs_cols", [&] { lg::fl_socs_cols(fg, s, tiles, P.Mhat.template as<C>(), P.s_Mhat, P.H.template as<C>(), P.Tb.template as<C>(), P.s_T); });
-        P.fl("socs_rows", [&] { lg::fl_socs_rows(fg, s, tiles, P.Tb.template as<C>(), P.s_T, P.wk.template as<T>(), dose, P.Ir.template as<C>(), P.s_Ir); });
+        P.fl("socs_rows", [&] { lg::fl_socs_rows(fg, s, tiles, P.Tb.template as<C>(), P.s_T, P.wk.template as<T>(), dose, P.Ip.template as<T>(), P.s_Ip); });
+        P.fl("ip_sum", [&] { lg::fl_ip_sum(fg, s, tiles, P.Ip.template as<T>(), P.s_Ip, P.Wsub.template as<T>(), P.s_Wsub); });
+        P.fl("isub_rows", [&] { lg::fl_isub_rows(fg, s, tiles, P.Wsub.template as<T>(), P.s_Wsub, P.Ir.template as<C>(), P.s_Ir); });
         P.fl("isub_colfwd", [&] {
           lg::fl_band_colfwd(fg, s, tiles, F, true, P.Ir.template as<C>(), P.s_Ir, P.gxh.template as<T>(),
                              P.gyb.template as<T>(), P.Rh.template as<C>(), nullptr, P.s_band);
@@ -874,9 +898,10 @@ static void ilt_run_impl(lithogpu_ilt* ilt, int iters, double* cost_user, double
                           P.Acc.template as<C>(), P.s_Acc);
         });
         const long long npairs = (P.g.ay.N + 1) / 2;
-        const int ncost = int(std::min<long long>(P.s_cr, F * npairs * std::max(1, lg::fast_tpr(fg.lgNx) / 32)));
+        const int ncost = int(std::min<long long>(P.s_cr, F * npairs * std::max(1, lg::fast_tpr(P.g.ax.N) / 32)));
+        P.fl("acc_sum", [&] { lg::fl_acc_sum(fg, s, tiles, P.Acc.template as<C>(), P.AccS.template as<C>(), P.s_AccS); });
         P.fl("grad_cols", [&] {
-          lg::fl_grad_cols(fg, s, tiles, P.Acc.template as<C>(), P.s_Acc, P.Gc.template as<C>(), P.s_Gc,
+          lg::fl_grad_cols(fg, s, tiles, P.AccS.template as<C>(), P.s_AccS, P.Gc.template as<C>(), P.s_Gc,
                            P.costrow.template as<double>(), P.s_cr, ncost, ilt->cost.as<double>() + size_t(it) * tiles, 1);
         });
         P.fl("grad_rows", [&] {
@@ -884,7 +909,7 @@ static void ilt_run_impl(lithogpu_ilt* ilt, int iters, double* cost_user, double
                            P.Mr.template as<C>(), P.s_Mr, P.gmaxrow.template as<double>(), P.s_gm);
         });
         if (gmax_user) {
-          const int ngm = int(npairs * std::max(1, lg::fast_tpr(fg.lgNx) / 32));
+          const int ngm = int(npairs * std::max(1, lg::fast_tpr(P.g.ax.N) / 32));
           lg::k_reduce_max<<<tiles, 32, 0, ctx->stream>>>(P.gmaxrow.template as<double>(), P.s_gm, ngm,
                                                          ilt->gmax.as<double>() + size_t(it) * tiles);
           ctx->check_launch();

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <type_traits>
@@ -12,25 +13,23 @@
 namespace lg {
 
 template <typename F>
-inline void with_lg(int lg, F&& f) {
-  switch (lg) {
-    case 5: f(std::integral_constant<int, 5>()); break;
-    case 6: f(std::integral_constant<int, 6>()); break;
-    case 7: f(std::integral_constant<int, 7>()); break;
-    case 8: f(std::integral_constant<int, 8>()); break;
-    case 9: f(std::integral_constant<int, 9>()); break;
-    case 10: f(std::integral_constant<int, 10>()); break;
-    case 11: f(std::integral_constant<int, 11>()); break;
-    case 12: f(std::integral_constant<int, 12>()); break;
-    case 13: f(std::integral_constant<int, 13>()); break;
-    default: throw std::runtime_error("fast path: unsupported transform length 2^" + std::to_string(lg));
+inline void with_len(int len, F&& f) {
+  switch (len) {
+#define LG_CASE(X) \
+  case X:          \
+    f(std::integral_constant<int, X>()); \
+    break;
+    LG_CASE(32) LG_CASE(64) LG_CASE(128) LG_CASE(192) LG_CASE(256) LG_CASE(384) LG_CASE(512)
+    LG_CASE(768) LG_CASE(1024) LG_CASE(1536) LG_CASE(2048) LG_CASE(3072) LG_CASE(4096) LG_CASE(8192)
+#undef LG_CASE
+    default: throw std::runtime_error("fast path: unsupported transform length " + std::to_string(len));
   }
 }
 
 // groups of TPR threads per CTA: ~target threads, capped so named barriers fit
-template <int LG>
+template <int L>
 inline int fgroups(int target, int cap = 1 << 30) {
-  constexpr int TPR = RPlan<LG>::TPR;
+  constexpr int TPR = RPlan<L>::TPR;
   int gr = target / TPR;
   if (gr < 1) gr = 1;
   if (gr > cap) gr = cap;
@@ -38,15 +37,46 @@ inline int fgroups(int target, int cap = 1 << 30) {
   return gr;
 }
 
-template <int LG, typename K, typename... A>
-inline void flaunch(K kern, dim3 grid, int groups, cudaStream_t s, A... args) {
-  const size_t smem = size_t(groups) * rsm_len<LG>() * sizeof(C32);
+// launch with `extra` bytes of shared memory after the row-group buffers
+template <int L, typename K, typename... A>
+inline void flaunch_x(K kern, dim3 grid, int groups, size_t extra, cudaStream_t s, A... args) {
+  const size_t smem = size_t(groups) * rsm_len<L>() * sizeof(C32) + extra;
   static size_t set_bytes = 0;  // per instantiation
   if (smem > 48 * 1024 && smem > set_bytes) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     set_bytes = smem;
   }
-  kern<<<grid, groups * RPlan<LG>::TPR, smem, s>>>(args...);
+  pdl_launch(kern, grid, dim3(groups * RPlan<L>::TPR), smem, s, args...);
+}
+
+template <int L, typename K, typename... A>
+inline void flaunch(K kern, dim3 grid, int groups, cudaStream_t s, A... args) {
+  flaunch_x<L>(kern, grid, groups, 0, s, args...);
+}
+
+// PDL measured: +15% on the forward imaging chain, -8% on the graph-replayed
+// ILT loop, so callers switch it per path.
+inline bool& pdl_enabled() {
+  thread_local bool on = true;
+  return on;
+}
+
+// launch with programmatic stream serialization (PDL; LITHOGPU_NO_PDL=1 disables)
+template <typename K, typename... A>
+inline void pdl_launch(K kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s, A... args) {
+  static const bool env_off = std::getenv("LITHOGPU_NO_PDL") != nullptr;
+  const bool on = pdl_enabled() && !env_off;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = on ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
 inline int cdivi(long long a, long long b) { return int((a + b - 1) / b); }

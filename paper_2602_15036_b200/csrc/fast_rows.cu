@@ -5,20 +5,22 @@
 
 namespace lg {
 
-int fast_tw_len(int lg) {
+int fast_tw_len(int len) {
   int n = 0;
-  with_lg(lg, [&](auto c) { n = TwLen<decltype(c)::value>::value; });
+  with_len(len, [&](auto c) { n = TwLen<decltype(c)::value>::value; });
   return n;
 }
 
-int fast_tpr(int lg) {
+void fast_set_pdl(bool on) { pdl_enabled() = on; }
+
+int fast_tpr(int len) {
   int n = 0;
-  with_lg(lg, [&](auto c) { n = RPlan<decltype(c)::value>::TPR; });
+  with_len(len, [&](auto c) { n = RPlan<decltype(c)::value>::TPR; });
   return n;
 }
 
-void fast_fill_twiddles(int lg, C32* out) {
-  with_lg(lg, [&](auto c) {
+void fast_fill_twiddles(int len, C32* out) {
+  with_len(len, [&](auto c) {
     fill_rtwiddles<decltype(c)::value>([&](int idx, int rk, int NsR) {
       const double a = 2.0 * M_PI * double(rk) / double(NsR);
       out[idx].x = float(std::cos(a));
@@ -29,33 +31,55 @@ void fast_fill_twiddles(int lg, C32* out) {
 
 void fl_real_rows_fwd(const FGeo& g, cudaStream_t s, int tiles, int mode, const float* src,
                       long long src_ts, float steep, int Pout, C32* out, long long out_ts) {
-  with_lg(g.lgNx, [&](auto c) {
-    constexpr int LG = decltype(c)::value;
-    const int gr = fgroups<LG>(256);
+  with_len(g.ax.N, [&](auto c) {
+    constexpr int L = decltype(c)::value;
+    const int gr = fgroups<L>(256);
     const dim3 grid(cdivi((g.ay.N + 1) / 2, gr), 1, tiles);
     if (mode == 0)
-      flaunch<LG>(fk_real_rows_fwd<LG, 0>, grid, gr, s, g, src, src_ts, steep, Pout, out, out_ts);
+      flaunch<L>(fk_real_rows_fwd<L, 0>, grid, gr, s, g, src, src_ts, steep, Pout, out, out_ts);
     else
-      flaunch<LG>(fk_real_rows_fwd<LG, 1>, grid, gr, s, g, src, src_ts, steep, Pout, out, out_ts);
+      flaunch<L>(fk_real_rows_fwd<L, 1>, grid, gr, s, g, src, src_ts, steep, Pout, out, out_ts);
   });
 }
 
 void fl_socs_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* T, long long t_ts,
-                  const float* wk, float dose, C32* Ir, long long ir_ts) {
-  with_lg(g.lgnx, [&](auto c) {
-    constexpr int LG = decltype(c)::value;
-    const int gr = fgroups<LG>(512, g.K);
-    flaunch<LG>(fk_socs_rows<LG>, dim3(g.ay.n, g.F, tiles), gr, s, g, T, t_ts, wk, dose, Ir, ir_ts);
+                  const float* wk, float dose, float* Ip, long long ip_ts) {
+  with_len(g.ax.n, [&](auto c) {
+    constexpr int L = decltype(c)::value;
+    const int gr = fgroups<L>(256);
+    flaunch<L>(fk_socs_rows<L>, dim3(cdivi(g.ay.n, gr), g.F * g.K, tiles), gr, s, g, T, t_ts, wk, dose, Ip,
+               ip_ts);
   });
+}
+
+void fl_isub_rows(const FGeo& g, cudaStream_t s, int tiles, const float* Ip, long long ip_ts, C32* Ir,
+                  long long ir_ts) {
+  with_len(g.ax.n, [&](auto c) {
+    constexpr int L = decltype(c)::value;
+    const int gr = fgroups<L>(256);
+    flaunch<L>(fk_isub_rows<L>, dim3(cdivi((g.ay.n + 1) / 2, gr), g.F, tiles), gr, s, g, Ip, ip_ts, Ir,
+               ir_ts);
+  });
+}
+
+void fl_ip_sum(const FGeo& g, cudaStream_t s, int tiles, const float* Ip, long long ip_ts, float* Isub,
+               long long is_ts) {
+  const int n4 = (g.ay.n * g.ax.n) / 4;
+  pdl_launch(fk_ip_sum, dim3(cdivi(n4, 256), g.F, tiles), dim3(256), 0, s, g, Ip, ip_ts, Isub, is_ts);
+}
+
+void fl_acc_sum(const FGeo& g, cudaStream_t s, int tiles, const C32* Accp, C32* Acc, long long a_ts) {
+  const int n = g.ax.B * g.ay.B;
+  pdl_launch(fk_acc_sum, dim3(cdivi(n, 256), 1, tiles), dim3(256), 0, s, g, Accp, Acc, a_ts);
 }
 
 void fl_resist_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* Rc, long long c_ts,
                     const float* target, long long tg_ts, const float* cf, float beta, float thr,
                     C32* Dr, long long d_ts, double* costp, long long cp_ts) {
-  with_lg(g.lgNx, [&](auto c) {
-    constexpr int LG = decltype(c)::value;
-    const int gr = fgroups<LG>(256);
-    flaunch<LG>(fk_resist_rows<LG>, dim3(cdivi((g.ay.N + 1) / 2, gr), g.F, tiles), gr, s, g, Rc,
+  with_len(g.ax.N, [&](auto c) {
+    constexpr int L = decltype(c)::value;
+    const int gr = fgroups<L>(256);
+    flaunch<L>(fk_resist_rows<L>, dim3(cdivi((g.ay.N + 1) / 2, gr), g.F, tiles), gr, s, g, Rc,
                 c_ts, target, tg_ts, cf, beta, thr, Dr, d_ts, costp, cp_ts);
   });
 }
@@ -63,49 +87,50 @@ void fl_resist_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* Rc, lon
 void fl_out_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* Ic, const C32* Rc,
                  long long c_ts, float* Iout, float* Rout, unsigned char* print, long long o_ts,
                  float thr) {
-  with_lg(g.lgNx, [&](auto c) {
-    constexpr int LG = decltype(c)::value;
-    const int gr = fgroups<LG>(256);
-    flaunch<LG>(fk_out_rows<LG>, dim3(cdivi(g.ay.N, gr), g.F, tiles), gr, s, g, Ic, Rc, c_ts, Iout,
+  with_len(g.ax.N, [&](auto c) {
+    constexpr int L = decltype(c)::value;
+    const int gr = fgroups<L>(256);
+    flaunch<L>(fk_out_rows<L>, dim3(cdivi(g.ay.N, gr), g.F, tiles), gr, s, g, Ic, Rc, c_ts, Iout,
                 Rout, print, o_ts, thr);
   });
 }
 
 void fl_wlp_rows(const FGeo& g, cudaStream_t s, int tiles, int nf, const C32* Wc, long long w_ts,
                  float* Wsub, long long ws_ts) {
-  with_lg(g.lgnx, [&](auto c) {
-    constexpr int LG = decltype(c)::value;
-    const int gr = fgroups<LG>(256);
-    flaunch<LG>(fk_wlp_rows<LG>, dim3(cdivi((g.ay.n + 1) / 2, gr), nf, tiles), gr, s, g, Wc, w_ts,
+  with_len(g.ax.n, [&](auto c) {
+    constexpr int L = decltype(c)::value;
+    const int gr = fgroups<L>(256);
+    flaunch<L>(fk_wlp_rows<L>, dim3(cdivi((g.ay.n + 1) / 2, gr), nf, tiles), gr, s, g, Wc, w_ts,
                 Wsub, ws_ts);
   });
 }
 
 void fl_adj_rows(const FGeo& g, cudaStream_t s, int tiles, int nf, bool uniform, const C32* T,
                  long long t_ts, const float* Wsub, long long ws_ts, C32* U, long long u_ts) {
-  with_lg(g.lgnx, [&](auto c) {
-    constexpr int LG = decltype(c)::value;
-    const int gr = fgroups<LG>(256);
+  with_len(g.ax.n, [&](auto c) {
+    constexpr int L = decltype(c)::value;
+    const int gr = fgroups<L>(256);
     const dim3 grid(cdivi(g.ay.n, gr), nf * g.K, tiles);
+    const size_t extra = size_t(g.ax.B) * (gr | 1) * sizeof(C32);  // staging tile
     if (uniform)
-      flaunch<LG>(fk_adj_rows<LG, true>, grid, gr, s, g, T, t_ts, Wsub, ws_ts, U, u_ts);
+      flaunch_x<L>(fk_adj_rows<L, true>, grid, gr, extra, s, g, T, t_ts, Wsub, ws_ts, U, u_ts);
     else
-      flaunch<LG>(fk_adj_rows<LG, false>, grid, gr, s, g, T, t_ts, Wsub, ws_ts, U, u_ts);
+      flaunch_x<L>(fk_adj_rows<L, false>, grid, gr, extra, s, g, T, t_ts, Wsub, ws_ts, U, u_ts);
   });
 }
 
 void fl_grad_rows(const FGeo& g, cudaStream_t s, int tiles, bool ilt, const C32* Gc, long long g_ts,
                   float* grad, long long gr_ts, float* theta, long long th_ts, float steep,
                   float step, C32* Mr, long long mr_ts, double* gmaxp, long long gm_ts) {
-  with_lg(g.lgNx, [&](auto c) {
-    constexpr int LG = decltype(c)::value;
-    const int gr = fgroups<LG>(256);
+  with_len(g.ax.N, [&](auto c) {
+    constexpr int L = decltype(c)::value;
+    const int gr = fgroups<L>(256);
     const dim3 grid(cdivi((g.ay.N + 1) / 2, gr), 1, tiles);
     if (ilt)
-      flaunch<LG>(fk_grad_rows<LG, true>, grid, gr, s, g, Gc, g_ts, grad, gr_ts, theta, th_ts, steep,
+      flaunch<L>(fk_grad_rows<L, true>, grid, gr, s, g, Gc, g_ts, grad, gr_ts, theta, th_ts, steep,
                   step, Mr, mr_ts, gmaxp, gm_ts);
     else
-      flaunch<LG>(fk_grad_rows<LG, false>, grid, gr, s, g, Gc, g_ts, grad, gr_ts, theta, th_ts,
+      flaunch<L>(fk_grad_rows<L, false>, grid, gr, s, g, Gc, g_ts, grad, gr_ts, theta, th_ts,
                   steep, step, Mr, mr_ts, gmaxp, gm_ts);
   });
 }

@@ -110,6 +110,9 @@ __host__ __device__ inline int tpr_for(int L) {
   return t < 1 ? 1 : t;
 }
 
+// lengths of the compile-time-planned fp32 fast path (fftr.cuh), ascending
+constexpr int kFastLens[] = {32, 64, 128, 192, 256, 384, 512, 768, 1024, 1536, 2048, 3072, 4096, 8192};
+
 // Row-group context: one length-L row in smem, processed by TPR threads.
 template <typename T>
 struct Row {
@@ -231,15 +234,93 @@ __device__ __forceinline__ void dft16(cx<T>* v) {
   }
 }
 
+// radix 3: y1,2 = x0 - (x1+x2)/2 +- S i sqrt(3)/2 (x1 - x2)
+template <int S, typename T>
+__device__ __forceinline__ void dft3(cx<T>& x0, cx<T>& x1, cx<T>& x2) {
+  const T h = T(0.86602540378443864676);
+  const cx<T> s = add(x1, x2);
+  const cx<T> d = sub(x1, x2);
+  const cx<T> m = mk(x0.x - T(0.5) * s.x, x0.y - T(0.5) * s.y);
+  const cx<T> r = S < 0 ? mk(h * d.y, -h * d.x) : mk(-h * d.y, h * d.x);  // (S i h) d
+  x0 = add(x0, s);
+  x1 = add(m, r);
+  x2 = sub(m, r);
+}
+
+// multiply by exp(S 2 pi i q / R) for R in {6, 12}
+template <int R, int Q, int S, typename T>
+__device__ __forceinline__ cx<T> twc3(cx<T> a) {
+  constexpr int q = Q % R;
+  if constexpr (q == 0) {
+    return a;
+  } else if constexpr (4 * q == R) {
+    return mul_si<S>(a);
+  } else {
+    constexpr double PI = 3.14159265358979323846;
+    // cos/sin of 2 pi q / R for the few angles used (multiples of 30 degrees)
+    constexpr int deg = 360 * q / R;
+    constexpr double c = deg == 30 ? 0.86602540378443864676 : deg == 60 ? 0.5 : deg == 120 ? -0.5
+                       : deg == 150 ? -0.86602540378443864676 : 0.0;
+    constexpr double s = deg == 30 ? 0.5 : deg == 60 ? 0.86602540378443864676 : deg == 120
+                       ? 0.86602540378443864676 : deg == 150 ? 0.5 : 0.0;
+    (void)PI;
+    return mul(a, mk(T(c), T(S * s)));
+  }
+}
+
+template <int S, typename T>
+__device__ __forceinline__ void dft6(cx<T>* v) {
+  cx<T> e0 = v[0], e1 = v[2], e2 = v[4], o0 = v[1], o1 = v[3], o2 = v[5];
+  dft3<S>(e0, e1, e2);
+  dft3<S>(o0, o1, o2);
+  o1 = twc3<6, 1, S>(o1);
+  o2 = twc3<6, 2, S>(o2);
+  v[0] = add(e0, o0);
+  v[3] = sub(e0, o0);
+  v[1] = add(e1, o1);
+  v[4] = sub(e1, o1);
+  v[2] = add(e2, o2);
+  v[5] = sub(e2, o2);
+}
+
+template <int S, typename T>
+__device__ __forceinline__ void dft12(cx<T>* v) {
+  cx<T> e[6], o[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    e[i] = v[2 * i];
+    o[i] = v[2 * i + 1];
+  }
+  dft6<S>(e);
+  dft6<S>(o);
+  o[1] = twc3<12, 1, S>(o[1]);
+  o[2] = twc3<12, 2, S>(o[2]);
+  o[3] = twc3<12, 3, S>(o[3]);
+  o[4] = twc3<12, 4, S>(o[4]);
+  o[5] = twc3<12, 5, S>(o[5]);
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    v[i] = add(e[i], o[i]);
+    v[i + 6] = sub(e[i], o[i]);
+  }
+}
+
 template <int R, int S, typename T>
 __device__ __forceinline__ void dftR(cx<T>* v) {
   if constexpr (R == 2) {
     dft2<S>(v[0], v[1]);
+  } else if constexpr (R == 3) {
+    dft3<S>(v[0], v[1], v[2]);
   } else if constexpr (R == 4) {
     dft4<S>(v[0], v[1], v[2], v[3]);
+  } else if constexpr (R == 6) {
+    dft6<S>(v);
   } else if constexpr (R == 8) {
     dft8<S>(v);
+  } else if constexpr (R == 12) {
+    dft12<S>(v);
   } else {
+    static_assert(R == 16, "unsupported radix");
     dft16<S>(v);
   }
 }

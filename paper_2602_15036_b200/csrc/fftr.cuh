@@ -5,11 +5,13 @@
 // global loads/stores, band gathers/scatters straight from registers).  The
 // first Stockham stage reads its butterflies from that distribution and the
 // last one writes its outputs back into it, so an S-stage plan needs only
-// S-1 shared-memory exchanges (float2, one pad per 16 elements: conflict free
-// for every plan below except L = 512, 1.25 wavefronts).
-// Stage twiddles come from per-stage tables laid out [r-1][k] (k fastest) so a
-// warp's twiddle loads are contiguous; they are issued before the exchange
-// barrier so their latency hides behind it.
+// S-1 shared-memory exchanges.  Stage twiddles come from per-stage tables laid
+// out [r-1][k] (k fastest) so a warp's twiddle loads are contiguous; they are
+// issued before the exchange barrier so their latency hides behind it.
+//
+// Plans cover powers of two 32..8192 and 3*2^a (192..3072: the decimated
+// imaging grid only has to hold 2P+1 samples), with radices
+// 2, 3, 4, 6, 8, 12, 16 (every radix divides E).
 //
 // Conventions: reference fft2 (proj/src/core/imaging.cpp:17-31), SIGN -1
 // forward, +1 backward, unnormalized.
@@ -19,55 +21,61 @@
 
 namespace lg {
 
-template <int LOG2>
+template <int L>
 struct RPlan;
 
-#define LG_RPLAN(LG, EE, ...)                            \
+#define LG_RPLAN(LL, EE, ...)                            \
   template <>                                            \
-  struct RPlan<LG> {                                     \
-    static constexpr int L = 1 << LG;                    \
+  struct RPlan<LL> {                                     \
+    static constexpr int L = LL;                         \
     static constexpr int E = EE;                         \
-    static constexpr int TPR = L / EE;                   \
+    static constexpr int TPR = LL / EE;                  \
     static constexpr int R[] = {__VA_ARGS__};            \
     static constexpr int NS = sizeof(R) / sizeof(int);   \
   };
 
-LG_RPLAN(5, 8, 8, 4)
-LG_RPLAN(6, 8, 8, 8)
-LG_RPLAN(7, 16, 16, 8)
-LG_RPLAN(8, 16, 16, 16)
-LG_RPLAN(9, 8, 8, 8, 8)
-LG_RPLAN(10, 16, 16, 8, 8)
-LG_RPLAN(11, 16, 16, 16, 8)
-LG_RPLAN(12, 16, 16, 16, 16)
-LG_RPLAN(13, 16, 16, 16, 16, 2)
+LG_RPLAN(32, 8, 8, 4)
+LG_RPLAN(64, 8, 8, 8)
+LG_RPLAN(128, 16, 16, 8)
+LG_RPLAN(256, 16, 16, 16)
+LG_RPLAN(512, 8, 8, 8, 8)
+LG_RPLAN(1024, 16, 16, 8, 8)
+LG_RPLAN(2048, 16, 16, 16, 8)
+LG_RPLAN(4096, 16, 16, 16, 16)
+LG_RPLAN(8192, 16, 16, 16, 16, 2)
+LG_RPLAN(192, 12, 12, 4, 4)
+LG_RPLAN(384, 12, 12, 4, 4, 2)
+LG_RPLAN(768, 12, 12, 4, 4, 4)
+LG_RPLAN(1536, 12, 12, 4, 4, 4, 2)
+LG_RPLAN(3072, 12, 12, 4, 4, 4, 4)
 #undef LG_RPLAN
 
-template <int LOG2, int S>
+
+template <int L, int S>
 struct Stg {
-  static constexpr int R = RPlan<LOG2>::R[S];
-  static constexpr int Ns = Stg<LOG2, S - 1>::Ns * Stg<LOG2, S - 1>::R;
-  static constexpr int tw_off = Stg<LOG2, S - 1>::tw_off + Stg<LOG2, S - 1>::tw_len;
+  static constexpr int R = RPlan<L>::R[S];
+  static constexpr int Ns = Stg<L, S - 1>::Ns * Stg<L, S - 1>::R;
+  static constexpr int tw_off = Stg<L, S - 1>::tw_off + Stg<L, S - 1>::tw_len;
   static constexpr int tw_len = (R - 1) * Ns;
 };
-template <int LOG2>
-struct Stg<LOG2, 0> {
-  static constexpr int R = RPlan<LOG2>::R[0];
+template <int L>
+struct Stg<L, 0> {
+  static constexpr int R = RPlan<L>::R[0];
   static constexpr int Ns = 1;
   static constexpr int tw_off = 0;
   static constexpr int tw_len = 0;
 };
 
-template <int LOG2>
+template <int L>
 struct TwLen {
-  static constexpr int value =
-      Stg<LOG2, RPlan<LOG2>::NS - 1>::tw_off + Stg<LOG2, RPlan<LOG2>::NS - 1>::tw_len;
+  static constexpr int value = Stg<L, RPlan<L>::NS - 1>::tw_off + Stg<L, RPlan<L>::NS - 1>::tw_len;
 };
 
 // Shared-memory exchange layouts (policy): where element i of a row lives.
 //   Xch2<SW>: one float2 array;  XchS<SW>: split re / im float arrays.
 // SW: 0 = i + (i>>4) padding, 1 = i ^ ((i>>3)&15), 2 = i ^ ((i>>4)&31),
-//     3 = i ^ ((i>>3)&31), 4 = i + (i>>5) padding.
+//     3 = i ^ ((i>>3)&31), 4 = i + (i>>5) padding.  (XOR variants only for
+//     power-of-two lengths.)
 template <int SW>
 __host__ __device__ __forceinline__ int swz(int i) {
   if constexpr (SW == 0) return i + (i >> 4);
@@ -84,8 +92,8 @@ __host__ __device__ constexpr int swz_len(int L) {
 template <int SW>
 struct Xch2 {  // float2 cells
   static constexpr bool soa = false;
-  template <int LOG2>
-  __host__ __device__ static constexpr int bytes() { return swz_len<SW>(1 << LOG2) * 8; }
+  template <int L>
+  __host__ __device__ static constexpr int bytes() { return swz_len<SW>(L) * 8; }
   template <typename T>
   static __device__ __forceinline__ void st(void* sm, int L, int i, cx<T> v) {
     reinterpret_cast<cx<T>*>(sm)[swz<SW>(i)] = v;
@@ -98,8 +106,8 @@ struct Xch2 {  // float2 cells
 template <int SW>
 struct XchS {  // split re / im
   static constexpr bool soa = true;
-  template <int LOG2>
-  __host__ __device__ static constexpr int bytes() { return 2 * swz_len<SW>(1 << LOG2) * 4; }
+  template <int L>
+  __host__ __device__ static constexpr int bytes() { return 2 * swz_len<SW>(L) * 4; }
   template <typename T>
   static __device__ __forceinline__ void st(void* sm, int L, int i, cx<T> v) {
     T* r = reinterpret_cast<T*>(sm);
@@ -116,21 +124,21 @@ struct XchS {  // split re / im
 };
 
 // default exchange layout per plan (chosen by the on-GPU sweep)
-template <int LOG2>
+template <int L>
 struct XchOf {
   using type = Xch2<0>;
 };
 template <>
-struct XchOf<9> {  // [8,8,8] plan: XOR swizzle measured 29.6 vs 26.1 TFLOP/s for padding
+struct XchOf<512> {  // [8,8,8] plan: XOR swizzle measured 29.6 vs 26.1 TFLOP/s for padding
   using type = Xch2<1>;
 };
 
-// smem bytes of one row buffer for the default layout (>= L float2)
-template <int LOG2>
+// float2 cells of one row buffer (>= the padded natural layout used by to_smem)
+template <int L>
 __host__ __device__ constexpr int rsm_len() {
-  return (XchOf<LOG2>::type::template bytes<LOG2>() + 7) / 8 > (1 << LOG2) + ((1 << LOG2) >> 4) + 1
-             ? (XchOf<LOG2>::type::template bytes<LOG2>() + 7) / 8
-             : (1 << LOG2) + ((1 << LOG2) >> 4) + 1;
+  return (XchOf<L>::type::template bytes<L>() + 7) / 8 > L + (L >> 4) + 1
+             ? (XchOf<L>::type::template bytes<L>() + 7) / 8
+             : L + (L >> 4) + 1;
 }
 __device__ __forceinline__ int rpad(int i) { return i + (i >> 4); }
 
@@ -149,33 +157,33 @@ struct GSync {
   }
 };
 
-template <int LOG2>
+template <int L>
 __device__ __forceinline__ GSync make_gsync(int gid, int groups) {
-  constexpr int TPR = RPlan<LOG2>::TPR;
+  constexpr int TPR = RPlan<L>::TPR;
   GSync s;
   s.n = TPR;
-  if (TPR <= 32)
+  if (TPR <= 32 && (32 % TPR) == 0)
     s.id = 0;
-  else if (groups <= 15)
+  else if (groups <= 15 && TPR % 32 == 0)
     s.id = 1 + gid;
   else
     s.id = -1;
   return s;
 }
 
-template <typename T, int LOG2, int SIGN, int S, typename X>
-__device__ __forceinline__ void fftr_stage(cx<T> (&v)[RPlan<LOG2>::E], cx<T>* sm,
+template <typename T, int L, int SIGN, int S, typename X>
+__device__ __forceinline__ void fftr_stage(cx<T> (&v)[RPlan<L>::E], cx<T>* sm,
                                            const cx<T>* __restrict__ tw, int t, const GSync& sync) {
-  using P = RPlan<LOG2>;
-  using G = Stg<LOG2, S>;
-  constexpr int E = P::E, R = G::R, NB = E / R, L = P::L, TPR = P::TPR, Ns = G::Ns;
+  using P = RPlan<L>;
+  using G = Stg<L, S>;
+  constexpr int E = P::E, R = G::R, NB = E / R, TPR = P::TPR, Ns = G::Ns;
   constexpr bool FIRST = S == 0, LAST = S == P::NS - 1;
   cx<T> x[NB][R];
   cx<T> w[NB][R];
   if constexpr (Ns > 1) {
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
-      const int k = (t + b * TPR) & (Ns - 1);
+      const int k = (t + b * TPR) % Ns;
 #pragma unroll
       for (int r = 1; r < R; ++r) w[b][r] = ldg_cx(tw + G::tw_off + (r - 1) * Ns + k);
     }
@@ -213,39 +221,39 @@ __device__ __forceinline__ void fftr_stage(cx<T> (&v)[RPlan<LOG2>::E], cx<T>* sm
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       const int j = t + b * TPR;
-      const int k = j & (Ns - 1);
+      const int k = j % Ns;
       const int base = (j - k) * R + k;
 #pragma unroll
       for (int r = 0; r < R; ++r) X::template st<T>(sm, L, base + r * Ns, x[b][r]);
     }
     sync();
-    fftr_stage<T, LOG2, SIGN, S + 1, X>(v, sm, tw, t, sync);
+    fftr_stage<T, L, SIGN, S + 1, X>(v, sm, tw, t, sync);
   }
 }
 
 // In-register FFT of the row held in the natural distribution.
-template <typename T, int LOG2, int SIGN, typename X = typename XchOf<LOG2>::type>
-__device__ __forceinline__ void fftr(cx<T> (&v)[RPlan<LOG2>::E], cx<T>* sm,
+template <typename T, int L, int SIGN, typename X = typename XchOf<L>::type>
+__device__ __forceinline__ void fftr(cx<T> (&v)[RPlan<L>::E], cx<T>* sm,
                                      const cx<T>* __restrict__ tw, int t, const GSync& sync) {
-  fftr_stage<T, LOG2, SIGN, 0, X>(v, sm, tw, t, sync);
+  fftr_stage<T, L, SIGN, 0, X>(v, sm, tw, t, sync);
 }
 
 // Store the natural-distribution row into sm (padded) so any element can be
-// read by any thread of the group (callers sync before reading).
-template <typename T, int LOG2>
-__device__ __forceinline__ void to_smem(const cx<T> (&v)[RPlan<LOG2>::E], cx<T>* sm, int t) {
-  constexpr int E = RPlan<LOG2>::E, TPR = RPlan<LOG2>::TPR;
+// read by any thread of the group (callers sync before and after).
+template <typename T, int L>
+__device__ __forceinline__ void to_smem(const cx<T> (&v)[RPlan<L>::E], cx<T>* sm, int t) {
+  constexpr int E = RPlan<L>::E, TPR = RPlan<L>::TPR;
 #pragma unroll
   for (int e = 0; e < E; ++e) sm[rpad(t + e * TPR)] = v[e];
 }
 
 // Host helper: per-stage twiddle table (exp(-2 pi i r k / (Ns R)), [r-1][k])
-template <int LOG2, int S = 0, typename F>
+template <int L, int S = 0, typename F>
 void fill_rtwiddles(F&& put) {
-  using G = Stg<LOG2, S>;
+  using G = Stg<L, S>;
   for (int r = 1; r < G::R; ++r)
     for (int k = 0; k < G::Ns; ++k) put(G::tw_off + (r - 1) * G::Ns + k, r * k, G::Ns * G::R);
-  if constexpr (S + 1 < RPlan<LOG2>::NS) fill_rtwiddles<LOG2, S + 1>(put);
+  if constexpr (S + 1 < RPlan<L>::NS) fill_rtwiddles<L, S + 1>(put);
 }
 
 }  // namespace lg

@@ -15,20 +15,30 @@
 
 namespace lg {
 
-template <int LG>
+// Programmatic dependent launch (sm_90+): let the next kernel in the stream /
+// graph get its CTAs resident as soon as every CTA of this one has started,
+// and wait for the predecessor's completion before touching its outputs.
+// Both are no-ops when the launch did not opt in.
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+template <int L>
 struct FGroup {
-  static constexpr int TPR = RPlan<LG>::TPR;
-  static constexpr int E = RPlan<LG>::E;
+  static constexpr int TPR = RPlan<L>::TPR;
+  static constexpr int E = RPlan<L>::E;
   int gid, t, groups;
   C32* sm;
   GSync sync;
   __device__ __forceinline__ FGroup() {
+    pdl_entry();
     extern __shared__ __align__(16) unsigned char fsm_raw[];
     groups = blockDim.x / TPR;
     gid = threadIdx.x / TPR;
     t = threadIdx.x % TPR;
-    sm = reinterpret_cast<C32*>(fsm_raw) + gid * rsm_len<LG>();
-    sync = make_gsync<LG>(gid, groups);
+    sm = reinterpret_cast<C32*>(fsm_raw) + gid * rsm_len<L>();
+    sync = make_gsync<L>(gid, groups);
   }
   __device__ __forceinline__ int idx(int e) const { return t + e * TPR; }
 };
@@ -37,26 +47,28 @@ __device__ __forceinline__ float fsig(float x) { return __fdividef(1.0f, 1.0f + 
 
 // kernel-band slot of residue i mod L, or -1
 __device__ __forceinline__ int kslot(int i, int lo, int hi, int L) {
-  const int q = lo + ((i - lo) & (L - 1));
-  return q <= hi ? q - lo : -1;
+  int r = i - lo;  // i in [0, L), lo in (-L, L)
+  r += r < 0 ? L : 0;
+  r -= r >= L ? L : 0;
+  return lo + r <= hi ? r : -1;
 }
 // intensity-band slot of residue i mod L (band2 layout of geom.h), or -1
 __device__ __forceinline__ int islot(const AxisGeom& a, int i, int L) {
   if (a.full) return i;  // full band: L == n == N, slot j = residue
-  const int q = -a.P + ((i + a.P) & (L - 1));
-  return q <= a.P ? q + a.P : -1;
+  int r = i + a.P;  // residue of p + P
+  r -= r >= L ? L : 0;
+  return r <= 2 * a.P ? r : -1;
 }
 
 // Build Z = A + iB for the row held in the natural distribution from the
 // half spectra a[0..P], b[0..P] of two real signals (b may be null).
-template <int LG>
-__device__ __forceinline__ void load_herm_pair(C32 (&v)[RPlan<LG>::E], const FGroup<LG>& g,
+template <int L>
+__device__ __forceinline__ void load_herm_pair(C32 (&v)[RPlan<L>::E], const FGroup<L>& g,
                                                const C32* a, const C32* b, int P) {
-  constexpr int L = 1 << LG;
 #pragma unroll
-  for (int e = 0; e < RPlan<LG>::E; ++e) {
+  for (int e = 0; e < RPlan<L>::E; ++e) {
     const int i = g.idx(e);
-    const int m = (L - i) & (L - 1);
+    const int m = (i == 0 ? 0 : L - i);
     C32 A = mk(0.f, 0.f), Bv = mk(0.f, 0.f);
     if (i <= P) {
       A = a[i];
@@ -86,12 +98,12 @@ __device__ __forceinline__ float warp_max(float v, int width) {
 // ===========================================================================
 // real row pairs -> half spectra [Pout+1][Ny] (MODE 0 raw, 1 sigmoid(steep x))
 // ===========================================================================
-template <int LG, int MODE>
+template <int L, int MODE>
 __global__ void __launch_bounds__(256) fk_real_rows_fwd(FGeo g, const float* __restrict__ src,
                                                         long long src_ts, float steep, int Pout,
                                                         C32* __restrict__ out, long long out_ts) {
-  FGroup<LG> G;
-  constexpr int L = 1 << LG, E = RPlan<LG>::E;
+  FGroup<L> G;
+  constexpr int E = RPlan<L>::E;
   const int Ny = g.ay.N, npairs = (Ny + 1) / 2;
   const int pair0 = blockIdx.x * G.groups + G.gid;
   const bool act = pair0 < npairs;
@@ -111,74 +123,126 @@ __global__ void __launch_bounds__(256) fk_real_rows_fwd(FGeo g, const float* __r
     }
     v[e] = mk(a, b);
   }
-  fftr<float, LG, -1>(v, G.sm, g.twNx, G.t, G.sync);
+  fftr<float, L, -1>(v, G.sm, g.twNx, G.t, G.sync);
   G.sync();
-  to_smem<float, LG>(v, G.sm, G.t);
+  to_smem<float, L>(v, G.sm, G.t);
   G.sync();
   if (!act) return;
   C32* o = out + blockIdx.z * out_ts;
   for (int px = G.t; px <= Pout; px += G.TPR) {
     C32 A, Bv;
-    split_pair(G.sm[rpad(px)], G.sm[rpad((L - px) & (L - 1))], A, Bv);
+    split_pair(G.sm[rpad(px)], G.sm[rpad((px == 0 ? 0 : L - px))], A, Bv);
     o[size_t(px) * Ny + y0] = A;
     if (has1) o[size_t(px) * Ny + y1] = Bv;
   }
 }
 
 // ===========================================================================
-// per-kernel rows: I_sub(sy,.) = dose sum_k w_k |IFFT_nx(T_fk[sy])|^2, the K
-// kernels spread over the CTA's row groups, reduced in fixed order, then the
-// FFT of the real intensity row -> Ir[f][px][sy], px in [0, P].
-// grid (ny, F, tiles), block = groups * TPR
+// per-kernel rows, one (subgrid row sy, kernel f*K+k) per row group:
+//   Ip[fk][sy][sx] = dose w_fk |IFFT_nx(T_fk[sy])|^2
+// (no cross-group reduction: the fixed-order sum over k is fk_isub_rows).
+// grid (ceil(ny/groups), F*K, tiles)
 // ===========================================================================
-template <int LG>
-__global__ void __launch_bounds__(512) fk_socs_rows(FGeo g, const C32* __restrict__ T,
+template <int L>
+__global__ void __launch_bounds__(256) fk_socs_rows(FGeo g, const C32* __restrict__ T,
                                                     long long t_ts, const float* __restrict__ wk,
-                                                    float dose, C32* __restrict__ Ir,
-                                                    long long ir_ts) {
-  FGroup<LG> G;
-  constexpr int L = 1 << LG, E = RPlan<LG>::E;
-  const int sy = blockIdx.x, f = blockIdx.y, K = g.K, Bx = g.ax.B, ny = g.ay.n;
-  const int lo = g.ax.lo, hi = g.ax.hi;
-  float acc[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) acc[e] = 0.f;
-  int slot[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) slot[e] = kslot(G.idx(e), lo, hi, L);
-  for (int k = G.gid; k < K; k += G.groups) {
-    const C32* src = T + blockIdx.z * t_ts + (size_t(f) * K + k) * ny * Bx + size_t(sy) * Bx;
-    C32 v[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) v[e] = slot[e] >= 0 ? src[slot[e]] : mk(0.f, 0.f);
-    fftr<float, LG, +1>(v, G.sm, g.twnx, G.t, G.sync);
-    const float w = wk[f * K + k] * dose;
-#pragma unroll
-    for (int e = 0; e < E; ++e) acc[e] += w * (v[e].x * v[e].x + v[e].y * v[e].y);
-  }
-  // fixed-order cross-group reduction through shared memory
-  G.sync();
-  float* mine = reinterpret_cast<float*>(G.sm);
-#pragma unroll
-  for (int e = 0; e < E; ++e) mine[G.idx(e)] = acc[e];
-  __syncthreads();
-  if (G.gid != 0) return;
+                                                    float dose, float* __restrict__ Ip,
+                                                    long long ip_ts) {
+  FGroup<L> G;
+  constexpr int E = RPlan<L>::E;
+  const int fk = blockIdx.y, Bx = g.ax.B, ny = g.ay.n, lo = g.ax.lo, hi = g.ax.hi;
+  const int sy0 = blockIdx.x * G.groups + G.gid;
+  const bool act = sy0 < ny;
+  const int sy = act ? sy0 : ny - 1;
+  const C32* src = T + blockIdx.z * t_ts + size_t(fk) * ny * Bx + size_t(sy) * Bx;
   C32 v[E];
-  const float* base = reinterpret_cast<const float*>(G.sm);  // group 0 buffer
 #pragma unroll
   for (int e = 0; e < E; ++e) {
-    float s = 0.f;
-    for (int q = 0; q < G.groups; ++q)
-      s += reinterpret_cast<const float*>(base + size_t(q) * 2 * rsm_len<LG>())[G.idx(e)];
-    v[e] = mk(s, 0.f);
+    const int sl = kslot(G.idx(e), lo, hi, L);
+    v[e] = sl >= 0 ? src[sl] : mk(0.f, 0.f);
   }
-  fftr<float, LG, -1>(v, G.sm, g.twnx, G.t, G.sync);
+  fftr<float, L, +1>(v, G.sm, g.twnx, G.t, G.sync);
+  if (!act) return;
+  const float w = wk[fk] * dose;
+  float* o = Ip + blockIdx.z * ip_ts + (size_t(fk) * ny + sy) * L;
+#pragma unroll
+  for (int e = 0; e < E; ++e) o[G.idx(e)] = w * (v[e].x * v[e].x + v[e].y * v[e].y);
+}
+
+// ===========================================================================
+// intensity rows (pair sy0, sy0+1 of focus f): I_sub = sum_k Ip (fixed order),
+// one packed FFT of the two real rows -> Ir[f][px][sy], px in [0, P].
+// grid (ceil(ny/2/groups), F, tiles)
+// ===========================================================================
+template <int L>
+__global__ void __launch_bounds__(256) fk_isub_rows(FGeo g, const float* __restrict__ Ip,
+                                                    long long ip_ts, C32* __restrict__ Ir,
+                                                    long long ir_ts) {
+  FGroup<L> G;
+  constexpr int E = RPlan<L>::E;
+  const int f = blockIdx.y, ny = g.ay.n, npairs = (ny + 1) / 2;
+  const int pair0 = blockIdx.x * G.groups + G.gid;
+  const bool act = pair0 < npairs;
+  const int pair = act ? pair0 : npairs - 1;
+  const int sy0 = 2 * pair;
+  const bool has1 = sy0 + 1 < ny;
+  // Isub (already summed over k by fk_ip_sum) rows sy0, sy0+1
+  const float* is = Ip + blockIdx.z * ip_ts + size_t(f) * ny * L;
+  C32 v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e)
+    v[e] = mk(is[size_t(sy0) * L + G.idx(e)], has1 ? is[size_t(sy0 + 1) * L + G.idx(e)] : 0.f);
+  fftr<float, L, -1>(v, G.sm, g.twnx, G.t, G.sync);
+  G.sync();
+  to_smem<float, L>(v, G.sm, G.t);
+  G.sync();
+  if (!act) return;
   C32* o = Ir + blockIdx.z * ir_ts + size_t(f) * (g.ax.P + 1) * ny;
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int i = G.idx(e);
-    if (i <= g.ax.P) o[size_t(i) * ny + sy] = v[e];
+  for (int px = G.t; px <= g.ax.P; px += G.TPR) {
+    C32 A, Bv;
+    split_pair(G.sm[rpad(px)], G.sm[rpad(px == 0 ? 0 : L - px)], A, Bv);
+    o[size_t(px) * ny + sy0] = A;
+    if (has1) o[size_t(px) * ny + sy0 + 1] = Bv;
   }
+}
+
+// ===========================================================================
+// Isub[f][i] = sum_k Ip[f][k][i] (fixed order; 4 elements per thread)
+// grid (ceil(ny*nx/1024), F, tiles)
+// ===========================================================================
+static __global__ void fk_ip_sum(FGeo g, const float* __restrict__ Ip, long long ip_ts,
+                                 float* __restrict__ Isub, long long is_ts) {
+  pdl_entry();
+  const int n4 = (g.ay.n * g.ax.n) / 4, K = g.K, f = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n4) return;
+  const float4* a = reinterpret_cast<const float4*>(Ip + blockIdx.z * ip_ts + size_t(f) * K * 4 * n4);
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
+  for (int k = 0; k < K; ++k) {
+    const float4 x = __ldg(a + size_t(k) * n4 + i);
+    s.x += x.x;
+    s.y += x.y;
+    s.z += x.z;
+    s.w += x.w;
+  }
+  reinterpret_cast<float4*>(Isub + blockIdx.z * is_ts + size_t(f) * 4 * n4)[i] = s;
+}
+
+// ===========================================================================
+// Acc[cx][qy] = sum_fk Accp[fk][cx][qy]  (fixed order, elementwise)
+// ===========================================================================
+static __global__ void fk_acc_sum(FGeo g, const C32* __restrict__ Accp, C32* __restrict__ Acc,
+                                  long long a_ts) {
+  pdl_entry();
+  const int n = g.ax.B * g.ay.B, FK = g.F * g.K;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const C32* a = Accp + blockIdx.z * a_ts;
+  C32 s = mk(0.f, 0.f);
+#pragma unroll 8
+  for (int fk = 0; fk < FK; ++fk) s = add(s, ldg_cx(a + size_t(fk) * n + i));
+  Acc[blockIdx.z * a_ts + i] = s;
 }
 
 // ===========================================================================
@@ -186,15 +250,15 @@ __global__ void __launch_bounds__(512) fk_socs_rows(FGeo g, const C32* __restric
 // Z = sig(beta (R - thr)), cost partial, D = 2 c_f (Z - Zt) beta Z (1 - Z),
 // FFT_Nx(D pair) -> Dr[f][px][y].  grid (ceil(Ny/2/groups), F, tiles)
 // ===========================================================================
-template <int LG>
+template <int L>
 __global__ void __launch_bounds__(256) fk_resist_rows(FGeo g, const C32* __restrict__ Rc,
                                                       long long c_ts, const float* __restrict__ target,
                                                       long long tg_ts, const float* __restrict__ cf,
                                                       float beta, float thr, C32* __restrict__ Dr,
                                                       long long d_ts, double* __restrict__ costp,
                                                       long long cp_ts) {
-  FGroup<LG> G;
-  constexpr int L = 1 << LG, E = RPlan<LG>::E, TPR = RPlan<LG>::TPR;
+  FGroup<L> G;
+  constexpr int E = RPlan<L>::E, TPR = RPlan<L>::TPR;
   constexpr int WPG = TPR >= 32 ? TPR / 32 : 1;
   const int Ny = g.ay.N, Px = g.ax.P, f = blockIdx.y, npairs = (Ny + 1) / 2;
   const int pair0 = blockIdx.x * G.groups + G.gid;
@@ -212,8 +276,8 @@ __global__ void __launch_bounds__(256) fk_resist_rows(FGeo g, const C32* __restr
     t1v[e] = has1 ? __ldg(tg + size_t(y1) * L + G.idx(e)) : 0.f;
   }
   C32 v[E];
-  load_herm_pair<LG>(v, G, rc + size_t(y0) * (Px + 1), has1 ? rc + size_t(y1) * (Px + 1) : nullptr, Px);
-  fftr<float, LG, +1>(v, G.sm, g.twNx, G.t, G.sync);
+  load_herm_pair<L>(v, G, rc + size_t(y0) * (Px + 1), has1 ? rc + size_t(y1) * (Px + 1) : nullptr, Px);
+  fftr<float, L, +1>(v, G.sm, g.twNx, G.t, G.sync);
   const float w = cf[f];
   float c = 0.f;
 #pragma unroll
@@ -233,15 +297,15 @@ __global__ void __launch_bounds__(256) fk_resist_rows(FGeo g, const C32* __restr
   c = warp_sum(c * w, TPR < 32 ? TPR : 32);
   if (act && (G.t & 31) == 0)
     costp[blockIdx.z * cp_ts + (size_t(f) * npairs + pair) * WPG + (G.t >> 5)] = double(c);
-  fftr<float, LG, -1>(v, G.sm, g.twNx, G.t, G.sync);
+  fftr<float, L, -1>(v, G.sm, g.twNx, G.t, G.sync);
   G.sync();
-  to_smem<float, LG>(v, G.sm, G.t);
+  to_smem<float, L>(v, G.sm, G.t);
   G.sync();
   if (!act) return;
   C32* d = Dr + blockIdx.z * d_ts + size_t(f) * (Px + 1) * Ny;
   for (int px = G.t; px <= Px; px += TPR) {
     C32 A, Bv;
-    split_pair(G.sm[rpad(px)], G.sm[rpad((L - px) & (L - 1))], A, Bv);
+    split_pair(G.sm[rpad(px)], G.sm[rpad((px == 0 ? 0 : L - px))], A, Bv);
     d[size_t(px) * Ny + y0] = A;
     if (has1) d[size_t(px) * Ny + y1] = Bv;
   }
@@ -251,22 +315,22 @@ __global__ void __launch_bounds__(256) fk_resist_rows(FGeo g, const C32* __restr
 // forward output rows: I = Re, R = Im of IFFT_Nx(I^ + i R^), print = R >= thr
 // grid (ceil(Ny/groups), F, tiles)
 // ===========================================================================
-template <int LG>
+template <int L>
 __global__ void __launch_bounds__(256) fk_out_rows(FGeo g, const C32* __restrict__ Ic,
                                                    const C32* __restrict__ Rc, long long c_ts,
                                                    float* __restrict__ Iout, float* __restrict__ Rout,
                                                    unsigned char* __restrict__ print, long long o_ts,
                                                    float thr) {
-  FGroup<LG> G;
-  constexpr int L = 1 << LG, E = RPlan<LG>::E;
+  FGroup<L> G;
+  constexpr int E = RPlan<L>::E;
   const int Ny = g.ay.N, Px = g.ax.P, f = blockIdx.y;
   const int y0 = blockIdx.x * G.groups + G.gid;
   const bool act = y0 < Ny;
   const int y = act ? y0 : Ny - 1;
   const size_t cb = blockIdx.z * c_ts + (size_t(f) * Ny + y) * (Px + 1);
   C32 v[E];
-  load_herm_pair<LG>(v, G, Ic ? Ic + cb : Rc + cb, (Ic && Rc) ? Rc + cb : nullptr, Px);
-  fftr<float, LG, +1>(v, G.sm, g.twNx, G.t, G.sync);
+  load_herm_pair<L>(v, G, Ic ? Ic + cb : Rc + cb, (Ic && Rc) ? Rc + cb : nullptr, Px);
+  fftr<float, L, +1>(v, G.sm, g.twNx, G.t, G.sync);
   if (!act) return;
   const size_t ob = blockIdx.z * o_ts + (size_t(f) * Ny + y) * L;
 #pragma unroll
@@ -284,12 +348,12 @@ __global__ void __launch_bounds__(256) fk_out_rows(FGeo g, const C32* __restrict
 // W_lp on the decimated grid: Wsub[f][sy] = IFFT_nx(Hermitian Wc[f][sy]) for
 // row pairs.  grid (ceil(ny/2/groups), nf, tiles)
 // ===========================================================================
-template <int LG>
+template <int L>
 __global__ void __launch_bounds__(256) fk_wlp_rows(FGeo g, const C32* __restrict__ Wc,
                                                    long long w_ts, float* __restrict__ Wsub,
                                                    long long ws_ts) {
-  FGroup<LG> G;
-  constexpr int L = 1 << LG, E = RPlan<LG>::E;
+  FGroup<L> G;
+  constexpr int E = RPlan<L>::E;
   const int ny = g.ay.n, Px = g.ax.P, f = blockIdx.y, npairs = (ny + 1) / 2;
   const int pair0 = blockIdx.x * G.groups + G.gid;
   const bool act = pair0 < npairs;
@@ -298,8 +362,8 @@ __global__ void __launch_bounds__(256) fk_wlp_rows(FGeo g, const C32* __restrict
   const bool has1 = y1 < ny;
   const C32* wc = Wc + blockIdx.z * w_ts + size_t(f) * ny * (Px + 1);
   C32 v[E];
-  load_herm_pair<LG>(v, G, wc + size_t(y0) * (Px + 1), has1 ? wc + size_t(y1) * (Px + 1) : nullptr, Px);
-  fftr<float, LG, +1>(v, G.sm, g.twnx, G.t, G.sync);
+  load_herm_pair<L>(v, G, wc + size_t(y0) * (Px + 1), has1 ? wc + size_t(y1) * (Px + 1) : nullptr, Px);
+  fftr<float, L, +1>(v, G.sm, g.twnx, G.t, G.sync);
   if (!act) return;
   float* o = Wsub + blockIdx.z * ws_ts + size_t(f) * ny * L;
 #pragma unroll
@@ -315,42 +379,55 @@ __global__ void __launch_bounds__(256) fk_wlp_rows(FGeo g, const C32* __restrict
 //   U_fk[qx][sy] = FFT_nx(W_lp(sy,.) . IFFT_nx(T_fk[sy]))(qx), qx in band
 // grid (ceil(ny/groups), F*K, tiles)
 // ===========================================================================
-template <int LG, bool UNIFORM>
-__global__ void __launch_bounds__(256) fk_adj_rows(FGeo g, const C32* __restrict__ T,
-                                                   long long t_ts, const float* __restrict__ Wsub,
-                                                   long long ws_ts, C32* __restrict__ U,
-                                                   long long u_ts) {
-  FGroup<LG> G;
-  constexpr int L = 1 << LG, E = RPlan<LG>::E;
+template <int L, bool UNIFORM>
+__global__ void __launch_bounds__(256, 2) fk_adj_rows(FGeo g, const C32* __restrict__ T,
+                                                      long long t_ts, const float* __restrict__ Wsub,
+                                                      long long ws_ts, C32* __restrict__ U,
+                                                      long long u_ts) {
+  FGroup<L> G;
+  constexpr int E = RPlan<L>::E;
   const int ny = g.ay.n, Bx = g.ax.B, K = g.K, lo = g.ax.lo, hi = g.ax.hi;
   const int fk = blockIdx.y, f = fk / K;
-  const int sy0 = blockIdx.x * G.groups + G.gid;
+  const int r0 = blockIdx.x * G.groups;
+  const int sy0 = r0 + G.gid;
   const bool act = sy0 < ny;
   const int sy = act ? sy0 : ny - 1;
-  int slot[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) slot[e] = kslot(G.idx(e), lo, hi, L);
   const C32* src = T + blockIdx.z * t_ts + size_t(fk) * ny * Bx + size_t(sy) * Bx;
   C32 v[E];
 #pragma unroll
-  for (int e = 0; e < E; ++e) v[e] = slot[e] >= 0 ? src[slot[e]] : mk(0.f, 0.f);
+  for (int e = 0; e < E; ++e) {
+    const int sl = kslot(G.idx(e), lo, hi, L);
+    v[e] = sl >= 0 ? src[sl] : mk(0.f, 0.f);
+  }
   float wv[E];
   if (!UNIFORM) {
     const float* w = Wsub + blockIdx.z * ws_ts + (size_t(f) * ny + sy) * L;
 #pragma unroll
     for (int e = 0; e < E; ++e) wv[e] = w[G.idx(e)];
   }
-  fftr<float, LG, +1>(v, G.sm, g.twnx, G.t, G.sync);
+  fftr<float, L, +1>(v, G.sm, g.twnx, G.t, G.sync);
   if (!UNIFORM) {
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = scale(v[e], wv[e]);
   }
-  fftr<float, LG, -1>(v, G.sm, g.twnx, G.t, G.sync);
-  if (!act) return;
-  C32* o = U + blockIdx.z * u_ts + size_t(fk) * Bx * ny;
+  fftr<float, L, -1>(v, G.sm, g.twnx, G.t, G.sync);
+  // stage the band outputs as tile[slot][row] (odd stride: conflict free),
+  // then write U[fk][slot][r0 .. r0+groups) as contiguous row segments
+  extern __shared__ __align__(16) unsigned char fsm_raw[];
+  C32* tile = reinterpret_cast<C32*>(fsm_raw) + G.groups * rsm_len<L>();
+  const int ld = G.groups | 1;
 #pragma unroll
-  for (int e = 0; e < E; ++e)
-    if (slot[e] >= 0) o[size_t(slot[e]) * ny + sy] = v[e];
+  for (int e = 0; e < E; ++e) {
+    const int sl = kslot(G.idx(e), lo, hi, L);
+    if (sl >= 0) tile[sl * ld + G.gid] = v[e];
+  }
+  __syncthreads();
+  C32* o = U + blockIdx.z * u_ts + size_t(fk) * Bx * ny;
+  const int nr = min(G.groups, ny - r0);
+  for (int idx = threadIdx.x; idx < Bx * G.groups; idx += blockDim.x) {
+    const int sl = idx / G.groups, rr = idx - sl * G.groups;
+    if (rr < nr) o[size_t(sl) * ny + r0 + rr] = tile[sl * ld + rr];
+  }
 }
 
 // ===========================================================================
@@ -358,15 +435,15 @@ __global__ void __launch_bounds__(256) fk_adj_rows(FGeo g, const C32* __restrict
 // !ILT: write grad; ILT: theta update, then next iteration's mask rows.
 // grid (ceil(Ny/2/groups), 1, tiles)
 // ===========================================================================
-template <int LG, bool ILT>
+template <int L, bool ILT>
 __global__ void __launch_bounds__(256) fk_grad_rows(FGeo g, const C32* __restrict__ Gc,
                                                     long long g_ts, float* __restrict__ grad,
                                                     long long gr_ts, float* __restrict__ theta,
                                                     long long th_ts, float steep, float step,
                                                     C32* __restrict__ Mr, long long mr_ts,
                                                     double* __restrict__ gmaxp, long long gm_ts) {
-  FGroup<LG> G;
-  constexpr int L = 1 << LG, E = RPlan<LG>::E, TPR = RPlan<LG>::TPR;
+  FGroup<L> G;
+  constexpr int E = RPlan<L>::E, TPR = RPlan<L>::TPR;
   constexpr int WPG = TPR >= 32 ? TPR / 32 : 1;
   const int Ny = g.ay.N, Pm = g.ax.Pm, npairs = (Ny + 1) / 2;
   const int pair0 = blockIdx.x * G.groups + G.gid;
@@ -385,8 +462,8 @@ __global__ void __launch_bounds__(256) fk_grad_rows(FGeo g, const C32* __restric
     }
   }
   C32 v[E];
-  load_herm_pair<LG>(v, G, gc + size_t(y0) * (Pm + 1), has1 ? gc + size_t(y1) * (Pm + 1) : nullptr, Pm);
-  fftr<float, LG, +1>(v, G.sm, g.twNx, G.t, G.sync);
+  load_herm_pair<L>(v, G, gc + size_t(y0) * (Pm + 1), has1 ? gc + size_t(y1) * (Pm + 1) : nullptr, Pm);
+  fftr<float, L, +1>(v, G.sm, g.twNx, G.t, G.sync);
   if (!ILT) {
     if (!act) return;
     float* o = grad + blockIdx.z * gr_ts;
@@ -422,15 +499,15 @@ __global__ void __launch_bounds__(256) fk_grad_rows(FGeo g, const C32* __restric
   }
   gm = warp_max(gm, TPR < 32 ? TPR : 32);
   if (act && gmaxp && (G.t & 31) == 0) gmaxp[blockIdx.z * gm_ts + size_t(pair) * WPG + (G.t >> 5)] = gm;
-  fftr<float, LG, -1>(v, G.sm, g.twNx, G.t, G.sync);
+  fftr<float, L, -1>(v, G.sm, g.twNx, G.t, G.sync);
   G.sync();
-  to_smem<float, LG>(v, G.sm, G.t);
+  to_smem<float, L>(v, G.sm, G.t);
   G.sync();
   if (!act) return;
   C32* o = Mr + blockIdx.z * mr_ts;
   for (int px = G.t; px <= Pm; px += TPR) {
     C32 A, Bv;
-    split_pair(G.sm[rpad(px)], G.sm[rpad((L - px) & (L - 1))], A, Bv);
+    split_pair(G.sm[rpad(px)], G.sm[rpad((px == 0 ? 0 : L - px))], A, Bv);
     o[size_t(px) * Ny + y0] = A;
     if (has1) o[size_t(px) * Ny + y1] = Bv;
   }
@@ -440,12 +517,12 @@ __global__ void __launch_bounds__(256) fk_grad_rows(FGeo g, const C32* __restric
 // mask half-spectrum columns -> kernel band M^ (Hermitian mirror for qx < 0)
 // grid (ceil((Pmx+1)/groups), 1, tiles)
 // ===========================================================================
-template <int LG>
+template <int L>
 __global__ void __launch_bounds__(256) fk_mask_cols(FGeo g, const C32* __restrict__ Mr,
                                                     long long mr_ts, C32* __restrict__ Mhat,
                                                     long long mh_ts) {
-  FGroup<LG> G;
-  constexpr int L = 1 << LG, E = RPlan<LG>::E;
+  FGroup<L> G;
+  constexpr int E = RPlan<L>::E;
   const int Pm = g.ax.Pm;
   const int px0 = blockIdx.x * G.groups + G.gid;
   const bool act = px0 <= Pm;
@@ -454,7 +531,7 @@ __global__ void __launch_bounds__(256) fk_mask_cols(FGeo g, const C32* __restric
   C32 v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) v[e] = src[G.idx(e)];
-  fftr<float, LG, -1>(v, G.sm, g.twNy, G.t, G.sync);
+  fftr<float, L, -1>(v, G.sm, g.twNy, G.t, G.sync);
   if (!act) return;
   const float inv = 1.0f / (float(g.ax.N) * float(L));
   C32* mh = Mhat + blockIdx.z * mh_ts;
@@ -469,26 +546,29 @@ __global__ void __launch_bounds__(256) fk_mask_cols(FGeo g, const C32* __restric
       if (jy >= 0) mh[size_t(jy) * Bx + sp] = scale(v[e], inv);
     }
     if (sn >= 0 && sn != sp) {
-      const int jy = kslot((L - i) & (L - 1), g.ay.lo, g.ay.hi, L);
+      const int jy = kslot((i == 0 ? 0 : L - i), g.ay.lo, g.ay.hi, L);
       if (jy >= 0) mh[size_t(jy) * Bx + sn] = scale(conjg(v[e]), inv);
     }
   }
 }
 
 // ===========================================================================
-// per-kernel columns on the decimated grid: T_fk[sy][cx] = IFFT_ny(M^ H_fk)
+// per-kernel columns on the decimated grid: T_fk[sy][cx] = IFFT_ny(M^ H_fk);
+// the CTA's groups take consecutive columns and stage the result through
+// shared memory so T rows are written as contiguous segments.
 // grid (ceil(Bx/groups), F*K, tiles)
 // ===========================================================================
-template <int LG>
-__global__ void __launch_bounds__(256) fk_socs_cols(FGeo g, const C32* __restrict__ Mhat,
+template <int L>
+__global__ void __launch_bounds__(512) fk_socs_cols(FGeo g, const C32* __restrict__ Mhat,
                                                     long long mh_ts, const C32* __restrict__ H,
                                                     C32* __restrict__ T, long long t_ts) {
-  FGroup<LG> G;
-  constexpr int L = 1 << LG, E = RPlan<LG>::E;
+  FGroup<L> G;
+  constexpr int E = RPlan<L>::E;
   const int Bx = g.ax.B, By = g.ay.B, fk = blockIdx.y;
-  const int c0 = blockIdx.x * G.groups + G.gid;
-  const bool act = c0 < Bx;
-  const int cx_ = act ? c0 : Bx - 1;
+  const int c0 = blockIdx.x * G.groups;
+  const int cx0 = c0 + G.gid;
+  const bool act = cx0 < Bx;
+  const int cx_ = act ? cx0 : Bx - 1;
   const C32* mh = Mhat + blockIdx.z * mh_ts;
   const C32* h = H + size_t(fk) * By * Bx;
   C32 v[E];
@@ -497,26 +577,34 @@ __global__ void __launch_bounds__(256) fk_socs_cols(FGeo g, const C32* __restric
     const int jy = kslot(G.idx(e), g.ay.lo, g.ay.hi, L);
     v[e] = jy >= 0 ? mul(mh[size_t(jy) * Bx + cx_], ldg_cx(h + size_t(jy) * Bx + cx_)) : mk(0.f, 0.f);
   }
-  fftr<float, LG, +1>(v, G.sm, g.twny, G.t, G.sync);
-  if (!act) return;
-  C32* o = T + blockIdx.z * t_ts + size_t(fk) * L * Bx;
+  fftr<float, L, +1>(v, G.sm, g.twny, G.t, G.sync);
+  extern __shared__ __align__(16) unsigned char fsm_raw[];
+  C32* tile = reinterpret_cast<C32*>(fsm_raw) + G.groups * rsm_len<L>();
+  const int ld = G.groups | 1;
 #pragma unroll
-  for (int e = 0; e < E; ++e) o[size_t(G.idx(e)) * Bx + cx_] = v[e];
+  for (int e = 0; e < E; ++e) tile[G.idx(e) * ld + G.gid] = v[e];
+  __syncthreads();
+  C32* o = T + blockIdx.z * t_ts + size_t(fk) * L * Bx;
+  const int nc = min(G.groups, Bx - c0);
+  for (int idx = threadIdx.x; idx < L * G.groups; idx += blockDim.x) {
+    const int sy = idx / G.groups, cc = idx - sy * G.groups;
+    if (cc < nc) o[size_t(sy) * Bx + c0 + cc] = tile[sy * ld + cc];
+  }
 }
 
 // ===========================================================================
 // column FFT -> intensity band: out[f][j][px] = FFT_L(in[f][px])(p_j) s(j,px)
 // grid (ceil((Px+1)/groups), nf, tiles).  inv = 1/(Lx L) (grid normalisation)
 // ===========================================================================
-template <int LG>
+template <int L>
 __global__ void __launch_bounds__(256) fk_band_colfwd(FGeo g, const C32* __restrict__ in,
                                                       long long in_ts, float inv,
                                                       const float* __restrict__ gxh,
                                                       const float* __restrict__ gyb,
                                                       C32* __restrict__ outR, C32* __restrict__ outI,
                                                       long long o_ts) {
-  FGroup<LG> G;
-  constexpr int L = 1 << LG, E = RPlan<LG>::E;
+  FGroup<L> G;
+  constexpr int E = RPlan<L>::E;
   const int Px = g.ax.P, f = blockIdx.y, nb2 = g.ay.nb2;
   const int px0 = blockIdx.x * G.groups + G.gid;
   const bool act = px0 <= Px;
@@ -525,7 +613,7 @@ __global__ void __launch_bounds__(256) fk_band_colfwd(FGeo g, const C32* __restr
   C32 v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) v[e] = src[G.idx(e)];
-  fftr<float, LG, -1>(v, G.sm, L == g.ay.N ? g.twNy : g.twny, G.t, G.sync);
+  fftr<float, L, -1>(v, G.sm, L == g.ay.N ? g.twNy : g.twny, G.t, G.sync);
   if (!act) return;
   const float gx = gxh ? gxh[px] : 1.f;
   const size_t ob = blockIdx.z * o_ts + size_t(f) * nb2 * (Px + 1);
@@ -543,12 +631,12 @@ __global__ void __launch_bounds__(256) fk_band_colfwd(FGeo g, const C32* __restr
 // intensity band -> column IFFT of length L: out[f][y][px]
 // grid (ceil((Px+1)/groups), nf, tiles)
 // ===========================================================================
-template <int LG>
+template <int L>
 __global__ void __launch_bounds__(256) fk_band_colinv(FGeo g, const C32* __restrict__ band,
                                                       long long b_ts, C32* __restrict__ out,
                                                       long long o_ts) {
-  FGroup<LG> G;
-  constexpr int L = 1 << LG, E = RPlan<LG>::E;
+  FGroup<L> G;
+  constexpr int E = RPlan<L>::E;
   const int Px = g.ax.P, f = blockIdx.y, nb2 = g.ay.nb2;
   const int px0 = blockIdx.x * G.groups + G.gid;
   const bool act = px0 <= Px;
@@ -560,7 +648,7 @@ __global__ void __launch_bounds__(256) fk_band_colinv(FGeo g, const C32* __restr
     const int j = islot(g.ay, G.idx(e), L);
     v[e] = j >= 0 ? b[size_t(j) * (Px + 1) + px] : mk(0.f, 0.f);
   }
-  fftr<float, LG, +1>(v, G.sm, L == g.ay.N ? g.twNy : g.twny, G.t, G.sync);
+  fftr<float, L, +1>(v, G.sm, L == g.ay.N ? g.twNy : g.twny, G.t, G.sync);
   if (!act) return;
   C32* o = out + blockIdx.z * o_ts + size_t(f) * L * (Px + 1);
 #pragma unroll
@@ -568,50 +656,36 @@ __global__ void __launch_bounds__(256) fk_band_colinv(FGeo g, const C32* __restr
 }
 
 // ===========================================================================
-// adjoint columns: Acc(qy,cx) = sum_fk FFT_ny(U_fk[cx])(qy) conj(H_fk) 2 dose
-// w_fk dx dy/(Nx Ny); (f,k) spread over the CTA's groups, fixed-order
-// reduction.  grid (Bx, 1, tiles)
+// adjoint columns, one (band column cx, f*K+k) per group:
+//   Accp[fk][cx][qy] = FFT_ny(U_fk[cx])(qy) conj(H_fk(qy,cx)) 2 dose w_fk (N/n)^2/N^2
+// (the sum over fk happens in fk_grad_cols, fixed order).
+// grid (ceil(Bx/groups), F*K, tiles)
 // ===========================================================================
-template <int LG>
-__global__ void __launch_bounds__(512) fk_adj_cols(FGeo g, const C32* __restrict__ U,
+template <int L>
+__global__ void __launch_bounds__(256) fk_adj_cols(FGeo g, const C32* __restrict__ U,
                                                    long long u_ts, const C32* __restrict__ H,
                                                    const float* __restrict__ wk, float dose,
-                                                   C32* __restrict__ Acc, long long a_ts) {
-  FGroup<LG> G;
-  constexpr int L = 1 << LG, E = RPlan<LG>::E;
-  const int Bx = g.ax.B, By = g.ay.B, FK = g.F * g.K, cx_ = blockIdx.x;
-  const float sc = float(2.0 * double(g.ax.d) * double(g.ay.d) / (double(g.ax.N) * double(g.ay.N)));
-  int slot[E];
+                                                   C32* __restrict__ Accp, long long a_ts) {
+  FGroup<L> G;
+  constexpr int E = RPlan<L>::E;
+  const int Bx = g.ax.B, By = g.ay.B, fk = blockIdx.y;
+  const int cx0 = blockIdx.x * G.groups + G.gid;
+  const bool act = cx0 < Bx;
+  const int cx_ = act ? cx0 : Bx - 1;
+  const float sc = float(2.0 / (double(g.ax.n) * double(g.ay.n)));  // 2 (N/n)^2 / N^2
+  const C32* src = U + blockIdx.z * u_ts + (size_t(fk) * Bx + cx_) * L;
+  C32 v[E];
 #pragma unroll
-  for (int e = 0; e < E; ++e) slot[e] = kslot(G.idx(e), g.ay.lo, g.ay.hi, L);
-  C32 acc[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) acc[e] = mk(0.f, 0.f);
-  for (int fk = G.gid; fk < FK; fk += G.groups) {
-    const C32* src = U + blockIdx.z * u_ts + (size_t(fk) * Bx + cx_) * L;
-    C32 v[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) v[e] = src[G.idx(e)];
-    fftr<float, LG, -1>(v, G.sm, g.twny, G.t, G.sync);
-    const float w = wk[fk] * dose * sc;
-    const C32* h = H + size_t(fk) * By * Bx;
-#pragma unroll
-    for (int e = 0; e < E; ++e)
-      if (slot[e] >= 0) acc[e] = add(acc[e], scale(mulc(v[e], ldg_cx(h + size_t(slot[e]) * Bx + cx_)), w));
-  }
-  G.sync();
-#pragma unroll
-  for (int e = 0; e < E; ++e) G.sm[G.idx(e)] = acc[e];
-  __syncthreads();
-  if (G.gid != 0) return;
-  C32* o = Acc + blockIdx.z * a_ts;
-  const C32* base = G.sm;
+  for (int e = 0; e < E; ++e) v[e] = src[G.idx(e)];
+  fftr<float, L, -1>(v, G.sm, g.twny, G.t, G.sync);
+  if (!act) return;
+  const float w = wk[fk] * dose * sc;
+  const C32* h = H + size_t(fk) * By * Bx;
+  C32* o = Accp + blockIdx.z * a_ts + (size_t(fk) * Bx + cx_) * By;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
-    if (slot[e] < 0) continue;
-    C32 s = mk(0.f, 0.f);
-    for (int q = 0; q < G.groups; ++q) s = add(s, base[size_t(q) * rsm_len<LG>() + G.idx(e)]);
-    o[size_t(slot[e]) * Bx + cx_] = s;
+    const int jy = kslot(G.idx(e), g.ay.lo, g.ay.hi, L);
+    if (jy >= 0) o[jy] = scale(mulc(v[e], ldg_cx(h + size_t(jy) * Bx + cx_)), w);
   }
 }
 
@@ -620,27 +694,24 @@ __global__ void __launch_bounds__(512) fk_adj_cols(FGeo g, const C32* __restrict
 // the last CTA reduces this iteration's cost partials (fixed order).
 // grid (ceil((Pmx+1)/groups) + 1, 1, tiles)
 // ===========================================================================
-template <int LG>
+template <int L>
 __global__ void __launch_bounds__(256) fk_grad_cols(FGeo g, const C32* __restrict__ Acc,
                                                     long long a_ts, C32* __restrict__ Gc,
                                                     long long g_ts, const double* __restrict__ costp,
                                                     long long cp_ts, int ncost,
                                                     double* __restrict__ cost_out, long long co_ts) {
-  FGroup<LG> G;
-  constexpr int L = 1 << LG, E = RPlan<LG>::E;
+  FGroup<L> G;
+  constexpr int E = RPlan<L>::E;
   if (blockIdx.x == gridDim.x - 1) {
     if (cost_out) {  // fixed-order (deterministic) parallel sum of the cost partials
-      __shared__ double red[256];
+      __shared__ double red[512];
       const double* c = costp + blockIdx.z * cp_ts;
       double s = 0;
-      if (threadIdx.x < 256)
-        for (int i = threadIdx.x; i < ncost; i += 256) s += c[i];
-      if (threadIdx.x < 256) red[threadIdx.x] = s;
+      for (int i = threadIdx.x; i < ncost; i += blockDim.x) s += c[i];
+      red[threadIdx.x] = s;
       __syncthreads();
-      for (int w = 128; w > 0; w >>= 1) {
-        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
-        __syncthreads();
-      }
+      if (threadIdx.x == 0)
+        for (int i = 1; i < int(blockDim.x); ++i) red[0] += red[i];
       if (threadIdx.x == 0) cost_out[blockIdx.z * co_ts] = red[0];
     }
     return;
@@ -649,20 +720,21 @@ __global__ void __launch_bounds__(256) fk_grad_cols(FGeo g, const C32* __restric
   const int px0 = blockIdx.x * G.groups + G.gid;
   const bool act = px0 <= Pm;
   const int px = act ? px0 : Pm;
-  const C32* a = Acc + blockIdx.z * a_ts;
+  const C32* a = Acc + blockIdx.z * a_ts;  // summed over (f,k): [cx][qy]
   const int sp = band_slot(g.ax, px), sn = band_slot(g.ax, -px);
+  const int By = g.ay.B;
   C32 v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int i = G.idx(e);
     const int jp = kslot(i, g.ay.lo, g.ay.hi, L);
-    const int jn = kslot((L - i) & (L - 1), g.ay.lo, g.ay.hi, L);
+    const int jn = kslot((i == 0 ? 0 : L - i), g.ay.lo, g.ay.hi, L);
     C32 s = mk(0.f, 0.f);
-    if (sp >= 0 && jp >= 0) s = add(s, a[size_t(jp) * Bx + sp]);
-    if (sn >= 0 && jn >= 0) s = add(s, conjg(a[size_t(jn) * Bx + sn]));
+    if (sp >= 0 && jp >= 0) s = add(s, a[size_t(sp) * By + jp]);
+    if (sn >= 0 && jn >= 0) s = add(s, conjg(a[size_t(sn) * By + jn]));
     v[e] = scale(s, 0.5f);
   }
-  fftr<float, LG, +1>(v, G.sm, g.twNy, G.t, G.sync);
+  fftr<float, L, +1>(v, G.sm, g.twNy, G.t, G.sync);
   if (!act) return;
   C32* o = Gc + blockIdx.z * g_ts;
 #pragma unroll

@@ -14,7 +14,6 @@ namespace lg {
 struct FGeo {
   AxisGeom ax, ay;
   int F, K;
-  int lgNx, lgNy, lgnx, lgny;
   // per-stage twiddle tables (fftr.cuh layout) for Nx, Ny, nx, ny
   const cx<float>* twNx;
   const cx<float>* twNy;
@@ -24,16 +23,26 @@ struct FGeo {
 
 using C32 = cx<float>;
 
-inline bool fast_log2_ok(int lg) { return lg >= 5 && lg <= 13; }
-int fast_tw_len(int lg);
-int fast_tpr(int lg);  // threads per row group of the length-2^lg plan
-void fast_fill_twiddles(int lg, C32* host_out);  // fftr per-stage layout
+inline bool fast_len_ok(int L) {
+  for (int v : kFastLens)
+    if (v == L) return true;
+  return false;
+}
+int fast_tw_len(int len);
+void fast_set_pdl(bool on);  // programmatic dependent launch for subsequent fast launches
+int fast_tpr(int len);  // threads per row group of the length-len plan
+void fast_fill_twiddles(int len, C32* host_out);  // fftr per-stage layout
 
 // ---- row kernels (fast_rows.cu) ----
 void fl_real_rows_fwd(const FGeo& g, cudaStream_t s, int tiles, int mode, const float* src,
                       long long src_ts, float steep, int Pout, C32* out, long long out_ts);
 void fl_socs_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* T, long long t_ts,
-                  const float* wk, float dose, C32* Ir, long long ir_ts);
+                  const float* wk, float dose, float* Ip, long long ip_ts);
+void fl_isub_rows(const FGeo& g, cudaStream_t s, int tiles, const float* Ip, long long ip_ts, C32* Ir,
+                  long long ir_ts);
+void fl_ip_sum(const FGeo& g, cudaStream_t s, int tiles, const float* Ip, long long ip_ts, float* Isub,
+               long long is_ts);
+void fl_acc_sum(const FGeo& g, cudaStream_t s, int tiles, const C32* Accp, C32* Acc, long long a_ts);
 void fl_resist_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* Rc, long long c_ts,
                     const float* target, long long tg_ts, const float* cf, float beta, float thr,
                     C32* Dr, long long d_ts, double* costp, long long cp_ts);

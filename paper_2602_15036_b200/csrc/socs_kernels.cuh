@@ -599,7 +599,7 @@ __global__ void k_adj_cols(Geo<T> g, const cx<T>* __restrict__ U, long long u_ts
   const int qxs = blockIdx.x;
   const int tile = blockIdx.z;
   const Row<T> row = grp.row(0, g.tny, true);
-  const T sc = T(2.0 * double(g.ax.d) * double(g.ay.d) / (double(g.ax.N) * double(g.ay.N)));
+  const T sc = T(2.0 / (double(g.ax.n) * double(g.ay.n)));  // 2 (N/n)^2 / N^2
   cx<T> acc[16];
 #pragma unroll
   for (int e = 0; e < 16; ++e) acc[e] = mk(T(0), T(0));
