@@ -333,7 +333,8 @@ def run_ours(args, world, rank, local):
                        "parallelism": f"tiles sharded over {world} rank(s), NCCL all-reduce of cost per iteration"},
             "roofline": {"bound": "fp32", "kernel": top, "achieved": achieved, "peak": peak_fp32,
                          "unit": "TFLOP/s", "frac": achieved / peak_fp32 if peak_fp32 else None,
-                         "traffic": None,
+                         "traffic": _ncu_traffic(top)[0],
+                         "traffic_source": _ncu_traffic(top)[1],
                          "peak_source": "measured on-box FFMA microbenchmark (lithogpu_fp32_peak)",
                          "flops_per_launch": top_flops, "algorithmic_bytes_per_launch": top_bytes,
                          "kernel_ms": top_ms,
@@ -424,6 +425,24 @@ def _batched_ilt(ctx, stream, dk, target32, theta0, prm, iters, tiles=8):
     solver.close()
     return {"tiles_per_gpu": tiles, "ms_per_step": ms, "tile_iter_s": tiles * iters / (ms * 1e-3),
             "note": f"{tiles} C2 tiles batched per launch, {iters} iterations per step"}
+
+
+def _ncu_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` (per launch) from
+    the newest committed `ncu --set full` capture summary (profiles/*_ncu.json,
+    tools/ncu_summarize.py).  ncu flushes caches before each replay, so this
+    counts the L2-resident intermediates a warm step never takes to HBM."""
+    import glob
+    best = None
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu.json"))):
+        try:
+            caps = json.load(open(p)).get("full_captures", {})
+        except Exception:
+            continue
+        c = caps.get("fk_" + kernel) or caps.get(kernel)
+        if c and c.get("dram_bytes") is not None:
+            best = (c["dram_bytes"], f"{os.path.basename(p)} ({c.get('kernel')}, grid {c.get('grid')})")
+    return best if best else (None, None)
 
 
 def _peaks():
