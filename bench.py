@@ -130,7 +130,16 @@ def fft_flops(L):
     return 5.0 * L * math.log2(L)
 
 
-def kernel_model(geo, F, K):
+def store_e(geo, F, K, tiles=1):
+    """Mirror of Plan::reserve: the ILT keeps E_fk for the adjoint rows while
+    F*K*n^2 complex64 per launch stays <= 96 MiB (LITHOGPU_STORE_E overrides)."""
+    env = os.environ.get("LITHOGPU_STORE_E")
+    if env is not None:
+        return env.startswith("1")
+    return 8 * F * K * geo["n"] ** 2 * tiles <= (96 << 20)
+
+
+def kernel_model(geo, F, K, tiles=1):
     """Per-launch FFT flops (5 L log2 L per length-L complex transform) and
     algorithmic bytes of each kernel of one ILT iteration on one tile, for the
     implemented decimated-band algorithm."""
@@ -138,22 +147,20 @@ def kernel_model(geo, F, K):
     P, Pm = B - 1, (B - 1) // 2
     c = 8  # complex64 bytes
     fN, fn = fft_flops(N), fft_flops(n)
+    se = store_e(geo, F, K, tiles)
     m = {
         "mask_cols": ((Pm + 1) * fN, (Pm + 1) * N * c + B * B * c),
         "socs_cols": (F * K * B * fn, F * K * (B * B * c + n * B * c)),
-        "socs_rows": (F * K * n * fn, F * K * (n * B * c + n * n * 4)),
-        "ip_sum": (0.0, F * (K + 1) * n * n * 4),
-        "isub_rows": (F * (n // 2) * fn, F * (n * n * 4 + (P + 1) * n * c)),
-        "isub_colfwd": (F * (P + 1) * fn, F * ((P + 1) * n * c + (2 * P + 1) * (P + 1) * c)),
-        "isub_colinv": (F * (P + 1) * fN, F * ((2 * P + 1) * (P + 1) * c + N * (P + 1) * c)),
+        "socs_rows": (F * K * n * fn, F * K * (n * B * c + n * n * 4 + (n * n * c if se else 0))),
+        "isub_rows": (F * (n // 2) * fn, F * (K * n * n * 4 + (P + 1) * n * c)),
+        "isub_cols": (F * (P + 1) * (fn + fN), F * ((P + 1) * n * c + N * (P + 1) * c)),
         "resist_rows": (F * (N // 2) * 2 * fN, F * (2 * N * (P + 1) * c + N * N * 4)),
-        "wlp_colfwd": (F * (P + 1) * fN, F * ((P + 1) * N * c + (2 * P + 1) * (P + 1) * c)),
-        "wlp_colinv": (F * (P + 1) * fn, F * ((2 * P + 1) * (P + 1) * c + n * (P + 1) * c)),
+        "wlp_cols": (F * (P + 1) * (fN + fn), F * ((P + 1) * N * c + n * (P + 1) * c)),
         "wlp_rows": (F * (n // 2) * fn, F * (n * (P + 1) * c + n * n * 4)),
-        "adj_rows": (F * K * n * 2 * fn, F * K * (2 * n * B * c) + F * n * n * 4),
+        "adj_rows": (F * K * n * (1 if se else 2) * fn,
+                     F * K * ((n * n * c) if se else (n * B * c)) + F * K * B * n * c + F * n * n * 4),
         "adj_cols": (F * K * B * fn, F * K * (B * n * c + 2 * B * B * c)),
-        "acc_sum": (0.0, (F * K + 1) * B * B * c),
-        "grad_cols": ((Pm + 1) * fN, B * B * c + N * (Pm + 1) * c),
+        "grad_cols": ((Pm + 1) * fN, F * K * B * B * c + N * (Pm + 1) * c),
         "grad_rows": ((N // 2) * 2 * fN, N * (Pm + 1) * c + 2 * N * N * 4 + (Pm + 1) * N * c),
     }
     return m

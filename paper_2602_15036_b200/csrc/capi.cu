@@ -435,8 +435,12 @@ struct Plan : PlanBase {
   // fp32 fast path (power-of-two tiles, register FFT kernels of socs_fast.cuh)
   bool fast = false;
   lg::FGeo fg{};
-  DevBuf ftNx, ftNy, ftnx, ftny, Wsub, Ih, Rh, Wh, Ip, AccS;
-  long long s_Wsub = 0, s_band = 0, s_Ip = 0, s_AccS = 0;
+  DevBuf ftNx, ftNy, ftnx, ftny, Wsub, Ih, Rh, Wh, Ip, Eb;
+  long long s_Wsub = 0, s_band = 0, s_Ip = 0, s_E = 0;
+  // ILT: keep the coherent fields E_fk from the forward rows for the adjoint
+  // rows (saves one n-point IFFT per (row, kernel)) while they stay
+  // L2-sized; beyond that recomputing them is cheaper than the HBM round trip
+  bool store_E = false;
 
   Plan(lithogpu_ctx* c, const lithogpu_grid& gr, int F_, int K_, const double* weights, int S,
        const int32_t* support, const double* values)
@@ -527,7 +531,7 @@ struct Plan : PlanBase {
         s_Wsub = (long long)F * ay.n * ax.n;
         s_band = (long long)F * ay.nb2 * (ax.P + 1);
         s_Ip = (long long)F * K * ay.n * ax.n;
-        s_AccS = (long long)By * Bx;
+        s_E = (long long)F * K * ay.n * ax.n;
         const long long npairs = (Ny + 1) / 2;
         const long long wpg = std::max(1, lg::fast_tpr(Nx) / 32);
         s_cr = std::max(s_cr, F * npairs * wpg);
@@ -570,6 +574,7 @@ struct Plan : PlanBase {
   void reserve(int tiles, bool adjoint) {
     if (tiles > cap) {
       ++gen;
+      Eb.release();
       Mr.release(); Mhat.release(); Tb.release(); Ir.release(); Ic.release(); Rc.release();
       Dr.release(); Wc.release(); U.release(); Acc.release(); Gc.release();
       costrow.release(); gmaxrow.release();
@@ -577,10 +582,12 @@ struct Plan : PlanBase {
     }
     const size_t c = sizeof(C) * size_t(cap);
     if (fast) {
+      const char* se = std::getenv("LITHOGPU_STORE_E");
+      store_E = adjoint && (se ? se[0] == '1' : c * s_E <= (96ll << 20));
+      if (store_E) Eb.ensure(c * s_E);
       Rh.ensure(c * s_band);
       Ih.ensure(c * s_band);
       Ip.ensure(sizeof(T) * size_t(cap) * s_Ip);
-      if (adjoint) AccS.ensure(c * s_AccS);
       Wsub.ensure(sizeof(T) * size_t(cap) * s_Wsub);  // W_lp (adjoint) / I_sub (forward) scratch
       if (adjoint) Wh.ensure(c * s_band);
     }
@@ -709,6 +716,40 @@ struct Plan : PlanBase {
        Gc.as<C>(), s_Gc, grad, gr_ts, theta, th_ts, steep, step, Mr.as<C>(), s_Mr, gm, s_gm);
   }
 
+  // fast path: band resampling columns (fused single pass when the plan pair
+  // has a fused kernel, else the two-pass form through the band buffers)
+  void isub_cols_fast(int tiles, bool want_i, bool want_r) {
+    cudaStream_t s = ctx->stream;
+    bool fused = false;
+    fl("isub_cols", [&] {
+      fused = lg::fl_band_col2(fg, s, tiles, F, true, Ir.as<C>(), s_Ir, gxh.as<T>(), gyb.as<T>(),
+                               want_r ? Rc.as<C>() : nullptr, want_i ? Ic.as<C>() : nullptr, s_C);
+    });
+    if (fused) return;
+    fl("isub_colfwd", [&] {
+      lg::fl_band_colfwd(fg, s, tiles, F, true, Ir.as<C>(), s_Ir, gxh.as<T>(), gyb.as<T>(),
+                         want_r ? Rh.as<C>() : nullptr, want_i ? Ih.as<C>() : nullptr, s_band);
+    });
+    if (want_i)
+      fl("isub_colinv", [&] { lg::fl_band_colinv(fg, s, tiles, F, false, Ih.as<C>(), s_band, Ic.as<C>(), s_C); });
+    if (want_r)
+      fl("isub_colinv", [&] { lg::fl_band_colinv(fg, s, tiles, F, false, Rh.as<C>(), s_band, Rc.as<C>(), s_C); });
+  }
+  void wlp_cols_fast(int tiles, int nf, bool gauss) {
+    cudaStream_t s = ctx->stream;
+    const float* gx = gauss ? gxh.as<T>() : nullptr;
+    const float* gy = gauss ? gyb.as<T>() : nullptr;
+    bool fused = false;
+    fl("wlp_cols", [&] {
+      fused = lg::fl_band_col2(fg, s, tiles, nf, false, Dr.as<C>(), s_Dr, gx, gy, Wc.as<C>(), nullptr, s_Wc);
+    });
+    if (fused) return;
+    fl("wlp_colfwd", [&] {
+      lg::fl_band_colfwd(fg, s, tiles, nf, false, Dr.as<C>(), s_Dr, gx, gy, Wh.as<C>(), nullptr, s_band);
+    });
+    fl("wlp_colinv", [&] { lg::fl_band_colinv(fg, s, tiles, nf, true, Wh.as<C>(), s_band, Wc.as<C>(), s_Wc); });
+  }
+
   // ---- composite operations ---------------------------------------------------
   // Forward images for focus stacks (all F computed; caller picks one).
   void forward(const T* mask, long long m_ts, int tiles, T dose, bool want_i, bool want_r) {
@@ -721,17 +762,11 @@ struct Plan : PlanBase {
         fl("real_rows_fwd", [&] { lg::fl_real_rows_fwd(fg, s, tiles, 0, mask, m_ts, 0.f, g.ax.Pm, Mr.as<C>(), s_Mr); });
         fl("mask_cols", [&] { lg::fl_mask_cols(fg, s, tiles, Mr.as<C>(), s_Mr, Mhat.as<C>(), s_Mhat); });
         fl("socs_cols", [&] { lg::fl_socs_cols(fg, s, tiles, Mhat.as<C>(), s_Mhat, H.as<C>(), Tb.as<C>(), s_T); });
-        fl("socs_rows", [&] { lg::fl_socs_rows(fg, s, tiles, Tb.as<C>(), s_T, wk.as<T>(), dose, Ip.as<T>(), s_Ip); });
-        fl("ip_sum", [&] { lg::fl_ip_sum(fg, s, tiles, Ip.as<T>(), s_Ip, Wsub.as<T>(), s_Wsub); });
-        fl("isub_rows", [&] { lg::fl_isub_rows(fg, s, tiles, Wsub.as<T>(), s_Wsub, Ir.as<C>(), s_Ir); });
-        fl("isub_colfwd", [&] {
-          lg::fl_band_colfwd(fg, s, tiles, F, true, Ir.as<C>(), s_Ir, gxh.as<T>(), gyb.as<T>(),
-                             want_r ? Rh.as<C>() : nullptr, want_i ? Ih.as<C>() : nullptr, s_band);
+        fl("socs_rows", [&] {
+          lg::fl_socs_rows(fg, s, tiles, Tb.as<C>(), s_T, wk.as<T>(), dose, Ip.as<T>(), s_Ip, nullptr, 0);
         });
-        if (want_i)
-          fl("isub_colinv", [&] { lg::fl_band_colinv(fg, s, tiles, F, false, Ih.as<C>(), s_band, Ic.as<C>(), s_C); });
-        if (want_r)
-          fl("isub_colinv", [&] { lg::fl_band_colinv(fg, s, tiles, F, false, Rh.as<C>(), s_band, Rc.as<C>(), s_C); });
+        fl("isub_rows", [&] { lg::fl_isub_rows(fg, s, tiles, Ip.as<T>(), s_Ip, K, Ir.as<C>(), s_Ir); });
+        isub_cols_fast(tiles, want_i, want_r);
         return;
       }
     }
@@ -753,19 +788,16 @@ struct Plan : PlanBase {
         fl("socs_cols", [&] { lg::fl_socs_cols(fg, s, 1, Mhat.as<C>(), s_Mhat, H.as<C>(), Tb.as<C>(), s_T); });
         if (W) {
           fl("real_rows_fwd", [&] { lg::fl_real_rows_fwd(fg, s, 1, 0, W, 0, 0.f, g.ax.P, Dr.as<C>(), s_Dr); });
-          fl("wlp_colfwd", [&] {
-            lg::fl_band_colfwd(fg, s, 1, 1, false, Dr.as<C>(), s_Dr, nullptr, nullptr, Wh.as<C>(), nullptr, s_band);
-          });
-          fl("wlp_colinv", [&] { lg::fl_band_colinv(fg, s, 1, 1, true, Wh.as<C>(), s_band, Wc.as<C>(), s_Wc); });
+          wlp_cols_fast(1, 1, false);
           fl("wlp_rows", [&] { lg::fl_wlp_rows(fg, s, 1, 1, Wc.as<C>(), s_Wc, Wsub.as<T>(), s_Wsub); });
         }
         fl("adj_rows", [&] {
-          lg::fl_adj_rows(fg, s, 1, 1, W == nullptr, Tb.as<C>(), s_T, Wsub.as<T>(), s_Wsub, U.as<C>(), s_U);
+          lg::fl_adj_rows(fg, s, 1, 1, W == nullptr, false, Tb.as<C>(), s_T, Wsub.as<T>(), s_Wsub, U.as<C>(),
+                          s_U);
         });
         fl("adj_cols", [&] { lg::fl_adj_cols(fg, s, 1, U.as<C>(), s_U, H.as<C>(), wk.as<T>(), dose, Acc.as<C>(), s_Acc); });
-        fl("acc_sum", [&] { lg::fl_acc_sum(fg, s, 1, Acc.as<C>(), AccS.as<C>(), s_AccS); });
         fl("grad_cols", [&] {
-          lg::fl_grad_cols(fg, s, 1, AccS.as<C>(), s_AccS, Gc.as<C>(), s_Gc, nullptr, 0, 0, nullptr, 0);
+          lg::fl_grad_cols(fg, s, 1, Acc.as<C>(), s_Acc, fg.F * fg.K, Gc.as<C>(), s_Gc, nullptr, 0, 0, nullptr, 0);
         });
         fl("grad_rows", [&] {
           lg::fl_grad_rows(fg, s, 1, false, Gc.as<C>(), s_Gc, grad, 0, nullptr, 0, 0.f, 0.f, Mr.as<C>(), s_Mr,
@@ -871,27 +903,22 @@ static void ilt_run_impl(lithogpu_ilt* ilt, int iters, double* cost_user, double
       for (int it = 0; it < iters; ++it) {
         P.fl("mask_cols", [&] { lg::fl_mask_cols(fg, s, tiles, P.Mr.template as<C>(), P.s_Mr, P.Mhat.template as<C>(), P.s_Mhat); });
         P.fl("socs_cols", [&] { lg::fl_socs_cols(fg, s, tiles, P.Mhat.template as<C>(), P.s_Mhat, P.H.template as<C>(), P.Tb.template as<C>(), P.s_T); });
-        P.fl("socs_rows", [&] { lg::fl_socs_rows(fg, s, tiles, P.Tb.template as<C>(), P.s_T, P.wk.template as<T>(), dose, P.Ip.template as<T>(), P.s_Ip); });
-        P.fl("ip_sum", [&] { lg::fl_ip_sum(fg, s, tiles, P.Ip.template as<T>(), P.s_Ip, P.Wsub.template as<T>(), P.s_Wsub); });
-        P.fl("isub_rows", [&] { lg::fl_isub_rows(fg, s, tiles, P.Wsub.template as<T>(), P.s_Wsub, P.Ir.template as<C>(), P.s_Ir); });
-        P.fl("isub_colfwd", [&] {
-          lg::fl_band_colfwd(fg, s, tiles, F, true, P.Ir.template as<C>(), P.s_Ir, P.gxh.template as<T>(),
-                             P.gyb.template as<T>(), P.Rh.template as<C>(), nullptr, P.s_band);
+        C* Ef = P.store_E ? P.Eb.template as<C>() : nullptr;
+        P.fl("socs_rows", [&] {
+          lg::fl_socs_rows(fg, s, tiles, P.Tb.template as<C>(), P.s_T, P.wk.template as<T>(), dose, P.Ip.template as<T>(),
+                           P.s_Ip, Ef, P.s_E);
         });
-        P.fl("isub_colinv", [&] { lg::fl_band_colinv(fg, s, tiles, F, false, P.Rh.template as<C>(), P.s_band, P.Rc.template as<C>(), P.s_C); });
+        P.fl("isub_rows", [&] { lg::fl_isub_rows(fg, s, tiles, P.Ip.template as<T>(), P.s_Ip, P.K, P.Ir.template as<C>(), P.s_Ir); });
+        P.isub_cols_fast(tiles, false, true);
         P.fl("resist_rows", [&] {
           lg::fl_resist_rows(fg, s, tiles, P.Rc.template as<C>(), P.s_C, ilt->target.as<T>(), NN, ilt->cfd.as<T>(), beta, thr,
                              P.Dr.template as<C>(), P.s_Dr, P.costrow.template as<double>(), P.s_cr);
         });
-        P.fl("wlp_colfwd", [&] {
-          lg::fl_band_colfwd(fg, s, tiles, F, false, P.Dr.template as<C>(), P.s_Dr, P.gxh.template as<T>(),
-                             P.gyb.template as<T>(), P.Wh.template as<C>(), nullptr, P.s_band);
-        });
-        P.fl("wlp_colinv", [&] { lg::fl_band_colinv(fg, s, tiles, F, true, P.Wh.template as<C>(), P.s_band, P.Wc.template as<C>(), P.s_Wc); });
+        P.wlp_cols_fast(tiles, F, true);
         P.fl("wlp_rows", [&] { lg::fl_wlp_rows(fg, s, tiles, F, P.Wc.template as<C>(), P.s_Wc, P.Wsub.template as<T>(), P.s_Wsub); });
         P.fl("adj_rows", [&] {
-          lg::fl_adj_rows(fg, s, tiles, F, false, P.Tb.template as<C>(), P.s_T, P.Wsub.template as<T>(), P.s_Wsub,
-                          P.U.template as<C>(), P.s_U);
+          lg::fl_adj_rows(fg, s, tiles, F, false, Ef != nullptr, Ef ? Ef : P.Tb.template as<C>(), Ef ? P.s_E : P.s_T,
+                          P.Wsub.template as<T>(), P.s_Wsub, P.U.template as<C>(), P.s_U);
         });
         P.fl("adj_cols", [&] {
           lg::fl_adj_cols(fg, s, tiles, P.U.template as<C>(), P.s_U, P.H.template as<C>(), P.wk.template as<T>(), dose,
@@ -899,9 +926,8 @@ static void ilt_run_impl(lithogpu_ilt* ilt, int iters, double* cost_user, double
         });
         const long long npairs = (P.g.ay.N + 1) / 2;
         const int ncost = int(std::min<long long>(P.s_cr, F * npairs * std::max(1, lg::fast_tpr(P.g.ax.N) / 32)));
-        P.fl("acc_sum", [&] { lg::fl_acc_sum(fg, s, tiles, P.Acc.template as<C>(), P.AccS.template as<C>(), P.s_AccS); });
         P.fl("grad_cols", [&] {
-          lg::fl_grad_cols(fg, s, tiles, P.AccS.template as<C>(), P.s_AccS, P.Gc.template as<C>(), P.s_Gc,
+          lg::fl_grad_cols(fg, s, tiles, P.Acc.template as<C>(), P.s_Acc, F * P.K, P.Gc.template as<C>(), P.s_Gc,
                            P.costrow.template as<double>(), P.s_cr, ncost, ilt->cost.as<double>() + size_t(it) * tiles, 1);
         });
         P.fl("grad_rows", [&] {
@@ -1373,8 +1399,10 @@ lithogpu_status lithogpu_intensity_gradient(lithogpu_kernels* ks, int focus, con
       LG_CUDA(cudaMemcpyAsync(wf.p, P.wk.template as<T>() + size_t(P.K) * focus, sizeof(T) * P.K, cudaMemcpyDeviceToDevice, ctx->stream));
       std::swap(P.H.p, Hf.p);
       std::swap(P.wk.p, wf.p);
+      const int fgF0 = P.fg.F;
       P.F = 1;
       P.g.F = 1;
+      P.fg.F = 1;
       try {
         P.gradient(m, w, T(dose), og.work);
       } catch (...) {
@@ -1382,12 +1410,14 @@ lithogpu_status lithogpu_intensity_gradient(lithogpu_kernels* ks, int focus, con
         std::swap(P.wk.p, wf.p);
         P.F = F0;
         P.g = g0;
+        P.fg.F = fgF0;
         throw;
       }
       std::swap(P.H.p, Hf.p);
       std::swap(P.wk.p, wf.p);
       P.F = F0;
       P.g = g0;
+      P.fg.F = fgF0;
       const bool host = og.finish();
       if (host || !is_device_ptr(mask)) LG_CUDA(cudaStreamSynchronize(ctx->stream));
     };

@@ -7,7 +7,7 @@ void fl_mask_cols(const FGeo& g, cudaStream_t s, int tiles, const C32* Mr, long 
                   C32* Mhat, long long mh_ts) {
   with_len(g.ay.N, [&](auto c) {
     constexpr int L = decltype(c)::value;
-    const int gr = fgroups<L>(256);
+    const int gr = spread_groups<L>((long long)tiles * (g.ax.Pm + 1));
     flaunch<L>(fk_mask_cols<L>, dim3(cdivi(g.ax.Pm + 1, gr), 1, tiles), gr, s, g, Mr, mr_ts, Mhat,
                 mh_ts);
   });
@@ -51,21 +51,53 @@ void fl_adj_cols(const FGeo& g, cudaStream_t s, int tiles, const C32* U, long lo
                  const C32* H, const float* wk, float dose, C32* Accp, long long a_ts) {
   with_len(g.ay.n, [&](auto c) {
     constexpr int L = decltype(c)::value;
-    const int gr = fgroups<L>(256);
-    flaunch<L>(fk_adj_cols<L>, dim3(cdivi(g.ax.B, gr), g.F * g.K, tiles), gr, s, g, U, u_ts, H, wk, dose,
-               Accp, a_ts);
+    const int kg = kgroups<L>(g.K);
+    flaunch<L>(fk_adj_cols<L>, dim3(g.ax.B, g.F * g.K / kg, tiles), kg, s, g, U, u_ts, H, wk, dose, Accp,
+               a_ts);
   });
 }
 
-void fl_grad_cols(const FGeo& g, cudaStream_t s, int tiles, const C32* Acc, long long a_ts, C32* Gc,
-                  long long g_ts, const double* costp, long long cp_ts, int ncost,
+void fl_grad_cols(const FGeo& g, cudaStream_t s, int tiles, const C32* Acc, long long a_ts, int nsum,
+                  C32* Gc, long long g_ts, const double* costp, long long cp_ts, int ncost,
                   double* cost_out, long long co_ts) {
   with_len(g.ay.N, [&](auto c) {
     constexpr int L = decltype(c)::value;
     const int gr = 1;  // one column per CTA: Pm+1 is small, spread it over SMs
-    flaunch<L>(fk_grad_cols<L>, dim3(cdivi(g.ax.Pm + 1, gr) + 1, 1, tiles), gr, s, g, Acc, a_ts, Gc,
+    with_len(g.ay.n, [&](auto cn) { nsum /= kgroups<decltype(cn)::value>(g.K); });  // fk_adj_cols partials
+    flaunch<L>(fk_grad_cols<L>, dim3(cdivi(g.ax.Pm + 1, gr) + 1, 1, tiles), gr, s, g, Acc, a_ts, nsum, Gc,
                 g_ts, costp, cp_ts, ncost, cost_out, co_ts);
   });
+}
+
+bool fl_band_col2(const FGeo& g, cudaStream_t s, int tiles, int nf, bool sub_in, const C32* in,
+                  long long in_ts, const float* gxh, const float* gyb, C32* outR, C32* outI,
+                  long long o_ts) {
+  // sub_in: n -> N (intensity band -> resist columns); else N -> n (W band)
+  const int Lin = sub_in ? g.ay.n : g.ay.N, Lout = sub_in ? g.ay.N : g.ay.n;
+  const float inv = float(1.0 / (double(sub_in ? g.ax.n : g.ax.N) * double(Lin)));
+  bool done = false;
+  with_len(Lin, [&](auto ci) {
+    constexpr int LI = decltype(ci)::value;
+    with_len(Lout, [&](auto co) {
+      constexpr int LO = decltype(co)::value;
+      using CP = Col2<LI, LO>;
+      constexpr int LBIG = LI > LO ? LI : LO, LSM = LI > LO ? LO : LI;
+      constexpr bool pair = (LBIG == 1024 || LBIG == 2048 || LBIG == 4096) && LSM >= 256 && LSM <= 1536;
+      if constexpr (pair && CP::ok && CP::TPR <= 256) {
+        const int gr = CP::TPR >= 128 ? 1 : 128 / CP::TPR;
+        const size_t smem = size_t(gr) * (CP::SM + 2 * CP::NB) * sizeof(C32);
+        static size_t set_bytes = 0;
+        if (smem > 48 * 1024 && smem > set_bytes) {
+          cudaFuncSetAttribute(fk_band_col2<LI, LO>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+          set_bytes = smem;
+        }
+        pdl_launch(fk_band_col2<LI, LO>, dim3(cdivi(g.ax.P + 1, gr), nf, tiles), dim3(gr * CP::TPR), smem, s,
+                   g, in, in_ts, inv, gxh, gyb, outR, outI, o_ts);
+        done = true;
+      }
+    });
+  });
+  return done;
 }
 
 }  // namespace lg

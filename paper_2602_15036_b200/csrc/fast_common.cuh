@@ -37,6 +37,28 @@ inline int fgroups(int target, int cap = 1 << 30) {
   return gr;
 }
 
+// kernel groups per CTA for the (row|column) x kernel-group kernels: the
+// largest power of two <= 256/TPR that divides K
+template <int L>
+inline int kgroups(int K) {
+  int kg = 256 / RPlan<L>::TPR;
+  if (kg < 1) kg = 1;
+  if (RPlan<L>::TPR > 32 && kg > 15) kg = 8;
+  while (kg > 1 && K % kg) kg >>= 1;
+  return kg;
+}
+
+// groups per CTA for low-parallelism transforms: spread `units` row groups
+// over the SMs first (>= ~2 CTAs per SM before packing groups together)
+template <int L>
+inline int spread_groups(long long units, int cap = 8) {
+  constexpr int TPR = RPlan<L>::TPR;
+  long long gr = units / (2 * 148);
+  int g = 1;
+  while (g * 2 <= gr && g * 2 <= cap && g * 2 * TPR <= 256) g *= 2;
+  return g;
+}
+
 // launch with `extra` bytes of shared memory after the row-group buffers
 template <int L, typename K, typename... A>
 inline void flaunch_x(K kern, dim3 grid, int groups, size_t extra, cudaStream_t s, A... args) {

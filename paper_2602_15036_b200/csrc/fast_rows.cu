@@ -43,34 +43,23 @@ void fl_real_rows_fwd(const FGeo& g, cudaStream_t s, int tiles, int mode, const 
 }
 
 void fl_socs_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* T, long long t_ts,
-                  const float* wk, float dose, float* Ip, long long ip_ts) {
+                  const float* wk, float dose, float* Ip, long long ip_ts, C32* Eo, long long e_ts) {
   with_len(g.ax.n, [&](auto c) {
     constexpr int L = decltype(c)::value;
-    const int gr = fgroups<L>(256);
-    flaunch<L>(fk_socs_rows<L>, dim3(cdivi(g.ay.n, gr), g.F * g.K, tiles), gr, s, g, T, t_ts, wk, dose, Ip,
-               ip_ts);
+    const int kg = kgroups<L>(g.K);
+    flaunch<L>(fk_socs_rows<L>, dim3(g.ay.n, g.F * g.K / kg, tiles), kg, s, g, T, t_ts, wk, dose, Ip, ip_ts,
+               Eo, e_ts);
   });
 }
 
-void fl_isub_rows(const FGeo& g, cudaStream_t s, int tiles, const float* Ip, long long ip_ts, C32* Ir,
-                  long long ir_ts) {
+void fl_isub_rows(const FGeo& g, cudaStream_t s, int tiles, const float* Ip, long long ip_ts, int nsum,
+                  C32* Ir, long long ir_ts) {
   with_len(g.ax.n, [&](auto c) {
     constexpr int L = decltype(c)::value;
-    const int gr = fgroups<L>(256);
-    flaunch<L>(fk_isub_rows<L>, dim3(cdivi((g.ay.n + 1) / 2, gr), g.F, tiles), gr, s, g, Ip, ip_ts, Ir,
-               ir_ts);
+    const int gr = spread_groups<L>((long long)tiles * g.F * ((g.ay.n + 1) / 2));
+    flaunch<L>(fk_isub_rows<L>, dim3(cdivi((g.ay.n + 1) / 2, gr), g.F, tiles), gr, s, g, Ip, ip_ts,
+               nsum / kgroups<L>(g.K), Ir, ir_ts);
   });
-}
-
-void fl_ip_sum(const FGeo& g, cudaStream_t s, int tiles, const float* Ip, long long ip_ts, float* Isub,
-               long long is_ts) {
-  const int n4 = (g.ay.n * g.ax.n) / 4;
-  pdl_launch(fk_ip_sum, dim3(cdivi(n4, 256), g.F, tiles), dim3(256), 0, s, g, Ip, ip_ts, Isub, is_ts);
-}
-
-void fl_acc_sum(const FGeo& g, cudaStream_t s, int tiles, const C32* Accp, C32* Acc, long long a_ts) {
-  const int n = g.ax.B * g.ay.B;
-  pdl_launch(fk_acc_sum, dim3(cdivi(n, 256), 1, tiles), dim3(256), 0, s, g, Accp, Acc, a_ts);
 }
 
 void fl_resist_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* Rc, long long c_ts,
@@ -99,23 +88,24 @@ void fl_wlp_rows(const FGeo& g, cudaStream_t s, int tiles, int nf, const C32* Wc
                  float* Wsub, long long ws_ts) {
   with_len(g.ax.n, [&](auto c) {
     constexpr int L = decltype(c)::value;
-    const int gr = fgroups<L>(256);
+    const int gr = spread_groups<L>((long long)tiles * nf * ((g.ay.n + 1) / 2));
     flaunch<L>(fk_wlp_rows<L>, dim3(cdivi((g.ay.n + 1) / 2, gr), nf, tiles), gr, s, g, Wc, w_ts,
                 Wsub, ws_ts);
   });
 }
 
-void fl_adj_rows(const FGeo& g, cudaStream_t s, int tiles, int nf, bool uniform, const C32* T,
-                 long long t_ts, const float* Wsub, long long ws_ts, C32* U, long long u_ts) {
+void fl_adj_rows(const FGeo& g, cudaStream_t s, int tiles, int nf, bool uniform, bool from_e,
+                 const C32* T, long long t_ts, const float* Wsub, long long ws_ts, C32* U, long long u_ts) {
   with_len(g.ax.n, [&](auto c) {
     constexpr int L = decltype(c)::value;
     const int gr = fgroups<L>(256);
     const dim3 grid(cdivi(g.ay.n, gr), nf * g.K, tiles);
     const size_t extra = size_t(g.ax.B) * (gr | 1) * sizeof(C32);  // staging tile
+    auto go = [&](auto kern) { flaunch_x<L>(kern, grid, gr, extra, s, g, T, t_ts, Wsub, ws_ts, U, u_ts); };
     if (uniform)
-      flaunch_x<L>(fk_adj_rows<L, true>, grid, gr, extra, s, g, T, t_ts, Wsub, ws_ts, U, u_ts);
+      from_e ? go(fk_adj_rows<L, true, true>) : go(fk_adj_rows<L, true, false>);
     else
-      flaunch_x<L>(fk_adj_rows<L, false>, grid, gr, extra, s, g, T, t_ts, Wsub, ws_ts, U, u_ts);
+      from_e ? go(fk_adj_rows<L, false, true>) : go(fk_adj_rows<L, false, false>);
   });
 }
 

@@ -138,22 +138,24 @@ __global__ void __launch_bounds__(256) fk_real_rows_fwd(FGeo g, const float* __r
 }
 
 // ===========================================================================
-// per-kernel rows, one (subgrid row sy, kernel f*K+k) per row group:
-//   Ip[fk][sy][sx] = dose w_fk |IFFT_nx(T_fk[sy])|^2
-// (no cross-group reduction: the fixed-order sum over k is fk_isub_rows).
-// grid (ceil(ny/groups), F*K, tiles)
+// per-kernel rows: CTA = one subgrid row sy x KG consecutive kernels (one per
+// row group), each group  E = IFFT_nx(T_fk[sy]),  then the KG intensity rows
+// dose w_fk |E|^2 are summed in shared memory in fixed group order:
+//   Ip[f][kg][sy][sx] = sum_{k in group kg} dose w_fk |E_fk|^2
+// (fk_isub_rows sums the K/KG partials, again in fixed order).
+// Eo (nullable) keeps E_fk[sy][x] for the adjoint rows.
+// grid (ny, F*K/KG, tiles), KG = blockDim / TPR divides K
 // ===========================================================================
 template <int L>
 __global__ void __launch_bounds__(256) fk_socs_rows(FGeo g, const C32* __restrict__ T,
                                                     long long t_ts, const float* __restrict__ wk,
                                                     float dose, float* __restrict__ Ip,
-                                                    long long ip_ts) {
+                                                    long long ip_ts, C32* __restrict__ Eo,
+                                                    long long e_ts) {
   FGroup<L> G;
   constexpr int E = RPlan<L>::E;
-  const int fk = blockIdx.y, Bx = g.ax.B, ny = g.ay.n, lo = g.ax.lo, hi = g.ax.hi;
-  const int sy0 = blockIdx.x * G.groups + G.gid;
-  const bool act = sy0 < ny;
-  const int sy = act ? sy0 : ny - 1;
+  const int Bx = g.ax.B, ny = g.ay.n, lo = g.ax.lo, hi = g.ax.hi;
+  const int sy = blockIdx.x, fk = blockIdx.y * G.groups + G.gid;
   const C32* src = T + blockIdx.z * t_ts + size_t(fk) * ny * Bx + size_t(sy) * Bx;
   C32 v[E];
 #pragma unroll
@@ -162,11 +164,26 @@ __global__ void __launch_bounds__(256) fk_socs_rows(FGeo g, const C32* __restric
     v[e] = sl >= 0 ? src[sl] : mk(0.f, 0.f);
   }
   fftr<float, L, +1>(v, G.sm, g.twnx, G.t, G.sync);
-  if (!act) return;
-  const float w = wk[fk] * dose;
-  float* o = Ip + blockIdx.z * ip_ts + (size_t(fk) * ny + sy) * L;
+  if (Eo) {  // keep the coherent field for the adjoint (fk_adj_rows<.., FROM_E>)
+    C32* eo = Eo + blockIdx.z * e_ts + (size_t(fk) * ny + sy) * L;
 #pragma unroll
-  for (int e = 0; e < E; ++e) o[G.idx(e)] = w * (v[e].x * v[e].x + v[e].y * v[e].y);
+    for (int e = 0; e < E; ++e) eo[G.idx(e)] = v[e];
+  }
+  const float w = wk[fk] * dose;
+  G.sync();  // group done with its exchange buffer: reuse it for the row
+  float* red = reinterpret_cast<float*>(G.sm);
+#pragma unroll
+  for (int e = 0; e < E; ++e) red[G.idx(e)] = w * (v[e].x * v[e].x + v[e].y * v[e].y);
+  __syncthreads();
+  extern __shared__ __align__(16) unsigned char fsm_raw[];
+  const float* base = reinterpret_cast<const float*>(fsm_raw);
+  constexpr int stride = 2 * rsm_len<L>();
+  float* o = Ip + blockIdx.z * ip_ts + (size_t(blockIdx.y) * ny + sy) * L;
+  for (int x = threadIdx.x; x < L; x += blockDim.x) {
+    float acc = base[x];
+    for (int gg = 1; gg < G.groups; ++gg) acc += base[gg * stride + x];
+    o[x] = acc;
+  }
 }
 
 // ===========================================================================
@@ -176,7 +193,7 @@ __global__ void __launch_bounds__(256) fk_socs_rows(FGeo g, const C32* __restric
 // ===========================================================================
 template <int L>
 __global__ void __launch_bounds__(256) fk_isub_rows(FGeo g, const float* __restrict__ Ip,
-                                                    long long ip_ts, C32* __restrict__ Ir,
+                                                    long long ip_ts, int nsum, C32* __restrict__ Ir,
                                                     long long ir_ts) {
   FGroup<L> G;
   constexpr int E = RPlan<L>::E;
@@ -186,12 +203,26 @@ __global__ void __launch_bounds__(256) fk_isub_rows(FGeo g, const float* __restr
   const int pair = act ? pair0 : npairs - 1;
   const int sy0 = 2 * pair;
   const bool has1 = sy0 + 1 < ny;
-  // Isub (already summed over k by fk_ip_sum) rows sy0, sy0+1
-  const float* is = Ip + blockIdx.z * ip_ts + size_t(f) * ny * L;
+  // Isub rows sy0, sy0+1 = sum over the nsum per-kernel partials Ip[f][k]
+  // (fixed order k = 0, 1, ..: deterministic, same bits as a separate pass)
+  const size_t plane = size_t(ny) * L;
+  const float* is = Ip + blockIdx.z * ip_ts + size_t(f) * nsum * plane;
+  const int sy1 = has1 ? sy0 + 1 : sy0;
   C32 v[E];
 #pragma unroll
-  for (int e = 0; e < E; ++e)
-    v[e] = mk(is[size_t(sy0) * L + G.idx(e)], has1 ? is[size_t(sy0 + 1) * L + G.idx(e)] : 0.f);
+  for (int e = 0; e < E; ++e) v[e] = mk(0.f, 0.f);
+  for (int k = 0; k < nsum; ++k) {
+    const float* a = is + k * plane;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      v[e].x += __ldg(a + size_t(sy0) * L + G.idx(e));
+      v[e].y += __ldg(a + size_t(sy1) * L + G.idx(e));
+    }
+  }
+  if (!has1) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e].y = 0.f;
+  }
   fftr<float, L, -1>(v, G.sm, g.twnx, G.t, G.sync);
   G.sync();
   to_smem<float, L>(v, G.sm, G.t);
@@ -204,45 +235,6 @@ __global__ void __launch_bounds__(256) fk_isub_rows(FGeo g, const float* __restr
     o[size_t(px) * ny + sy0] = A;
     if (has1) o[size_t(px) * ny + sy0 + 1] = Bv;
   }
-}
-
-// ===========================================================================
-// Isub[f][i] = sum_k Ip[f][k][i] (fixed order; 4 elements per thread)
-// grid (ceil(ny*nx/1024), F, tiles)
-// ===========================================================================
-static __global__ void fk_ip_sum(FGeo g, const float* __restrict__ Ip, long long ip_ts,
-                                 float* __restrict__ Isub, long long is_ts) {
-  pdl_entry();
-  const int n4 = (g.ay.n * g.ax.n) / 4, K = g.K, f = blockIdx.y;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n4) return;
-  const float4* a = reinterpret_cast<const float4*>(Ip + blockIdx.z * ip_ts + size_t(f) * K * 4 * n4);
-  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 8
-  for (int k = 0; k < K; ++k) {
-    const float4 x = __ldg(a + size_t(k) * n4 + i);
-    s.x += x.x;
-    s.y += x.y;
-    s.z += x.z;
-    s.w += x.w;
-  }
-  reinterpret_cast<float4*>(Isub + blockIdx.z * is_ts + size_t(f) * 4 * n4)[i] = s;
-}
-
-// ===========================================================================
-// Acc[cx][qy] = sum_fk Accp[fk][cx][qy]  (fixed order, elementwise)
-// ===========================================================================
-static __global__ void fk_acc_sum(FGeo g, const C32* __restrict__ Accp, C32* __restrict__ Acc,
-                                  long long a_ts) {
-  pdl_entry();
-  const int n = g.ax.B * g.ay.B, FK = g.F * g.K;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const C32* a = Accp + blockIdx.z * a_ts;
-  C32 s = mk(0.f, 0.f);
-#pragma unroll 8
-  for (int fk = 0; fk < FK; ++fk) s = add(s, ldg_cx(a + size_t(fk) * n + i));
-  Acc[blockIdx.z * a_ts + i] = s;
 }
 
 // ===========================================================================
@@ -379,7 +371,7 @@ __global__ void __launch_bounds__(256) fk_wlp_rows(FGeo g, const C32* __restrict
 //   U_fk[qx][sy] = FFT_nx(W_lp(sy,.) . IFFT_nx(T_fk[sy]))(qx), qx in band
 // grid (ceil(ny/groups), F*K, tiles)
 // ===========================================================================
-template <int L, bool UNIFORM>
+template <int L, bool UNIFORM, bool FROM_E>
 __global__ void __launch_bounds__(256, 2) fk_adj_rows(FGeo g, const C32* __restrict__ T,
                                                       long long t_ts, const float* __restrict__ Wsub,
                                                       long long ws_ts, C32* __restrict__ U,
@@ -392,12 +384,18 @@ __global__ void __launch_bounds__(256, 2) fk_adj_rows(FGeo g, const C32* __restr
   const int sy0 = r0 + G.gid;
   const bool act = sy0 < ny;
   const int sy = act ? sy0 : ny - 1;
-  const C32* src = T + blockIdx.z * t_ts + size_t(fk) * ny * Bx + size_t(sy) * Bx;
   C32 v[E];
+  if (FROM_E) {  // T holds the fields E_fk[sy][x] kept by fk_socs_rows
+    const C32* src = T + blockIdx.z * t_ts + (size_t(fk) * ny + sy) * L;
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int sl = kslot(G.idx(e), lo, hi, L);
-    v[e] = sl >= 0 ? src[sl] : mk(0.f, 0.f);
+    for (int e = 0; e < E; ++e) v[e] = src[G.idx(e)];
+  } else {
+    const C32* src = T + blockIdx.z * t_ts + size_t(fk) * ny * Bx + size_t(sy) * Bx;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int sl = kslot(G.idx(e), lo, hi, L);
+      v[e] = sl >= 0 ? src[sl] : mk(0.f, 0.f);
+    }
   }
   float wv[E];
   if (!UNIFORM) {
@@ -405,7 +403,7 @@ __global__ void __launch_bounds__(256, 2) fk_adj_rows(FGeo g, const C32* __restr
 #pragma unroll
     for (int e = 0; e < E; ++e) wv[e] = w[G.idx(e)];
   }
-  fftr<float, L, +1>(v, G.sm, g.twnx, G.t, G.sync);
+  if (!FROM_E) fftr<float, L, +1>(v, G.sm, g.twnx, G.t, G.sync);
   if (!UNIFORM) {
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = scale(v[e], wv[e]);
@@ -656,10 +654,95 @@ __global__ void __launch_bounds__(256) fk_band_colinv(FGeo g, const C32* __restr
 }
 
 // ===========================================================================
-// adjoint columns, one (band column cx, f*K+k) per group:
-//   Accp[fk][cx][qy] = FFT_ny(U_fk[cx])(qy) conj(H_fk(qy,cx)) 2 dose w_fk (N/n)^2/N^2
-// (the sum over fk happens in fk_grad_cols, fixed order).
-// grid (ceil(Bx/groups), F*K, tiles)
+// fused band resampling column: out[f][y][px] = IFFT_LOUT(band(FFT_LIN(in[f][px]))
+// s(j,px)), i.e. fk_band_colfwd + fk_band_colinv without the band round trip.
+// One column per group of max(TPR_in, TPR_out) threads; the smaller plan runs
+// on the group's leading warps.  outI (optional) gets the unscaled band.
+// grid (ceil((Px+1)/groups), nf, tiles)
+// ===========================================================================
+template <int LIN, int LOUT>
+struct Col2 {
+  static constexpr int TIN = RPlan<LIN>::TPR, TOUT = RPlan<LOUT>::TPR;
+  static constexpr int TPR = TIN > TOUT ? TIN : TOUT;
+  static constexpr int SM = rsm_len<LIN>() > rsm_len<LOUT>() ? rsm_len<LIN>() : rsm_len<LOUT>();
+  static constexpr int NB = LIN < LOUT ? LIN : LOUT;  // >= nb2
+  static constexpr bool ok = TIN % 32 == 0 && TOUT % 32 == 0;
+};
+
+__device__ __forceinline__ GSync sub_gsync(int nthreads, int id) {
+  GSync s;
+  s.n = nthreads;
+  s.id = nthreads == 32 ? 0 : id;
+  return s;
+}
+
+template <int LIN, int LOUT>
+__global__ void __launch_bounds__(256) fk_band_col2(FGeo g, const C32* __restrict__ in,
+                                                    long long in_ts, float inv,
+                                                    const float* __restrict__ gxh,
+                                                    const float* __restrict__ gyb,
+                                                    C32* __restrict__ outR, C32* __restrict__ outI,
+                                                    long long o_ts) {
+  pdl_entry();
+  using CP = Col2<LIN, LOUT>;
+  constexpr int EI = RPlan<LIN>::E, EO = RPlan<LOUT>::E;
+  extern __shared__ __align__(16) unsigned char fsm_raw[];
+  const int groups = blockDim.x / CP::TPR, gid = threadIdx.x / CP::TPR, t = threadIdx.x % CP::TPR;
+  C32* sm = reinterpret_cast<C32*>(fsm_raw) + gid * CP::SM;
+  C32* bbR = reinterpret_cast<C32*>(fsm_raw) + groups * CP::SM + gid * 2 * CP::NB;
+  C32* bbI = bbR + CP::NB;
+  // barriers: 1..groups whole group, groups+1.. leading sub-group
+  const GSync gsync = groups == 1 ? GSync{-1, CP::TPR} : GSync{1 + gid, CP::TPR};
+  const int Px = g.ax.P, f = blockIdx.y;
+  const int px0 = blockIdx.x * groups + gid;
+  const bool act = px0 <= Px;
+  const int px = act ? px0 : Px;
+  if (t < CP::TIN) {
+    const GSync s1 = CP::TIN == CP::TPR ? gsync : sub_gsync(CP::TIN, 1 + groups + gid);
+    const C32* src = in + blockIdx.z * in_ts + (size_t(f) * (Px + 1) + px) * LIN;
+    C32 v[EI];
+#pragma unroll
+    for (int e = 0; e < EI; ++e) v[e] = src[t + e * CP::TIN];
+    fftr<float, LIN, -1>(v, sm, LIN == g.ay.N ? g.twNy : g.twny, t, s1);
+    const float gx = gxh ? gxh[px] : 1.f;
+#pragma unroll
+    for (int e = 0; e < EI; ++e) {
+      const int j = islot(g.ay, t + e * CP::TIN, LIN);
+      if (j < 0) continue;
+      const C32 c = scale(v[e], inv);
+      if (outI) bbI[j] = c;
+      bbR[j] = gyb ? scale(c, gx * gyb[j]) : c;
+    }
+  }
+  gsync();
+  if (t >= CP::TOUT) return;
+  const GSync s2 = CP::TOUT == CP::TPR ? gsync : sub_gsync(CP::TOUT, 1 + groups + gid);
+  const size_t ob = blockIdx.z * o_ts + size_t(f) * LOUT * (Px + 1);
+  for (int pass = 0; pass < 2; ++pass) {
+    C32* out = pass == 0 ? outR : outI;
+    if (!out) continue;
+    const C32* bb = pass == 0 ? bbR : bbI;
+    C32 v[EO];
+#pragma unroll
+    for (int e = 0; e < EO; ++e) {
+      const int j = islot(g.ay, t + e * CP::TOUT, LOUT);
+      v[e] = j >= 0 ? bb[j] : mk(0.f, 0.f);
+    }
+    fftr<float, LOUT, +1>(v, sm, LOUT == g.ay.N ? g.twNy : g.twny, t, s2);
+    if (act) {
+#pragma unroll
+      for (int e = 0; e < EO; ++e) out[ob + size_t(t + e * CP::TOUT) * (Px + 1) + px] = v[e];
+    }
+    s2();  // sm reused by the second pass
+  }
+}
+
+// ===========================================================================
+// adjoint columns: CTA = one band column cx x KG consecutive kernels (one per
+// group), each FFT_ny(U_fk[cx]) conj(H_fk(.,cx)) 2 dose w_fk (N/n)^2/N^2 over
+// the kernel band, summed over the CTA's kernels in fixed group order:
+//   Accp[fk/KG][cx][qy]   (fk_grad_cols sums the F*K/KG partials, fixed order)
+// grid (Bx, F*K/KG, tiles)
 // ===========================================================================
 template <int L>
 __global__ void __launch_bounds__(256) fk_adj_cols(FGeo g, const C32* __restrict__ U,
@@ -668,24 +751,29 @@ __global__ void __launch_bounds__(256) fk_adj_cols(FGeo g, const C32* __restrict
                                                    C32* __restrict__ Accp, long long a_ts) {
   FGroup<L> G;
   constexpr int E = RPlan<L>::E;
-  const int Bx = g.ax.B, By = g.ay.B, fk = blockIdx.y;
-  const int cx0 = blockIdx.x * G.groups + G.gid;
-  const bool act = cx0 < Bx;
-  const int cx_ = act ? cx0 : Bx - 1;
+  const int Bx = g.ax.B, By = g.ay.B, cx = blockIdx.x, fk = blockIdx.y * G.groups + G.gid;
   const float sc = float(2.0 / (double(g.ax.n) * double(g.ay.n)));  // 2 (N/n)^2 / N^2
-  const C32* src = U + blockIdx.z * u_ts + (size_t(fk) * Bx + cx_) * L;
+  const C32* src = U + blockIdx.z * u_ts + (size_t(fk) * Bx + cx) * L;
   C32 v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) v[e] = src[G.idx(e)];
   fftr<float, L, -1>(v, G.sm, g.twny, G.t, G.sync);
-  if (!act) return;
   const float w = wk[fk] * dose * sc;
   const C32* h = H + size_t(fk) * By * Bx;
-  C32* o = Accp + blockIdx.z * a_ts + (size_t(fk) * Bx + cx_) * By;
+  G.sync();
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int jy = kslot(G.idx(e), g.ay.lo, g.ay.hi, L);
-    if (jy >= 0) o[jy] = scale(mulc(v[e], ldg_cx(h + size_t(jy) * Bx + cx_)), w);
+    if (jy >= 0) G.sm[jy] = scale(mulc(v[e], ldg_cx(h + size_t(jy) * Bx + cx)), w);
+  }
+  __syncthreads();
+  extern __shared__ __align__(16) unsigned char fsm_raw[];
+  const C32* base = reinterpret_cast<const C32*>(fsm_raw);
+  C32* o = Accp + blockIdx.z * a_ts + (size_t(blockIdx.y) * Bx + cx) * By;
+  for (int jy = threadIdx.x; jy < By; jy += blockDim.x) {
+    C32 acc = base[jy];
+    for (int gg = 1; gg < G.groups; ++gg) acc = add(acc, base[gg * rsm_len<L>() + jy]);
+    o[jy] = acc;
   }
 }
 
@@ -696,7 +784,7 @@ __global__ void __launch_bounds__(256) fk_adj_cols(FGeo g, const C32* __restrict
 // ===========================================================================
 template <int L>
 __global__ void __launch_bounds__(256) fk_grad_cols(FGeo g, const C32* __restrict__ Acc,
-                                                    long long a_ts, C32* __restrict__ Gc,
+                                                    long long a_ts, int nsum, C32* __restrict__ Gc,
                                                     long long g_ts, const double* __restrict__ costp,
                                                     long long cp_ts, int ncost,
                                                     double* __restrict__ cost_out, long long co_ts) {
@@ -720,9 +808,12 @@ __global__ void __launch_bounds__(256) fk_grad_cols(FGeo g, const C32* __restric
   const int px0 = blockIdx.x * G.groups + G.gid;
   const bool act = px0 <= Pm;
   const int px = act ? px0 : Pm;
-  const C32* a = Acc + blockIdx.z * a_ts;  // summed over (f,k): [cx][qy]
+  // Acc holds nsum per-(f,k) partials [fk][cx][qy]; they are summed here in
+  // fixed order (deterministic, same bits as a separate reduction pass)
+  const C32* a = Acc + blockIdx.z * a_ts;
   const int sp = band_slot(g.ax, px), sn = band_slot(g.ax, -px);
   const int By = g.ay.B;
+  const size_t plane = size_t(Bx) * By;
   C32 v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) {
@@ -730,8 +821,16 @@ __global__ void __launch_bounds__(256) fk_grad_cols(FGeo g, const C32* __restric
     const int jp = kslot(i, g.ay.lo, g.ay.hi, L);
     const int jn = kslot((i == 0 ? 0 : L - i), g.ay.lo, g.ay.hi, L);
     C32 s = mk(0.f, 0.f);
-    if (sp >= 0 && jp >= 0) s = add(s, a[size_t(sp) * By + jp]);
-    if (sn >= 0 && jn >= 0) s = add(s, conjg(a[size_t(sn) * By + jn]));
+    if (sp >= 0 && jp >= 0) {
+      C32 q = mk(0.f, 0.f);
+      for (int k = 0; k < nsum; ++k) q = add(q, ldg_cx(a + k * plane + size_t(sp) * By + jp));
+      s = add(s, q);
+    }
+    if (sn >= 0 && jn >= 0) {
+      C32 q = mk(0.f, 0.f);
+      for (int k = 0; k < nsum; ++k) q = add(q, ldg_cx(a + k * plane + size_t(sn) * By + jn));
+      s = add(s, conjg(q));
+    }
     v[e] = scale(s, 0.5f);
   }
   fftr<float, L, +1>(v, G.sm, g.twNy, G.t, G.sync);

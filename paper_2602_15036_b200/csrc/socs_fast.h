@@ -36,13 +36,13 @@ void fast_fill_twiddles(int len, C32* host_out);  // fftr per-stage layout
 // ---- row kernels (fast_rows.cu) ----
 void fl_real_rows_fwd(const FGeo& g, cudaStream_t s, int tiles, int mode, const float* src,
                       long long src_ts, float steep, int Pout, C32* out, long long out_ts);
+// Eo (nullable): keep the coherent fields E_fk[sy][x] for fl_adj_rows(from_e)
 void fl_socs_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* T, long long t_ts,
-                  const float* wk, float dose, float* Ip, long long ip_ts);
-void fl_isub_rows(const FGeo& g, cudaStream_t s, int tiles, const float* Ip, long long ip_ts, C32* Ir,
-                  long long ir_ts);
-void fl_ip_sum(const FGeo& g, cudaStream_t s, int tiles, const float* Ip, long long ip_ts, float* Isub,
-               long long is_ts);
-void fl_acc_sum(const FGeo& g, cudaStream_t s, int tiles, const C32* Accp, C32* Acc, long long a_ts);
+                  const float* wk, float dose, float* Ip, long long ip_ts, C32* Eo, long long e_ts);
+// sums the per-kernel-group partials of Ip written by fl_socs_rows (fixed
+// order) before the row transform; nsum = K (the launcher divides by the groups)
+void fl_isub_rows(const FGeo& g, cudaStream_t s, int tiles, const float* Ip, long long ip_ts, int nsum,
+                  C32* Ir, long long ir_ts);
 void fl_resist_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* Rc, long long c_ts,
                     const float* target, long long tg_ts, const float* cf, float beta, float thr,
                     C32* Dr, long long d_ts, double* costp, long long cp_ts);
@@ -51,8 +51,9 @@ void fl_out_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* Ic, const 
                  float thr);
 void fl_wlp_rows(const FGeo& g, cudaStream_t s, int tiles, int nf, const C32* Wc, long long w_ts,
                  float* Wsub, long long ws_ts);
-void fl_adj_rows(const FGeo& g, cudaStream_t s, int tiles, int nf, bool uniform, const C32* T,
-                 long long t_ts, const float* Wsub, long long ws_ts, C32* U, long long u_ts);
+// from_e: T holds E_fk[sy][x] (fl_socs_rows Eo) instead of the column pass T_fk[sy][cx]
+void fl_adj_rows(const FGeo& g, cudaStream_t s, int tiles, int nf, bool uniform, bool from_e,
+                 const C32* T, long long t_ts, const float* Wsub, long long ws_ts, C32* U, long long u_ts);
 void fl_grad_rows(const FGeo& g, cudaStream_t s, int tiles, bool ilt, const C32* Gc, long long g_ts,
                   float* grad, long long gr_ts, float* theta, long long th_ts, float steep,
                   float step, C32* Mr, long long mr_ts, double* gmaxp, long long gm_ts);
@@ -71,8 +72,15 @@ void fl_band_colinv(const FGeo& g, cudaStream_t s, int tiles, int nf, bool sub, 
                     long long b_ts, C32* out, long long o_ts);
 void fl_adj_cols(const FGeo& g, cudaStream_t s, int tiles, const C32* U, long long u_ts,
                  const C32* H, const float* wk, float dose, C32* Acc, long long a_ts);
-void fl_grad_cols(const FGeo& g, cudaStream_t s, int tiles, const C32* Acc, long long a_ts, C32* Gc,
-                  long long g_ts, const double* costp, long long cp_ts, int ncost,
+// Acc: the per-kernel-group partials of fl_adj_cols, summed in fixed order;
+// nsum = F*K (the launcher divides by the groups)
+void fl_grad_cols(const FGeo& g, cudaStream_t s, int tiles, const C32* Acc, long long a_ts, int nsum,
+                  C32* Gc, long long g_ts, const double* costp, long long cp_ts, int ncost,
                   double* cost_out, long long co_ts);
+// fused fl_band_colfwd + fl_band_colinv (false when the plan pair is not
+// supported: caller falls back to the two-pass form)
+bool fl_band_col2(const FGeo& g, cudaStream_t s, int tiles, int nf, bool sub_in, const C32* in,
+                  long long in_ts, const float* gxh, const float* gyb, C32* outR, C32* outI,
+                  long long o_ts);
 
 }  // namespace lg

@@ -170,3 +170,63 @@ def test_threshold_semantics(ctx):
     v = np.array([0.1, 0.25, 0.2500001, 0.3, 0.0])
     out = L.threshold(v, 0.25, ctx)
     assert out.tolist() == [0.0, 1.0, 1.0, 1.0, 0.0]
+
+
+def test_gradient_selects_focus_stack(ctx):
+    """intensity_gradient on stack `focus` of a multi-focus set (fp32 fast path
+    views the stack as a one-focus plan)."""
+    rng = np.random.default_rng(17)
+    ks = kernels_for(256, 1.0, (-40.0, 0.0, 40.0), k=8, grid_n=21)
+    mask = rng.random((256, 256))
+    W = rng.standard_normal((256, 256))
+    for f in (0, 2):
+        want = O.weighted_gradient(mask, ks.weights[f], ks.support, ks.values[f], W, dose=1.1)
+        got = L.intensity_gradient(mask, ks, 1.1, weight=W, focus=f, precision="f32", ctx=ctx)
+        assert rel_linf(got, want) < 1e-4
+
+
+@pytest.mark.parametrize("n,F,K", [(256, 1, 16), (512, 3, 8)])
+def test_ilt_multi_iteration_graph_vs_oracle(ctx, n, F, K):
+    """several ILT iterations in one call, repeated so the CUDA-graph capture
+    and replay paths both run, against the oracle iterated the same way."""
+    rng = np.random.default_rng(11 * n + F)
+    foci = [-40.0, 0.0, 40.0][:F] if F == 3 else [0.0]
+    ks = kernels_for(n, 1.0, foci, k=K, grid_n=21)
+    target = (rng.random((n, n)) > 0.5).astype(np.float64)
+    theta0 = rng.standard_normal((n, n)) * 0.5
+    prm = L.IltParams(mask_steepness=4.0, resist_beta=30.0, threshold=0.25, resist_sigma_nm=2.0,
+                      dose=1.0, step=0.05, focus_weights=[1.0 / F] * F)
+    solver = L.IltSolver(ks, prm, 1, "f32", ctx)
+    solver.set_tiles(target[None], theta0[None])
+    costs = [solver.run(2)[:, 0] for _ in range(3)]  # eager, capture, replay
+    theta_gpu, _ = solver.get_tiles()
+    th = theta0.copy()
+    c_ref = []
+    for _ in range(6):
+        c, _ = O.ilt_iteration(th, target, ks.weights, ks.support, ks.values, [1.0 / F] * F,
+                               [4.0, 30.0, 0.25, 2.0, 1.0, 0.05], 1.0)
+        c_ref.append(c)
+    got = np.concatenate(costs)
+    assert np.abs(got - np.array(c_ref)).max() <= 1e-4 * np.abs(c_ref).max()
+    assert rel_linf(theta_gpu[0] - theta0, th - theta0) < 1e-3
+
+
+def test_ilt_stored_fields_bit_identical(ctx, monkeypatch):
+    """keeping E_fk for the adjoint (LITHOGPU_STORE_E=1) and recomputing it
+    (=0) run the same arithmetic: results must be bitwise equal."""
+    rng = np.random.default_rng(23)
+    n = 512
+    ks = kernels_for(n, 1.0, (0.0,), k=16, grid_n=21)
+    target = (rng.random((n, n)) > 0.5).astype(np.float64)
+    prm = L.IltParams(step=0.05, focus_weights=[1.0])
+    out = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("LITHOGPU_STORE_E", flag)
+        dk = L.DeviceKernels(ks, "f32", ctx)
+        solver = L.IltSolver(dk, prm, 1, "f32", ctx)
+        solver.set_tiles(target[None])
+        cost = solver.run(3)
+        out.append((cost.copy(), solver.get_tiles()[0].copy()))
+        solver.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1], out[1][1])
