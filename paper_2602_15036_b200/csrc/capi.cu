@@ -435,7 +435,7 @@ struct Plan : PlanBase {
   // fp32 fast path (power-of-two tiles, register FFT kernels of socs_fast.cuh)
   bool fast = false;
   lg::FGeo fg{};
-  DevBuf ftNx, ftNy, ftnx, ftny, Wsub, Ih, Rh, Wh, Ip, Eb;
+  DevBuf ftNx, ftNy, ftnx, ftny, Wsub, Ih, Rh, Wh, Ip, Eb, Ht;
   long long s_Wsub = 0, s_band = 0, s_Ip = 0, s_E = 0;
   // ILT: keep the coherent fields E_fk from the forward rows for the adjoint
   // rows (saves one n-point IFFT per (row, kernel)) while they stay
@@ -524,6 +524,18 @@ struct Plan : PlanBase {
           LG_CUDA(cudaMemcpy(b.p, h.data(), h.size() * sizeof(lg::C32), cudaMemcpyHostToDevice));
           return b.as<lg::C32>();
         };
+        // column-major copy of the kernel band for the fast column kernels
+        {
+          std::vector<lg::C32> ht(h.size());
+          for (int fk = 0; fk < F * K; ++fk)
+            for (int jy = 0; jy < By; ++jy)
+              for (int jx = 0; jx < Bx; ++jx) {
+                const C& src = h[(size_t(fk) * By + jy) * Bx + jx];
+                ht[(size_t(fk) * Bx + jx) * By + jy] = lg::C32{float(src.x), float(src.y)};
+              }
+          Ht.ensure(ht.size() * sizeof(lg::C32));
+          LG_CUDA(cudaMemcpy(Ht.p, ht.data(), ht.size() * sizeof(lg::C32), cudaMemcpyHostToDevice));
+        }
         fg.twNx = table(Nx, ftNx);
         fg.twNy = table(Ny, ftNy);
         fg.twnx = table(ax.n, ftnx);
@@ -761,7 +773,7 @@ struct Plan : PlanBase {
         lg::fast_set_pdl(true);
         fl("real_rows_fwd", [&] { lg::fl_real_rows_fwd(fg, s, tiles, 0, mask, m_ts, 0.f, g.ax.Pm, Mr.as<C>(), s_Mr); });
         fl("mask_cols", [&] { lg::fl_mask_cols(fg, s, tiles, Mr.as<C>(), s_Mr, Mhat.as<C>(), s_Mhat); });
-        fl("socs_cols", [&] { lg::fl_socs_cols(fg, s, tiles, Mhat.as<C>(), s_Mhat, H.as<C>(), Tb.as<C>(), s_T); });
+        fl("socs_cols", [&] { lg::fl_socs_cols(fg, s, tiles, Mhat.as<C>(), s_Mhat, Ht.as<C>(), Tb.as<C>(), s_T); });
         fl("socs_rows", [&] {
           lg::fl_socs_rows(fg, s, tiles, Tb.as<C>(), s_T, wk.as<T>(), dose, Ip.as<T>(), s_Ip, nullptr, 0);
         });
@@ -785,7 +797,7 @@ struct Plan : PlanBase {
         cudaStream_t s = ctx->stream;
         fl("real_rows_fwd", [&] { lg::fl_real_rows_fwd(fg, s, 1, 0, mask, 0, 0.f, g.ax.Pm, Mr.as<C>(), s_Mr); });
         fl("mask_cols", [&] { lg::fl_mask_cols(fg, s, 1, Mr.as<C>(), s_Mr, Mhat.as<C>(), s_Mhat); });
-        fl("socs_cols", [&] { lg::fl_socs_cols(fg, s, 1, Mhat.as<C>(), s_Mhat, H.as<C>(), Tb.as<C>(), s_T); });
+        fl("socs_cols", [&] { lg::fl_socs_cols(fg, s, 1, Mhat.as<C>(), s_Mhat, Ht.as<C>(), Tb.as<C>(), s_T); });
         if (W) {
           fl("real_rows_fwd", [&] { lg::fl_real_rows_fwd(fg, s, 1, 0, W, 0, 0.f, g.ax.P, Dr.as<C>(), s_Dr); });
           wlp_cols_fast(1, 1, false);
@@ -795,7 +807,7 @@ struct Plan : PlanBase {
           lg::fl_adj_rows(fg, s, 1, 1, W == nullptr, false, Tb.as<C>(), s_T, Wsub.as<T>(), s_Wsub, U.as<C>(),
                           s_U);
         });
-        fl("adj_cols", [&] { lg::fl_adj_cols(fg, s, 1, U.as<C>(), s_U, H.as<C>(), wk.as<T>(), dose, Acc.as<C>(), s_Acc); });
+        fl("adj_cols", [&] { lg::fl_adj_cols(fg, s, 1, U.as<C>(), s_U, Ht.as<C>(), wk.as<T>(), dose, Acc.as<C>(), s_Acc); });
         fl("grad_cols", [&] {
           lg::fl_grad_cols(fg, s, 1, Acc.as<C>(), s_Acc, fg.F * fg.K, Gc.as<C>(), s_Gc, nullptr, 0, 0, nullptr, 0);
         });
@@ -902,7 +914,7 @@ static void ilt_run_impl(lithogpu_ilt* ilt, int iters, double* cost_user, double
         P.fl("real_rows_fwd", [&] { lg::fl_real_rows_fwd(fg, s, tiles, 1, theta, NN, a, P.g.ax.Pm, P.Mr.template as<C>(), P.s_Mr); });
       for (int it = 0; it < iters; ++it) {
         P.fl("mask_cols", [&] { lg::fl_mask_cols(fg, s, tiles, P.Mr.template as<C>(), P.s_Mr, P.Mhat.template as<C>(), P.s_Mhat); });
-        P.fl("socs_cols", [&] { lg::fl_socs_cols(fg, s, tiles, P.Mhat.template as<C>(), P.s_Mhat, P.H.template as<C>(), P.Tb.template as<C>(), P.s_T); });
+        P.fl("socs_cols", [&] { lg::fl_socs_cols(fg, s, tiles, P.Mhat.template as<C>(), P.s_Mhat, P.Ht.template as<C>(), P.Tb.template as<C>(), P.s_T); });
         C* Ef = P.store_E ? P.Eb.template as<C>() : nullptr;
         P.fl("socs_rows", [&] {
           lg::fl_socs_rows(fg, s, tiles, P.Tb.template as<C>(), P.s_T, P.wk.template as<T>(), dose, P.Ip.template as<T>(),
@@ -921,7 +933,7 @@ static void ilt_run_impl(lithogpu_ilt* ilt, int iters, double* cost_user, double
                           P.Wsub.template as<T>(), P.s_Wsub, P.U.template as<C>(), P.s_U);
         });
         P.fl("adj_cols", [&] {
-          lg::fl_adj_cols(fg, s, tiles, P.U.template as<C>(), P.s_U, P.H.template as<C>(), P.wk.template as<T>(), dose,
+          lg::fl_adj_cols(fg, s, tiles, P.U.template as<C>(), P.s_U, P.Ht.template as<C>(), P.wk.template as<T>(), dose,
                           P.Acc.template as<C>(), P.s_Acc);
         });
         const long long npairs = (P.g.ay.N + 1) / 2;
@@ -1397,6 +1409,13 @@ lithogpu_status lithogpu_intensity_gradient(lithogpu_kernels* ks, int focus, con
       wf.ensure(sizeof(T) * P.K);
       LG_CUDA(cudaMemcpyAsync(Hf.p, P.H.template as<char>() + hsz * focus, hsz, cudaMemcpyDeviceToDevice, ctx->stream));
       LG_CUDA(cudaMemcpyAsync(wf.p, P.wk.template as<T>() + size_t(P.K) * focus, sizeof(T) * P.K, cudaMemcpyDeviceToDevice, ctx->stream));
+      DevBuf& Htf = ctx->slot(11);
+      if (P.fast) {  // column-major fast-path copy of the same stack
+        Htf.ensure(hsz);
+        LG_CUDA(cudaMemcpyAsync(Htf.p, P.Ht.template as<char>() + hsz * focus, hsz, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+        std::swap(P.Ht.p, Htf.p);
+      }
       std::swap(P.H.p, Hf.p);
       std::swap(P.wk.p, wf.p);
       const int fgF0 = P.fg.F;
@@ -1406,6 +1425,7 @@ lithogpu_status lithogpu_intensity_gradient(lithogpu_kernels* ks, int focus, con
       try {
         P.gradient(m, w, T(dose), og.work);
       } catch (...) {
+        if (P.fast) std::swap(P.Ht.p, Htf.p);
         std::swap(P.H.p, Hf.p);
         std::swap(P.wk.p, wf.p);
         P.F = F0;
@@ -1413,6 +1433,7 @@ lithogpu_status lithogpu_intensity_gradient(lithogpu_kernels* ks, int focus, con
         P.fg.F = fgF0;
         throw;
       }
+      if (P.fast) std::swap(P.Ht.p, Htf.p);
       std::swap(P.H.p, Hf.p);
       std::swap(P.wk.p, wf.p);
       P.F = F0;

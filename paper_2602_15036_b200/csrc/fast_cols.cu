@@ -64,7 +64,8 @@ void fl_grad_cols(const FGeo& g, cudaStream_t s, int tiles, const C32* Acc, long
     constexpr int L = decltype(c)::value;
     const int gr = 1;  // one column per CTA: Pm+1 is small, spread it over SMs
     with_len(g.ay.n, [&](auto cn) { nsum /= kgroups<decltype(cn)::value>(g.K); });  // fk_adj_cols partials
-    flaunch<L>(fk_grad_cols<L>, dim3(cdivi(g.ax.Pm + 1, gr) + 1, 1, tiles), gr, s, g, Acc, a_ts, nsum, Gc,
+    const size_t extra = size_t(gr) * 2 * g.ay.B * sizeof(C32);  // summed band columns
+    flaunch_x<L>(fk_grad_cols<L>, dim3(cdivi(g.ax.Pm + 1, gr) + 1, 1, tiles), gr, extra, s, g, Acc, a_ts, nsum, Gc,
                 g_ts, costp, cp_ts, ncost, cost_out, co_ts);
   });
 }

@@ -532,8 +532,8 @@ __global__ void __launch_bounds__(256) fk_mask_cols(FGeo g, const C32* __restric
   fftr<float, L, -1>(v, G.sm, g.twNy, G.t, G.sync);
   if (!act) return;
   const float inv = 1.0f / (float(g.ax.N) * float(L));
-  C32* mh = Mhat + blockIdx.z * mh_ts;
-  const int Bx = g.ax.B;
+  C32* mh = Mhat + blockIdx.z * mh_ts;  // column-major band [cx][jy]
+  const int By = g.ay.B;
   const int sp = band_slot(g.ax, px);
   const int sn = px > 0 ? band_slot(g.ax, -px) : -1;
 #pragma unroll
@@ -541,11 +541,11 @@ __global__ void __launch_bounds__(256) fk_mask_cols(FGeo g, const C32* __restric
     const int i = G.idx(e);
     if (sp >= 0) {
       const int jy = kslot(i, g.ay.lo, g.ay.hi, L);
-      if (jy >= 0) mh[size_t(jy) * Bx + sp] = scale(v[e], inv);
+      if (jy >= 0) mh[size_t(sp) * By + jy] = scale(v[e], inv);
     }
     if (sn >= 0 && sn != sp) {
       const int jy = kslot((i == 0 ? 0 : L - i), g.ay.lo, g.ay.hi, L);
-      if (jy >= 0) mh[size_t(jy) * Bx + sn] = scale(conjg(v[e]), inv);
+      if (jy >= 0) mh[size_t(sn) * By + jy] = scale(conjg(v[e]), inv);
     }
   }
 }
@@ -567,13 +567,14 @@ __global__ void __launch_bounds__(512) fk_socs_cols(FGeo g, const C32* __restric
   const int cx0 = c0 + G.gid;
   const bool act = cx0 < Bx;
   const int cx_ = act ? cx0 : Bx - 1;
-  const C32* mh = Mhat + blockIdx.z * mh_ts;
-  const C32* h = H + size_t(fk) * By * Bx;
+  // M^ and H are column-major [cx][jy]: each group reads contiguous columns
+  const C32* mh = Mhat + blockIdx.z * mh_ts + size_t(cx_) * By;
+  const C32* h = H + (size_t(fk) * Bx + cx_) * By;
   C32 v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int jy = kslot(G.idx(e), g.ay.lo, g.ay.hi, L);
-    v[e] = jy >= 0 ? mul(mh[size_t(jy) * Bx + cx_], ldg_cx(h + size_t(jy) * Bx + cx_)) : mk(0.f, 0.f);
+    v[e] = jy >= 0 ? mul(mh[jy], ldg_cx(h + jy)) : mk(0.f, 0.f);
   }
   fftr<float, L, +1>(v, G.sm, g.twny, G.t, G.sync);
   extern __shared__ __align__(16) unsigned char fsm_raw[];
@@ -759,12 +760,12 @@ __global__ void __launch_bounds__(256) fk_adj_cols(FGeo g, const C32* __restrict
   for (int e = 0; e < E; ++e) v[e] = src[G.idx(e)];
   fftr<float, L, -1>(v, G.sm, g.twny, G.t, G.sync);
   const float w = wk[fk] * dose * sc;
-  const C32* h = H + size_t(fk) * By * Bx;
+  const C32* h = H + (size_t(fk) * Bx + cx) * By;  // column-major [fk][cx][jy]
   G.sync();
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int jy = kslot(G.idx(e), g.ay.lo, g.ay.hi, L);
-    if (jy >= 0) G.sm[jy] = scale(mulc(v[e], ldg_cx(h + size_t(jy) * Bx + cx)), w);
+    if (jy >= 0) G.sm[jy] = scale(mulc(v[e], ldg_cx(h + jy)), w);
   }
   __syncthreads();
   extern __shared__ __align__(16) unsigned char fsm_raw[];
@@ -808,12 +809,24 @@ __global__ void __launch_bounds__(256) fk_grad_cols(FGeo g, const C32* __restric
   const int px0 = blockIdx.x * G.groups + G.gid;
   const bool act = px0 <= Pm;
   const int px = act ? px0 : Pm;
-  // Acc holds nsum per-(f,k) partials [fk][cx][qy]; they are summed here in
-  // fixed order (deterministic, same bits as a separate reduction pass)
+  // Acc holds nsum partials [.][cx][qy] (fk_adj_cols kernel groups): the
+  // group first sums band columns sp and -px (sn) in fixed order into shared
+  // memory with all its threads (short code, loads in flight together), then
+  // gathers the Hermitian column from there
   const C32* a = Acc + blockIdx.z * a_ts;
   const int sp = band_slot(g.ax, px), sn = band_slot(g.ax, -px);
   const int By = g.ay.B;
   const size_t plane = size_t(Bx) * By;
+  extern __shared__ __align__(16) unsigned char fsm_raw[];
+  C32* col = reinterpret_cast<C32*>(fsm_raw) + G.groups * rsm_len<L>() + G.gid * 2 * By;
+  for (int idx = G.t; idx < 2 * By; idx += G.TPR) {
+    const int which = idx >= By, jy = idx - which * By, slot = which ? sn : sp;
+    C32 q = mk(0.f, 0.f);
+    if (slot >= 0)
+      for (int k = 0; k < nsum; ++k) q = add(q, ldg_cx(a + k * plane + size_t(slot) * By + jy));
+    col[idx] = q;
+  }
+  G.sync();
   C32 v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) {
@@ -821,16 +834,8 @@ __global__ void __launch_bounds__(256) fk_grad_cols(FGeo g, const C32* __restric
     const int jp = kslot(i, g.ay.lo, g.ay.hi, L);
     const int jn = kslot((i == 0 ? 0 : L - i), g.ay.lo, g.ay.hi, L);
     C32 s = mk(0.f, 0.f);
-    if (sp >= 0 && jp >= 0) {
-      C32 q = mk(0.f, 0.f);
-      for (int k = 0; k < nsum; ++k) q = add(q, ldg_cx(a + k * plane + size_t(sp) * By + jp));
-      s = add(s, q);
-    }
-    if (sn >= 0 && jn >= 0) {
-      C32 q = mk(0.f, 0.f);
-      for (int k = 0; k < nsum; ++k) q = add(q, ldg_cx(a + k * plane + size_t(sn) * By + jn));
-      s = add(s, conjg(q));
-    }
+    if (sp >= 0 && jp >= 0) s = add(s, col[jp]);
+    if (sn >= 0 && jn >= 0) s = add(s, conjg(col[By + jn]));
     v[e] = scale(s, 0.5f);
   }
   fftr<float, L, +1>(v, G.sm, g.twNy, G.t, G.sync);
