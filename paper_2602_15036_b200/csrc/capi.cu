@@ -554,6 +554,13 @@ struct Plan : PlanBase {
 
   template <typename Fn>
   void fl(const char* name, Fn&& fn) {
+    // LITHOGPU_ABLATE=name[,name..]: skip those launches (timing ablation
+    // only, tools/ablate.py; results are then meaningless)
+    static const char* ablate = std::getenv("LITHOGPU_ABLATE");
+    if (ablate) {
+      const std::string list = std::string(",") + ablate + ",";
+      if (list.find(std::string(",") + name + ",") != std::string::npos) return;
+    }
     ctx->prof_begin(name);
     fn();
     ctx->prof_end();

@@ -795,12 +795,23 @@ __global__ void __launch_bounds__(256) fk_grad_cols(FGeo g, const C32* __restric
     if (cost_out) {  // fixed-order (deterministic) parallel sum of the cost partials
       __shared__ double red[512];
       const double* c = costp + blockIdx.z * cp_ts;
+      const int bd = blockDim.x;
       double s = 0;
-      for (int i = threadIdx.x; i < ncost; i += blockDim.x) s += c[i];
+      int i = threadIdx.x;
+      for (; i + 7 * bd < ncost; i += 8 * bd) {  // 8 loads in flight, summed in index order
+        double x[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = c[i + j * bd];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s += x[j];
+      }
+      for (; i < ncost; i += bd) s += c[i];
       red[threadIdx.x] = s;
       __syncthreads();
-      if (threadIdx.x == 0)
-        for (int i = 1; i < int(blockDim.x); ++i) red[0] += red[i];
+      for (int h = bd / 2; h > 0; h >>= 1) {  // fixed pairwise tree (bd is a power of two)
+        if (int(threadIdx.x) < h) red[threadIdx.x] += red[threadIdx.x + h];
+        __syncthreads();
+      }
       if (threadIdx.x == 0) cost_out[blockIdx.z * co_ts] = red[0];
     }
     return;
@@ -822,8 +833,10 @@ __global__ void __launch_bounds__(256) fk_grad_cols(FGeo g, const C32* __restric
   for (int idx = G.t; idx < 2 * By; idx += G.TPR) {
     const int which = idx >= By, jy = idx - which * By, slot = which ? sn : sp;
     C32 q = mk(0.f, 0.f);
-    if (slot >= 0)
+    if (slot >= 0) {
+#pragma unroll 4
       for (int k = 0; k < nsum; ++k) q = add(q, ldg_cx(a + k * plane + size_t(slot) * By + jy));
+    }
     col[idx] = q;
   }
   G.sync();
