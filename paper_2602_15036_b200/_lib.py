@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblithogpu.so")
+# LITHOGPU_LIB: alternative build of the same library (A/B timing variants, tools/)
+LIB_PATH = os.environ.get("LITHOGPU_LIB") or os.path.join(_HERE, "liblithogpu.so")
 
 OK, ERR_DOMAIN, ERR_USAGE = 0, 1, 2
 F32, F64, U8 = 0, 1, 2

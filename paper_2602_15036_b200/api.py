@@ -493,10 +493,12 @@ class IltSolver:
                                      gmax.ctypes.data if with_gmax else None))
         return (cost, gmax) if with_gmax else cost
 
-    def run_device(self, iterations: int, cost_dev=None):
-        """Enqueue without host sync of results (cost_dev: device f64 [iters, tiles] or None)."""
+    def run_device(self, iterations: int, cost_dev=None, gmax_dev=None):
+        """Enqueue without host sync of results (cost_dev / gmax_dev: device
+        f64 [iters, tiles] or None; gmax = max |dL/dtheta| per tile)."""
         ptr = cost_dev.data_ptr() if cost_dev is not None else None
-        check(lib().lithogpu_ilt_run(self._h, iterations, ptr, None))
+        gptr = gmax_dev.data_ptr() if gmax_dev is not None else None
+        check(lib().lithogpu_ilt_run(self._h, iterations, ptr, gptr))
 
     def get_tiles(self, like=None, dtype=F64):
         shape = (self.n_tiles, self.grid.ny, self.grid.nx)

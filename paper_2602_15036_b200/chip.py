@@ -1,7 +1,8 @@
 """Chip-scale ILT over halo-padded tiles, sharded across ranks (one process
 per GPU).  SURVEY.md §8e: tiles are independent (cyclic convolution inside
 each halo-padded window), so the only data-path exchange is the all-reduce of
-the global ILT cost and convergence scalars once per iteration.
+the global ILT cost and convergence scalars (per iteration, batched into one
+call per graph-replayed segment of iterations).
 
 Torch is plumbing here: torch.distributed (NCCL on GPUs, gloo in CPU tests)
 for the scalar all-reduce; all imaging / adjoint work runs in liblithogpu.so.
@@ -68,20 +69,49 @@ class ChipIlt:
         self.target32 = self.target.float().contiguous()
         self.solver.set_tiles(self.target32)
 
-    def run(self, iters: int, want_mask: bool = False) -> ChipResult:
-        import torch
-        dev = self.target.device
-        cost = torch.zeros((iters, self.solver.n_tiles), dtype=torch.float64, device=dev)
-        gl_cost = torch.zeros(iters, dtype=torch.float64, device=dev)
-        for it in range(iters):
-            self.solver.run_device(1, cost[it])
-            gl_cost[it] = cost[it].sum()
-            allreduce_scalars(gl_cost[it:it + 1], None)
-        res = ChipResult(gl_cost.cpu().numpy(), np.zeros(iters), self.mine)
+    def run(self, iters: int, want_mask: bool = False, sync_every: Optional[int] = None,
+            tol: Optional[float] = None) -> ChipResult:
+        """`iters` ILT iterations of this rank's tiles (see segmented_ilt)."""
+        gl_cost, gl_gmax = segmented_ilt(self.solver.run_device, iters, self.solver.n_tiles, sync_every, tol,
+                                         self.target.device)
+        res = ChipResult(gl_cost, gl_gmax, self.mine)
         if want_mask:
             _, m = self.solver.get_tiles()
             res.mask = m
         return res
+
+
+def segmented_ilt(run_segment, iters: int, n_tiles: int, sync_every: Optional[int] = None,
+                  tol: Optional[float] = None, device="cpu"):
+    """Drive `iters` ILT iterations as graph-replayed segments of `sync_every`
+    (default: all of them).  run_segment(k, cost[k, n_tiles], gmax[k, n_tiles])
+    enqueues k iterations of this rank's tiles.  After each segment the
+    per-iteration global cost (sum over tiles and ranks) and max |dL/dtheta|
+    (max over tiles and ranks) of the whole segment are all-reduced in one
+    call each: no blocking collective per iteration on the critical path.
+    With `tol`, stop after the first segment whose last global relative cost
+    change is <= tol.  Returns (global cost [done], global gmax [done])."""
+    import torch
+    seg = max(1, min(iters, sync_every or iters))
+    cost = torch.zeros((iters, n_tiles), dtype=torch.float64, device=device)
+    gmax = torch.zeros((iters, n_tiles), dtype=torch.float64, device=device)
+    gl_cost = torch.zeros(iters, dtype=torch.float64, device=device)
+    gl_gmax = torch.zeros(iters, dtype=torch.float64, device=device)
+    done = 0
+    while done < iters:
+        k = min(seg, iters - done)
+        run_segment(k, cost[done:done + k], gmax[done:done + k])
+        gl_cost[done:done + k] = cost[done:done + k].sum(dim=1)
+        gl_gmax[done:done + k] = gmax[done:done + k].amax(dim=1)
+        c, g = allreduce_scalars(gl_cost[done:done + k].clone(), gl_gmax[done:done + k].clone())
+        gl_cost[done:done + k] = c
+        gl_gmax[done:done + k] = g
+        done += k
+        if tol is not None and done >= 2:
+            c2 = gl_cost[done - 2:done].cpu().numpy()
+            if abs(c2[1] - c2[0]) <= tol * abs(c2[0]):
+                break
+    return gl_cost[:done].cpu().numpy(), gl_gmax[:done].cpu().numpy()
 
 
 def _raster(ctx, grid, xy, starts, out_dev, dbu):

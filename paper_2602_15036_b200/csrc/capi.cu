@@ -915,7 +915,11 @@ static void ilt_run_impl(lithogpu_ilt* ilt, int iters, double* cost_user, double
     if (P.fast) {
       cudaStream_t s = ctx->stream;
       const lg::FGeo& fg = P.fg;
-      lg::fast_set_pdl(false);  // PDL slows the graph-replayed ILT loop
+      static const bool ilt_pdl = [] {
+        const char* e = std::getenv("LITHOGPU_ILT_PDL");
+        return e && e[0] == '1';
+      }();
+      lg::fast_set_pdl(ilt_pdl);
       const int F = P.F;
       if (need_prime)
         P.fl("real_rows_fwd", [&] { lg::fl_real_rows_fwd(fg, s, tiles, 1, theta, NN, a, P.g.ax.Pm, P.Mr.template as<C>(), P.s_Mr); });

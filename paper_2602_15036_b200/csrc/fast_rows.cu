@@ -35,10 +35,11 @@ void fl_real_rows_fwd(const FGeo& g, cudaStream_t s, int tiles, int mode, const 
     constexpr int L = decltype(c)::value;
     const int gr = fgroups<L>(256);
     const dim3 grid(cdivi((g.ay.N + 1) / 2, gr), 1, tiles);
+    const size_t extra = size_t(Pout + 1) * 2 * gr * sizeof(C32) + 16;  // transposed-store tile
     if (mode == 0)
-      flaunch<L>(fk_real_rows_fwd<L, 0>, grid, gr, s, g, src, src_ts, steep, Pout, out, out_ts);
+      flaunch_x<L>(fk_real_rows_fwd<L, 0>, grid, gr, extra, s, g, src, src_ts, steep, Pout, out, out_ts);
     else
-      flaunch<L>(fk_real_rows_fwd<L, 1>, grid, gr, s, g, src, src_ts, steep, Pout, out, out_ts);
+      flaunch_x<L>(fk_real_rows_fwd<L, 1>, grid, gr, extra, s, g, src, src_ts, steep, Pout, out, out_ts);
   });
 }
 
@@ -57,7 +58,8 @@ void fl_isub_rows(const FGeo& g, cudaStream_t s, int tiles, const float* Ip, lon
   with_len(g.ax.n, [&](auto c) {
     constexpr int L = decltype(c)::value;
     const int gr = spread_groups<L>((long long)tiles * g.F * ((g.ay.n + 1) / 2));
-    flaunch<L>(fk_isub_rows<L>, dim3(cdivi((g.ay.n + 1) / 2, gr), g.F, tiles), gr, s, g, Ip, ip_ts,
+    const size_t extra = size_t(g.ax.P + 1) * 2 * gr * sizeof(C32) + 16;
+    flaunch_x<L>(fk_isub_rows<L>, dim3(cdivi((g.ay.n + 1) / 2, gr), g.F, tiles), gr, extra, s, g, Ip, ip_ts,
                nsum / kgroups<L>(g.K), Ir, ir_ts);
   });
 }
@@ -68,7 +70,7 @@ void fl_resist_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* Rc, lon
   with_len(g.ax.N, [&](auto c) {
     constexpr int L = decltype(c)::value;
     const int gr = fgroups<L>(256);
-    flaunch<L>(fk_resist_rows<L>, dim3(cdivi((g.ay.N + 1) / 2, gr), g.F, tiles), gr, s, g, Rc,
+    flaunch_x<L>(fk_resist_rows<L>, dim3(cdivi((g.ay.N + 1) / 2, gr), g.F, tiles), gr, row_slab_bytes<L>(gr) + size_t(g.ax.P + 1) * 2 * gr * sizeof(C32) + 16, s, g, Rc,
                 c_ts, target, tg_ts, cf, beta, thr, Dr, d_ts, costp, cp_ts);
   });
 }
@@ -116,8 +118,9 @@ void fl_grad_rows(const FGeo& g, cudaStream_t s, int tiles, bool ilt, const C32*
     constexpr int L = decltype(c)::value;
     const int gr = fgroups<L>(256);
     const dim3 grid(cdivi((g.ay.N + 1) / 2, gr), 1, tiles);
+    const size_t extra = row_slab_bytes<L>(gr) + size_t(g.ax.Pm + 1) * 2 * gr * sizeof(C32) + 16;
     if (ilt)
-      flaunch<L>(fk_grad_rows<L, true>, grid, gr, s, g, Gc, g_ts, grad, gr_ts, theta, th_ts, steep,
+      flaunch_x<L>(fk_grad_rows<L, true>, grid, gr, extra, s, g, Gc, g_ts, grad, gr_ts, theta, th_ts, steep,
                   step, Mr, mr_ts, gmaxp, gm_ts);
     else
       flaunch<L>(fk_grad_rows<L, false>, grid, gr, s, g, Gc, g_ts, grad, gr_ts, theta, th_ts,

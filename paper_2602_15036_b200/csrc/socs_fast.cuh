@@ -15,12 +15,16 @@
 
 namespace lg {
 
-// Programmatic dependent launch (sm_90+): let the next kernel in the stream /
-// graph get its CTAs resident as soon as every CTA of this one has started,
-// and wait for the predecessor's completion before touching its outputs.
-// Both are no-ops when the launch did not opt in.
+// Programmatic dependent launch (sm_90+): wait for the predecessor's
+// completion (and memory flush) before touching its outputs.  No explicit
+// launch_dependents: the implicit trigger at CTA exit lets the next grid's
+// CTAs take the slots the draining tail frees, without stealing slots from
+// this grid's later waves (an early trigger measured slower).
+// No-op when the launch did not opt in.
 __device__ __forceinline__ void pdl_entry() {
+#ifdef LG_PDL_EARLY_TRIGGER
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
@@ -85,6 +89,68 @@ __device__ __forceinline__ void load_herm_pair(C32 (&v)[RPlan<L>::E], const FGro
   }
 }
 
+// Two real rows (L floats each) staged into the group's shared-memory slab
+// [2][L] with cp.async (16-byte chunks, L2-only) at kernel entry, so the
+// transform runs without holding them in registers.  Reader: stage_wait()
+// then a group barrier.
+template <int L>
+__host__ __device__ constexpr size_t groups_bytes(int groups) {
+  return (size_t(groups) * rsm_len<L>() * sizeof(C32) + 15) & ~size_t(15);
+}
+template <int L>
+__device__ __forceinline__ float* row_slab(int groups, int gid) {
+  extern __shared__ __align__(16) unsigned char fsm_raw[];
+  return reinterpret_cast<float*>(fsm_raw + groups_bytes<L>(groups)) + size_t(gid) * 2 * L;
+}
+template <int L>
+__device__ __forceinline__ void stage_rows_async(float* dst, const float* r0, const float* r1, int t) {
+  constexpr int CH = L / 4, TPR = RPlan<L>::TPR;
+#pragma unroll
+  for (int c = t; c < 2 * CH; c += TPR) {
+    const float* src = c < CH ? r0 + 4 * c : r1 + 4 * (c - CH);
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst + 4 * c));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src) : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void stage_wait() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+template <int L>
+__host__ __device__ constexpr size_t row_slab_bytes(int groups) {
+  return size_t(groups) * 2 * L * sizeof(float);
+}
+
+// Transposed store of a CTA's row pairs into a column-major half spectrum
+// o[px][y] (px in [0, Pout]): the group's row pair sits in its exchange buffer
+// (to_smem, synced); it is split into the two real rows' spectra, staged as
+// tile[px][R] (R = 2 * groups rows of the CTA) and written as contiguous runs
+// of R rows per column instead of 8-byte scattered stores.  CTA-wide barrier
+// inside: every thread of the CTA must call it.  tile_off: byte offset of the
+// tile past the row-group buffers.
+template <int L>
+__device__ __forceinline__ void store_pair_cols(const FGroup<L>& G, size_t tile_off, C32* o, int ld,
+                                                int ybase, int nrows, int Pout) {
+  extern __shared__ __align__(16) unsigned char fsm_raw[];
+  C32* tile = reinterpret_cast<C32*>(fsm_raw + tile_off);
+  const int R = 2 * G.groups;
+  for (int px = G.t; px <= Pout; px += G.TPR) {
+    C32 A, Bv;
+    split_pair(G.sm[rpad(px)], G.sm[rpad(px == 0 ? 0 : L - px)], A, Bv);
+    tile[px * R + 2 * G.gid] = A;
+    tile[px * R + 2 * G.gid + 1] = Bv;
+  }
+  __syncthreads();
+  const int rows = min(R, nrows - ybase);
+  for (int idx = threadIdx.x; idx < (Pout + 1) * R; idx += blockDim.x) {
+    const int px = idx / R, r = idx - px * R;
+    if (r < rows) o[size_t(px) * ld + ybase + r] = tile[idx];
+  }
+}
+
+// min resident CTAs for the full-resolution row kernels (3 measured slower: tail)
+#ifndef LG_FULLROW_MINB
+#define LG_FULLROW_MINB 2
+#endif
+
 // warp-partial (deterministic) reduction: lane 0 of each warp-slice writes
 __device__ __forceinline__ float warp_sum(float v, int width) {
   for (int o = width / 2; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o, width);
@@ -127,14 +193,8 @@ __global__ void __launch_bounds__(256) fk_real_rows_fwd(FGeo g, const float* __r
   G.sync();
   to_smem<float, L>(v, G.sm, G.t);
   G.sync();
-  if (!act) return;
-  C32* o = out + blockIdx.z * out_ts;
-  for (int px = G.t; px <= Pout; px += G.TPR) {
-    C32 A, Bv;
-    split_pair(G.sm[rpad(px)], G.sm[rpad((px == 0 ? 0 : L - px))], A, Bv);
-    o[size_t(px) * Ny + y0] = A;
-    if (has1) o[size_t(px) * Ny + y1] = Bv;
-  }
+  store_pair_cols<L>(G, groups_bytes<L>(G.groups), out + blockIdx.z * out_ts, Ny,
+                     2 * blockIdx.x * G.groups, Ny, Pout);
 }
 
 // ===========================================================================
@@ -227,14 +287,8 @@ __global__ void __launch_bounds__(256) fk_isub_rows(FGeo g, const float* __restr
   G.sync();
   to_smem<float, L>(v, G.sm, G.t);
   G.sync();
-  if (!act) return;
-  C32* o = Ir + blockIdx.z * ir_ts + size_t(f) * (g.ax.P + 1) * ny;
-  for (int px = G.t; px <= g.ax.P; px += G.TPR) {
-    C32 A, Bv;
-    split_pair(G.sm[rpad(px)], G.sm[rpad(px == 0 ? 0 : L - px)], A, Bv);
-    o[size_t(px) * ny + sy0] = A;
-    if (has1) o[size_t(px) * ny + sy0 + 1] = Bv;
-  }
+  store_pair_cols<L>(G, groups_bytes<L>(G.groups), Ir + blockIdx.z * ir_ts + size_t(f) * (g.ax.P + 1) * ny,
+                     ny, 2 * blockIdx.x * G.groups, ny, g.ax.P);
 }
 
 // ===========================================================================
@@ -243,7 +297,7 @@ __global__ void __launch_bounds__(256) fk_isub_rows(FGeo g, const float* __restr
 // FFT_Nx(D pair) -> Dr[f][px][y].  grid (ceil(Ny/2/groups), F, tiles)
 // ===========================================================================
 template <int L>
-__global__ void __launch_bounds__(256) fk_resist_rows(FGeo g, const C32* __restrict__ Rc,
+__global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_resist_rows(FGeo g, const C32* __restrict__ Rc,
                                                       long long c_ts, const float* __restrict__ target,
                                                       long long tg_ts, const float* __restrict__ cf,
                                                       float beta, float thr, C32* __restrict__ Dr,
@@ -259,28 +313,26 @@ __global__ void __launch_bounds__(256) fk_resist_rows(FGeo g, const C32* __restr
   const int y0 = 2 * pair, y1 = y0 + 1;
   const bool has1 = y1 < Ny;
   const C32* rc = Rc + blockIdx.z * c_ts + size_t(f) * Ny * (Px + 1);
-  // target rows prefetched before the transform (latency hidden behind it)
+  // target rows staged into shared memory behind the transform
   const float* tg = target + blockIdx.z * tg_ts;
-  float t0v[E], t1v[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    t0v[e] = __ldg(tg + size_t(y0) * L + G.idx(e));
-    t1v[e] = has1 ? __ldg(tg + size_t(y1) * L + G.idx(e)) : 0.f;
-  }
+  float* tsl = row_slab<L>(G.groups, G.gid);
+  stage_rows_async<L>(tsl, tg + size_t(y0) * L, tg + size_t(has1 ? y1 : y0) * L, G.t);
   C32 v[E];
   load_herm_pair<L>(v, G, rc + size_t(y0) * (Px + 1), has1 ? rc + size_t(y1) * (Px + 1) : nullptr, Px);
   fftr<float, L, +1>(v, G.sm, g.twNx, G.t, G.sync);
+  stage_wait();
+  G.sync();
   const float w = cf[f];
   float c = 0.f;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const float z0 = fsig(beta * (v[e].x - thr));
-    const float e0 = z0 - t0v[e];
+    const float e0 = z0 - tsl[G.idx(e)];
     float d1 = 0.f;
     c += e0 * e0;
     if (has1) {
       const float z1 = fsig(beta * (v[e].y - thr));
-      const float e1 = z1 - t1v[e];
+      const float e1 = z1 - tsl[L + G.idx(e)];
       c += e1 * e1;
       d1 = 2.f * w * e1 * beta * z1 * (1.f - z1);
     }
@@ -293,14 +345,8 @@ __global__ void __launch_bounds__(256) fk_resist_rows(FGeo g, const C32* __restr
   G.sync();
   to_smem<float, L>(v, G.sm, G.t);
   G.sync();
-  if (!act) return;
-  C32* d = Dr + blockIdx.z * d_ts + size_t(f) * (Px + 1) * Ny;
-  for (int px = G.t; px <= Px; px += TPR) {
-    C32 A, Bv;
-    split_pair(G.sm[rpad(px)], G.sm[rpad((px == 0 ? 0 : L - px))], A, Bv);
-    d[size_t(px) * Ny + y0] = A;
-    if (has1) d[size_t(px) * Ny + y1] = Bv;
-  }
+  store_pair_cols<L>(G, groups_bytes<L>(G.groups) + row_slab_bytes<L>(G.groups),
+                     Dr + blockIdx.z * d_ts + size_t(f) * (Px + 1) * Ny, Ny, 2 * blockIdx.x * G.groups, Ny, Px);
 }
 
 // ===========================================================================
@@ -434,7 +480,7 @@ __global__ void __launch_bounds__(256, 2) fk_adj_rows(FGeo g, const C32* __restr
 // grid (ceil(Ny/2/groups), 1, tiles)
 // ===========================================================================
 template <int L, bool ILT>
-__global__ void __launch_bounds__(256) fk_grad_rows(FGeo g, const C32* __restrict__ Gc,
+__global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_grad_rows(FGeo g, const C32* __restrict__ Gc,
                                                     long long g_ts, float* __restrict__ grad,
                                                     long long gr_ts, float* __restrict__ theta,
                                                     long long th_ts, float steep, float step,
@@ -451,17 +497,18 @@ __global__ void __launch_bounds__(256) fk_grad_rows(FGeo g, const C32* __restric
   const bool has1 = y1 < Ny;
   const C32* gc = Gc + blockIdx.z * g_ts;
   float* th = theta + blockIdx.z * th_ts;
-  float t0v[E], t1v[E];  // theta rows prefetched before the transform
+  float* tsl = nullptr;  // theta rows staged into shared memory behind the transform
   if (ILT) {
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      t0v[e] = th[size_t(y0) * L + G.idx(e)];
-      t1v[e] = has1 ? th[size_t(y1) * L + G.idx(e)] : 0.f;
-    }
+    tsl = row_slab<L>(G.groups, G.gid);
+    stage_rows_async<L>(tsl, th + size_t(y0) * L, th + size_t(has1 ? y1 : y0) * L, G.t);
   }
   C32 v[E];
   load_herm_pair<L>(v, G, gc + size_t(y0) * (Pm + 1), has1 ? gc + size_t(y1) * (Pm + 1) : nullptr, Pm);
   fftr<float, L, +1>(v, G.sm, g.twNx, G.t, G.sync);
+  if (ILT) {
+    stage_wait();
+    G.sync();
+  }
   if (!ILT) {
     if (!act) return;
     float* o = grad + blockIdx.z * gr_ts;
@@ -477,14 +524,14 @@ __global__ void __launch_bounds__(256) fk_grad_rows(FGeo g, const C32* __restric
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int i = G.idx(e);
-    const float t0 = t0v[e];
+    const float t0 = tsl[i];
     const float m0 = fsig(steep * t0);
     const float g0 = v[e].x * steep * m0 * (1.f - m0);
     const float n0 = t0 - step * g0;
     gm = fmaxf(gm, fabsf(g0));
     float n1v = 0.f;
     if (has1) {
-      const float t1 = t1v[e];
+      const float t1 = tsl[L + i];
       const float m1 = fsig(steep * t1);
       const float g1 = v[e].y * steep * m1 * (1.f - m1);
       const float n1 = t1 - step * g1;
@@ -501,14 +548,8 @@ __global__ void __launch_bounds__(256) fk_grad_rows(FGeo g, const C32* __restric
   G.sync();
   to_smem<float, L>(v, G.sm, G.t);
   G.sync();
-  if (!act) return;
-  C32* o = Mr + blockIdx.z * mr_ts;
-  for (int px = G.t; px <= Pm; px += TPR) {
-    C32 A, Bv;
-    split_pair(G.sm[rpad(px)], G.sm[rpad((px == 0 ? 0 : L - px))], A, Bv);
-    o[size_t(px) * Ny + y0] = A;
-    if (has1) o[size_t(px) * Ny + y1] = Bv;
-  }
+  store_pair_cols<L>(G, groups_bytes<L>(G.groups) + row_slab_bytes<L>(G.groups), Mr + blockIdx.z * mr_ts, Ny,
+                     2 * blockIdx.x * G.groups, Ny, Pm);
 }
 
 // ===========================================================================

@@ -164,3 +164,57 @@ def test_two_rank_cost_allreduce_gloo():
     want = float(sum(t * t for t in range(10)))
     assert res[0][2] == res[1][2] == want
     assert res[0][3] == res[1][3] == 9.0
+
+
+def _segment_worker(rank, world, port, q):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_15036_b200 import chip
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    mine = list(chip.shard(5, world, rank))
+    state = {"it": 0}
+
+    def run_segment(k, cost, gmax):  # fake solver: cost = (iter+1)*(tile+1), decreasing gmax
+        for j in range(k):
+            it = state["it"] + j
+            for a, t in enumerate(mine):
+                cost[j, a] = (it + 1) * (t + 1) if it < 3 else 4.0 * (t + 1)
+                gmax[j, a] = 1.0 / (it + 1) + t
+        state["it"] += k
+
+    c_all, g_all = chip.segmented_ilt(run_segment, 7, len(mine), sync_every=3)
+    state["it"] = 0
+    c_tol, _ = chip.segmented_ilt(run_segment, 7, len(mine), sync_every=2, tol=1e-12)
+    q.put((rank, c_all.tolist(), g_all.tolist(), len(c_tol)))
+    dist.destroy_process_group()
+
+
+def test_segmented_ilt_allreduce_gloo():
+    """per-iteration global cost / max|grad| of the sharded chip ILT, reduced
+    once per segment, with the tolerance stop (world_size 2, gloo)."""
+    import socket
+
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_segment_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    tiles_sum = sum(t + 1 for t in range(5))
+    want = [(it + 1) * tiles_sum if it < 3 else 4.0 * tiles_sum for it in range(7)]
+    assert res[0][1] == res[1][1] == want
+    assert res[0][2] == res[1][2] == [1.0 / (it + 1) + 4 for it in range(7)]
+    # segments of 2: costs 15, 30 | 45, 60 | 60, 60 -> stop after the third segment
+    assert res[0][3] == res[1][3] == 6

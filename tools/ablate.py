@@ -66,6 +66,9 @@ def main():
     iters = int(sys.argv[sys.argv.index("--iters") + 1]) if "--iters" in sys.argv else 50
     reps = int(sys.argv[sys.argv.index("--reps") + 1]) if "--reps" in sys.argv else 5
     base = run(None, iters, reps)
+    if "--base" in sys.argv:
+        print(json.dumps({"ms_per_iter": base}))
+        return
     out = {"ms_per_iter": base, "marginal_us": {}}
     for n in NAMES:
         out["marginal_us"][n] = round((base - run(n, iters, reps)) * 1e3, 2)
