@@ -56,6 +56,15 @@ lithogpu_status guarded(Fn&& fn) {
   }
 }
 
+// LITHOGPU_UNFUSED=1: the two-pass forms of the fused column kernels (A/B timing)
+bool unfused() {
+  static const bool v = [] {
+    const char* e = std::getenv("LITHOGPU_UNFUSED");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
 void require(bool ok, const char* msg) {
   if (!ok) throw UsageError(msg);
 }
@@ -552,6 +561,38 @@ struct Plan : PlanBase {
     }
   }
 
+  // ---- launch trace (LITHOGPU_TRACE=<path>, diagnostic) ----
+  DevBuf trace_buf;
+  std::vector<std::string> trace_names;
+  static constexpr int kTraceSlots = 64;
+  void trace_reset() {
+    trace_names.clear();
+    trace_buf.ensure(size_t(kTraceSlots) * lg::kTraceCtas * 2 * sizeof(unsigned long long));
+    LG_CUDA(cudaMemsetAsync(trace_buf.p, 0, size_t(kTraceSlots) * lg::kTraceCtas * 2 * sizeof(unsigned long long),
+                            ctx->stream));
+  }
+  void trace_dump(const char* path) {
+    std::vector<unsigned long long> h(size_t(kTraceSlots) * lg::kTraceCtas * 2);
+    LG_CUDA(cudaStreamSynchronize(ctx->stream));
+    LG_CUDA(cudaMemcpy(h.data(), trace_buf.p, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    FILE* f = std::fopen(path, "a");
+    if (!f) return;
+    for (size_t sl = 0; sl < trace_names.size(); ++sl) {
+      unsigned long long t0 = ~0ull, t1 = 0;
+      int n = 0;
+      for (int c = 0; c < lg::kTraceCtas; ++c) {
+        const unsigned long long a = h[(sl * lg::kTraceCtas + c) * 2], b = h[(sl * lg::kTraceCtas + c) * 2 + 1];
+        if (!a) continue;
+        ++n;
+        t0 = std::min(t0, a);
+        t1 = std::max(t1, b);
+      }
+      std::fprintf(f, "{\"slot\": %zu, \"name\": \"%s\", \"start_ns\": %llu, \"end_ns\": %llu, \"ctas\": %d}\n", sl,
+                   trace_names[sl].c_str(), t0, t1, n);
+    }
+    std::fclose(f);
+  }
+
   template <typename Fn>
   void fl(const char* name, Fn&& fn) {
     // LITHOGPU_ABLATE=name[,name..]: skip those launches (timing ablation
@@ -561,10 +602,18 @@ struct Plan : PlanBase {
       const std::string list = std::string(",") + ablate + ",";
       if (list.find(std::string(",") + name + ",") != std::string::npos) return;
     }
+    if (trace_buf.p && int(trace_names.size()) < kTraceSlots) {
+      fg.trace = static_cast<unsigned long long*>(trace_buf.p);
+      fg.trace_slot = int(trace_names.size());
+      trace_names.push_back(name);
+    } else {
+      fg.trace = nullptr;
+    }
     ctx->prof_begin(name);
     fn();
     ctx->prof_end();
     ctx->check_launch();
+    fg.trace = nullptr;
   }
 
   void set_sigma(double sigma_nm) {
@@ -740,7 +789,8 @@ struct Plan : PlanBase {
   void isub_cols_fast(int tiles, bool want_i, bool want_r) {
     cudaStream_t s = ctx->stream;
     bool fused = false;
-    fl("isub_cols", [&] {
+    if (!unfused())
+      fl("isub_cols", [&] {
       fused = lg::fl_band_col2(fg, s, tiles, F, true, Ir.as<C>(), s_Ir, gxh.as<T>(), gyb.as<T>(),
                                want_r ? Rc.as<C>() : nullptr, want_i ? Ic.as<C>() : nullptr, s_C);
     });
@@ -759,7 +809,8 @@ struct Plan : PlanBase {
     const float* gx = gauss ? gxh.as<T>() : nullptr;
     const float* gy = gauss ? gyb.as<T>() : nullptr;
     bool fused = false;
-    fl("wlp_cols", [&] {
+    if (!unfused())
+      fl("wlp_cols", [&] {
       fused = lg::fl_band_col2(fg, s, tiles, nf, false, Dr.as<C>(), s_Dr, gx, gy, Wc.as<C>(), nullptr, s_Wc);
     });
     if (fused) return;
@@ -876,6 +927,7 @@ struct lithogpu_ilt {
     GraphKey key;
     cudaGraphExec_t exec;
     long long nk;  // kernels per replay
+    std::vector<std::string> trace_names;  // launch names per trace slot (LITHOGPU_TRACE)
   };
   std::vector<GraphEntry> graphs;
   std::vector<GraphKey> warm;
@@ -943,15 +995,16 @@ static void ilt_run_impl(lithogpu_ilt* ilt, int iters, double* cost_user, double
           lg::fl_adj_rows(fg, s, tiles, F, false, Ef != nullptr, Ef ? Ef : P.Tb.template as<C>(), Ef ? P.s_E : P.s_T,
                           P.Wsub.template as<T>(), P.s_Wsub, P.U.template as<C>(), P.s_U);
         });
+        const long long npairs = (P.g.ay.N + 1) / 2;
+        const int ncost = int(std::min<long long>(P.s_cr, F * npairs * std::max(1, lg::fast_tpr(P.g.ax.N) / 32)));
+        double* cost_it = ilt->cost.as<double>() + size_t(it) * tiles;
         P.fl("adj_cols", [&] {
           lg::fl_adj_cols(fg, s, tiles, P.U.template as<C>(), P.s_U, P.Ht.template as<C>(), P.wk.template as<T>(), dose,
                           P.Acc.template as<C>(), P.s_Acc);
         });
-        const long long npairs = (P.g.ay.N + 1) / 2;
-        const int ncost = int(std::min<long long>(P.s_cr, F * npairs * std::max(1, lg::fast_tpr(P.g.ax.N) / 32)));
         P.fl("grad_cols", [&] {
           lg::fl_grad_cols(fg, s, tiles, P.Acc.template as<C>(), P.s_Acc, F * P.K, P.Gc.template as<C>(), P.s_Gc,
-                           P.costrow.template as<double>(), P.s_cr, ncost, ilt->cost.as<double>() + size_t(it) * tiles, 1);
+                           P.costrow.template as<double>(), P.s_cr, ncost, cost_it, 1);
         });
         P.fl("grad_rows", [&] {
           lg::fl_grad_rows(fg, s, tiles, true, P.Gc.template as<C>(), P.s_Gc, nullptr, 0, theta, NN, a, step,
@@ -991,6 +1044,8 @@ static void ilt_run_impl(lithogpu_ilt* ilt, int iters, double* cost_user, double
   }
   };  // enqueue
 
+  static const char* trace_path = std::getenv("LITHOGPU_TRACE");
+  if (trace_path) P.trace_reset();
   // CUDA graph of the whole `iters`-iteration launch sequence: captured on the
   // second call with an identical configuration, replayed afterwards.
   const bool graphable = ctx->stream != nullptr && !ctx->profiling && iters > 0 &&
@@ -1019,11 +1074,12 @@ static void ilt_run_impl(lithogpu_ilt* ilt, int iters, double* cost_user, double
       const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
       cudaGraphDestroy(graph);
       LG_CUDA(ie);
-      ilt->graphs.push_back({key, exec, ctx->launches - l0});
+      ilt->graphs.push_back({key, exec, ctx->launches - l0, P.trace_names});
       ctx->launches = l0;
       hit = &ilt->graphs.back();
     }
     if (hit) {
+      if (trace_path) P.trace_names = hit->trace_names;
       LG_CUDA(cudaGraphLaunch(hit->exec, ctx->stream));
       ctx->launches += hit->nk;
     } else {
@@ -1031,6 +1087,7 @@ static void ilt_run_impl(lithogpu_ilt* ilt, int iters, double* cost_user, double
       ilt->warm.push_back(key);
     }
   }
+  if (trace_path) P.trace_dump(trace_path);
 
   if (cost_user) {
     const size_t bytes = sizeof(double) * size_t(iters) * tiles;

@@ -102,3 +102,4 @@ bool fl_band_col2(const FGeo& g, cudaStream_t s, int tiles, int nf, bool sub_in,
 }
 
 }  // namespace lg
+

@@ -7,6 +7,11 @@
 #include <stdexcept>
 #include <string>
 #include <type_traits>
+#include <unordered_set>
+
+#ifndef LG_DEFAULT_CARVEOUT
+#define LG_DEFAULT_CARVEOUT -1
+#endif
 
 #include "socs_fast.cuh"
 
@@ -83,9 +88,29 @@ inline bool& pdl_enabled() {
   return on;
 }
 
+// Shared-memory carveout applied once per kernel (LITHOGPU_CARVEOUT=percent;
+// -1 = driver default).  Kernels of one ILT iteration that ask for different
+// L1/shared splits force the SMs to drain and reconfigure between launches.
+inline int carveout_pct() {
+  static const int pct = [] {
+    const char* e = std::getenv("LITHOGPU_CARVEOUT");
+    return e ? std::atoi(e) : LG_DEFAULT_CARVEOUT;
+  }();
+  return pct;
+}
+template <typename K>
+inline void apply_carveout(K kern) {
+  const int pct = carveout_pct();
+  if (pct < 0) return;
+  thread_local std::unordered_set<const void*> done;
+  if (done.insert(reinterpret_cast<const void*>(kern)).second)
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+}
+
 // launch with programmatic stream serialization (PDL; LITHOGPU_NO_PDL=1 disables)
 template <typename K, typename... A>
 inline void pdl_launch(K kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s, A... args) {
+  apply_carveout(kern);
   static const bool env_off = std::getenv("LITHOGPU_NO_PDL") != nullptr;
   const bool on = pdl_enabled() && !env_off;
   cudaLaunchConfig_t cfg = {};

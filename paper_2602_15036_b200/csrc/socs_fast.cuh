@@ -28,6 +28,30 @@ __device__ __forceinline__ void pdl_entry() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
+// ---- launch trace (diagnostic; FGeo::trace) ----
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned long long* trace_cell(const FGeo& g) {
+  const unsigned cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  return cta < unsigned(kTraceCtas) ? g.trace + (size_t(g.trace_slot) * kTraceCtas + cta) * 2 : nullptr;
+}
+__device__ __forceinline__ void trace_begin(const FGeo& g) {
+  if (g.trace && threadIdx.x == 0)
+    if (auto* c = trace_cell(g)) c[0] = gtimer();
+}
+__device__ __forceinline__ void trace_end(const FGeo& g) {
+  if (g.trace && (threadIdx.x & 31) == 0)
+    if (auto* c = trace_cell(g)) atomicMax(c + 1, gtimer());
+}
+struct TraceScope {  // CTA begin at construction, per-warp end at scope exit
+  const FGeo& g;
+  __device__ __forceinline__ explicit TraceScope(const FGeo& g_) : g(g_) { trace_begin(g); }
+  __device__ __forceinline__ ~TraceScope() { trace_end(g); }
+};
+
 template <int L>
 struct FGroup {
   static constexpr int TPR = RPlan<L>::TPR;
@@ -65,25 +89,31 @@ __device__ __forceinline__ int islot(const AxisGeom& a, int i, int L) {
 }
 
 // Build Z = A + iB for the row held in the natural distribution from the
-// half spectra a[0..P], b[0..P] of two real signals (b may be null).
+// half spectra a[p*ld], b[p*ld] (p in [0, P]) of two real signals (b may be
+// null; ld = 1 for row-major spectra, the column length for column-major).  Element
+// e holds indices t + e*TPR, so only e < ceil((P+1)/TPR) can hit [0, P] and
+// only e >= E - ceil(P/TPR) can hit the mirror [L-P, L): the other slots are
+// zero by a warp-uniform test, without per-element divergent branches.
 template <int L>
 __device__ __forceinline__ void load_herm_pair(C32 (&v)[RPlan<L>::E], const FGroup<L>& g,
-                                               const C32* a, const C32* b, int P) {
+                                               const C32* a, const C32* b, int P, int ld) {
+  constexpr int E = RPlan<L>::E, TPR = RPlan<L>::TPR;
+  const int nlo = (P + TPR) / TPR, nhi = (P + TPR - 1) / TPR;
 #pragma unroll
-  for (int e = 0; e < RPlan<L>::E; ++e) {
+  for (int e = 0; e < E; ++e) {
     const int i = g.idx(e);
     const int m = (i == 0 ? 0 : L - i);
     C32 A = mk(0.f, 0.f), Bv = mk(0.f, 0.f);
-    if (i <= P) {
-      A = a[i];
-      if (b) Bv = b[i];
+    if (e < nlo && i <= P) {
+      A = a[size_t(i) * ld];
+      if (b) Bv = b[size_t(i) * ld];
       if (m == i) {
         A.y = 0.f;
         Bv.y = 0.f;
       }
-    } else if (m <= P) {
-      A = conjg(a[m]);
-      if (b) Bv = conjg(b[m]);
+    } else if (e >= E - nhi && m <= P) {
+      A = conjg(a[size_t(m) * ld]);
+      if (b) Bv = conjg(b[size_t(m) * ld]);
     }
     v[e] = mk(A.x - Bv.y, A.y + Bv.x);
   }
@@ -146,9 +176,10 @@ __device__ __forceinline__ void store_pair_cols(const FGroup<L>& G, size_t tile_
   }
 }
 
-// min resident CTAs for the full-resolution row kernels (3 measured slower: tail)
+// min resident CTAs for the full-resolution row kernels (64 registers with the
+// 2048 = 8*8*8*4 plan)
 #ifndef LG_FULLROW_MINB
-#define LG_FULLROW_MINB 2
+#define LG_FULLROW_MINB 4
 #endif
 
 // warp-partial (deterministic) reduction: lane 0 of each warp-slice writes
@@ -169,6 +200,7 @@ __global__ void __launch_bounds__(256) fk_real_rows_fwd(FGeo g, const float* __r
                                                         long long src_ts, float steep, int Pout,
                                                         C32* __restrict__ out, long long out_ts) {
   FGroup<L> G;
+  TraceScope trace_(g);
   constexpr int E = RPlan<L>::E;
   const int Ny = g.ay.N, npairs = (Ny + 1) / 2;
   const int pair0 = blockIdx.x * G.groups + G.gid;
@@ -213,6 +245,7 @@ __global__ void __launch_bounds__(256) fk_socs_rows(FGeo g, const C32* __restric
                                                     long long ip_ts, C32* __restrict__ Eo,
                                                     long long e_ts) {
   FGroup<L> G;
+  TraceScope trace_(g);
   constexpr int E = RPlan<L>::E;
   const int Bx = g.ax.B, ny = g.ay.n, lo = g.ax.lo, hi = g.ax.hi;
   const int sy = blockIdx.x, fk = blockIdx.y * G.groups + G.gid;
@@ -256,6 +289,7 @@ __global__ void __launch_bounds__(256) fk_isub_rows(FGeo g, const float* __restr
                                                     long long ip_ts, int nsum, C32* __restrict__ Ir,
                                                     long long ir_ts) {
   FGroup<L> G;
+  TraceScope trace_(g);
   constexpr int E = RPlan<L>::E;
   const int f = blockIdx.y, ny = g.ay.n, npairs = (ny + 1) / 2;
   const int pair0 = blockIdx.x * G.groups + G.gid;
@@ -304,6 +338,7 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_resist_rows(FGeo g, c
                                                       long long d_ts, double* __restrict__ costp,
                                                       long long cp_ts) {
   FGroup<L> G;
+  TraceScope trace_(g);
   constexpr int E = RPlan<L>::E, TPR = RPlan<L>::TPR;
   constexpr int WPG = TPR >= 32 ? TPR / 32 : 1;
   const int Ny = g.ay.N, Px = g.ax.P, f = blockIdx.y, npairs = (Ny + 1) / 2;
@@ -318,7 +353,7 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_resist_rows(FGeo g, c
   float* tsl = row_slab<L>(G.groups, G.gid);
   stage_rows_async<L>(tsl, tg + size_t(y0) * L, tg + size_t(has1 ? y1 : y0) * L, G.t);
   C32 v[E];
-  load_herm_pair<L>(v, G, rc + size_t(y0) * (Px + 1), has1 ? rc + size_t(y1) * (Px + 1) : nullptr, Px);
+  load_herm_pair<L>(v, G, rc + y0, has1 ? rc + y1 : nullptr, Px, Ny);  // column-major [px][y]
   fftr<float, L, +1>(v, G.sm, g.twNx, G.t, G.sync);
   stage_wait();
   G.sync();
@@ -360,14 +395,15 @@ __global__ void __launch_bounds__(256) fk_out_rows(FGeo g, const C32* __restrict
                                                    unsigned char* __restrict__ print, long long o_ts,
                                                    float thr) {
   FGroup<L> G;
+  TraceScope trace_(g);
   constexpr int E = RPlan<L>::E;
   const int Ny = g.ay.N, Px = g.ax.P, f = blockIdx.y;
   const int y0 = blockIdx.x * G.groups + G.gid;
   const bool act = y0 < Ny;
   const int y = act ? y0 : Ny - 1;
-  const size_t cb = blockIdx.z * c_ts + (size_t(f) * Ny + y) * (Px + 1);
+  const size_t cb = blockIdx.z * c_ts + size_t(f) * Ny * (Px + 1) + y;  // column-major [f][px][y]
   C32 v[E];
-  load_herm_pair<L>(v, G, Ic ? Ic + cb : Rc + cb, (Ic && Rc) ? Rc + cb : nullptr, Px);
+  load_herm_pair<L>(v, G, Ic ? Ic + cb : Rc + cb, (Ic && Rc) ? Rc + cb : nullptr, Px, Ny);
   fftr<float, L, +1>(v, G.sm, g.twNx, G.t, G.sync);
   if (!act) return;
   const size_t ob = blockIdx.z * o_ts + (size_t(f) * Ny + y) * L;
@@ -391,6 +427,7 @@ __global__ void __launch_bounds__(256) fk_wlp_rows(FGeo g, const C32* __restrict
                                                    long long w_ts, float* __restrict__ Wsub,
                                                    long long ws_ts) {
   FGroup<L> G;
+  TraceScope trace_(g);
   constexpr int E = RPlan<L>::E;
   const int ny = g.ay.n, Px = g.ax.P, f = blockIdx.y, npairs = (ny + 1) / 2;
   const int pair0 = blockIdx.x * G.groups + G.gid;
@@ -400,7 +437,7 @@ __global__ void __launch_bounds__(256) fk_wlp_rows(FGeo g, const C32* __restrict
   const bool has1 = y1 < ny;
   const C32* wc = Wc + blockIdx.z * w_ts + size_t(f) * ny * (Px + 1);
   C32 v[E];
-  load_herm_pair<L>(v, G, wc + size_t(y0) * (Px + 1), has1 ? wc + size_t(y1) * (Px + 1) : nullptr, Px);
+  load_herm_pair<L>(v, G, wc + y0, has1 ? wc + y1 : nullptr, Px, ny);  // column-major [px][sy]
   fftr<float, L, +1>(v, G.sm, g.twnx, G.t, G.sync);
   if (!act) return;
   float* o = Wsub + blockIdx.z * ws_ts + size_t(f) * ny * L;
@@ -423,6 +460,7 @@ __global__ void __launch_bounds__(256, 2) fk_adj_rows(FGeo g, const C32* __restr
                                                       long long ws_ts, C32* __restrict__ U,
                                                       long long u_ts) {
   FGroup<L> G;
+  TraceScope trace_(g);
   constexpr int E = RPlan<L>::E;
   const int ny = g.ay.n, Bx = g.ax.B, K = g.K, lo = g.ax.lo, hi = g.ax.hi;
   const int fk = blockIdx.y, f = fk / K;
@@ -487,6 +525,7 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_grad_rows(FGeo g, con
                                                     C32* __restrict__ Mr, long long mr_ts,
                                                     double* __restrict__ gmaxp, long long gm_ts) {
   FGroup<L> G;
+  TraceScope trace_(g);
   constexpr int E = RPlan<L>::E, TPR = RPlan<L>::TPR;
   constexpr int WPG = TPR >= 32 ? TPR / 32 : 1;
   const int Ny = g.ay.N, Pm = g.ax.Pm, npairs = (Ny + 1) / 2;
@@ -503,7 +542,7 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_grad_rows(FGeo g, con
     stage_rows_async<L>(tsl, th + size_t(y0) * L, th + size_t(has1 ? y1 : y0) * L, G.t);
   }
   C32 v[E];
-  load_herm_pair<L>(v, G, gc + size_t(y0) * (Pm + 1), has1 ? gc + size_t(y1) * (Pm + 1) : nullptr, Pm);
+  load_herm_pair<L>(v, G, gc + y0, has1 ? gc + y1 : nullptr, Pm, Ny);  // column-major [px][y]
   fftr<float, L, +1>(v, G.sm, g.twNx, G.t, G.sync);
   if (ILT) {
     stage_wait();
@@ -561,6 +600,7 @@ __global__ void __launch_bounds__(256) fk_mask_cols(FGeo g, const C32* __restric
                                                     long long mr_ts, C32* __restrict__ Mhat,
                                                     long long mh_ts) {
   FGroup<L> G;
+  TraceScope trace_(g);
   constexpr int E = RPlan<L>::E;
   const int Pm = g.ax.Pm;
   const int px0 = blockIdx.x * G.groups + G.gid;
@@ -602,6 +642,7 @@ __global__ void __launch_bounds__(512) fk_socs_cols(FGeo g, const C32* __restric
                                                     long long mh_ts, const C32* __restrict__ H,
                                                     C32* __restrict__ T, long long t_ts) {
   FGroup<L> G;
+  TraceScope trace_(g);
   constexpr int E = RPlan<L>::E;
   const int Bx = g.ax.B, By = g.ay.B, fk = blockIdx.y;
   const int c0 = blockIdx.x * G.groups;
@@ -644,6 +685,7 @@ __global__ void __launch_bounds__(256) fk_band_colfwd(FGeo g, const C32* __restr
                                                       C32* __restrict__ outR, C32* __restrict__ outI,
                                                       long long o_ts) {
   FGroup<L> G;
+  TraceScope trace_(g);
   constexpr int E = RPlan<L>::E;
   const int Px = g.ax.P, f = blockIdx.y, nb2 = g.ay.nb2;
   const int px0 = blockIdx.x * G.groups + G.gid;
@@ -676,6 +718,7 @@ __global__ void __launch_bounds__(256) fk_band_colinv(FGeo g, const C32* __restr
                                                       long long b_ts, C32* __restrict__ out,
                                                       long long o_ts) {
   FGroup<L> G;
+  TraceScope trace_(g);
   constexpr int E = RPlan<L>::E;
   const int Px = g.ax.P, f = blockIdx.y, nb2 = g.ay.nb2;
   const int px0 = blockIdx.x * G.groups + G.gid;
@@ -690,9 +733,9 @@ __global__ void __launch_bounds__(256) fk_band_colinv(FGeo g, const C32* __restr
   }
   fftr<float, L, +1>(v, G.sm, L == g.ay.N ? g.twNy : g.twny, G.t, G.sync);
   if (!act) return;
-  C32* o = out + blockIdx.z * o_ts + size_t(f) * L * (Px + 1);
+  C32* o = out + blockIdx.z * o_ts + (size_t(f) * (Px + 1) + px) * L;  // column-major [f][px][y]
 #pragma unroll
-  for (int e = 0; e < E; ++e) o[size_t(G.idx(e)) * (Px + 1) + px] = v[e];
+  for (int e = 0; e < E; ++e) o[G.idx(e)] = v[e];
 }
 
 // ===========================================================================
@@ -726,6 +769,7 @@ __global__ void __launch_bounds__(256) fk_band_col2(FGeo g, const C32* __restric
                                                     C32* __restrict__ outR, C32* __restrict__ outI,
                                                     long long o_ts) {
   pdl_entry();
+  TraceScope trace_(g);
   using CP = Col2<LIN, LOUT>;
   constexpr int EI = RPlan<LIN>::E, EO = RPlan<LOUT>::E;
   extern __shared__ __align__(16) unsigned char fsm_raw[];
@@ -759,7 +803,7 @@ __global__ void __launch_bounds__(256) fk_band_col2(FGeo g, const C32* __restric
   gsync();
   if (t >= CP::TOUT) return;
   const GSync s2 = CP::TOUT == CP::TPR ? gsync : sub_gsync(CP::TOUT, 1 + groups + gid);
-  const size_t ob = blockIdx.z * o_ts + size_t(f) * LOUT * (Px + 1);
+  const size_t ob = blockIdx.z * o_ts + (size_t(f) * (Px + 1) + px) * LOUT;  // column-major [f][px][y]
   for (int pass = 0; pass < 2; ++pass) {
     C32* out = pass == 0 ? outR : outI;
     if (!out) continue;
@@ -773,7 +817,7 @@ __global__ void __launch_bounds__(256) fk_band_col2(FGeo g, const C32* __restric
     fftr<float, LOUT, +1>(v, sm, LOUT == g.ay.N ? g.twNy : g.twny, t, s2);
     if (act) {
 #pragma unroll
-      for (int e = 0; e < EO; ++e) out[ob + size_t(t + e * CP::TOUT) * (Px + 1) + px] = v[e];
+      for (int e = 0; e < EO; ++e) out[ob + t + e * CP::TOUT] = v[e];
     }
     s2();  // sm reused by the second pass
   }
@@ -792,6 +836,7 @@ __global__ void __launch_bounds__(256) fk_adj_cols(FGeo g, const C32* __restrict
                                                    const float* __restrict__ wk, float dose,
                                                    C32* __restrict__ Accp, long long a_ts) {
   FGroup<L> G;
+  TraceScope trace_(g);
   constexpr int E = RPlan<L>::E;
   const int Bx = g.ax.B, By = g.ay.B, cx = blockIdx.x, fk = blockIdx.y * G.groups + G.gid;
   const float sc = float(2.0 / (double(g.ax.n) * double(g.ay.n)));  // 2 (N/n)^2 / N^2
@@ -819,6 +864,31 @@ __global__ void __launch_bounds__(256) fk_adj_cols(FGeo g, const C32* __restrict
   }
 }
 
+// Fixed-order (deterministic) CTA sum of n cost partials into *out: strided
+// per-thread sums with 8 loads in flight, then a fixed pairwise tree
+// (blockDim a power of two <= 512).
+__device__ __forceinline__ void reduce_cost(const double* __restrict__ c, int n, double* out) {
+  __shared__ double red[512];
+  const int bd = blockDim.x;
+  double s = 0;
+  int i = threadIdx.x;
+  for (; i + 7 * bd < n; i += 8 * bd) {
+    double x[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = c[i + j * bd];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += x[j];
+  }
+  for (; i < n; i += bd) s += c[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int h = bd / 2; h > 0; h >>= 1) {
+    if (int(threadIdx.x) < h) red[threadIdx.x] += red[threadIdx.x + h];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+
 // ===========================================================================
 // gradient columns: Hermitian part of Acc, IFFT_Ny -> Gc[y][px], px in [0,Pmx];
 // the last CTA reduces this iteration's cost partials (fixed order).
@@ -831,30 +901,10 @@ __global__ void __launch_bounds__(256) fk_grad_cols(FGeo g, const C32* __restric
                                                     long long cp_ts, int ncost,
                                                     double* __restrict__ cost_out, long long co_ts) {
   FGroup<L> G;
+  TraceScope trace_(g);
   constexpr int E = RPlan<L>::E;
   if (blockIdx.x == gridDim.x - 1) {
-    if (cost_out) {  // fixed-order (deterministic) parallel sum of the cost partials
-      __shared__ double red[512];
-      const double* c = costp + blockIdx.z * cp_ts;
-      const int bd = blockDim.x;
-      double s = 0;
-      int i = threadIdx.x;
-      for (; i + 7 * bd < ncost; i += 8 * bd) {  // 8 loads in flight, summed in index order
-        double x[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) x[j] = c[i + j * bd];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) s += x[j];
-      }
-      for (; i < ncost; i += bd) s += c[i];
-      red[threadIdx.x] = s;
-      __syncthreads();
-      for (int h = bd / 2; h > 0; h >>= 1) {  // fixed pairwise tree (bd is a power of two)
-        if (int(threadIdx.x) < h) red[threadIdx.x] += red[threadIdx.x + h];
-        __syncthreads();
-      }
-      if (threadIdx.x == 0) cost_out[blockIdx.z * co_ts] = red[0];
-    }
+    if (cost_out) reduce_cost(costp + blockIdx.z * cp_ts, ncost, cost_out + blockIdx.z * co_ts);
     return;
   }
   const int Pm = g.ax.Pm, Bx = g.ax.B;
@@ -894,9 +944,9 @@ __global__ void __launch_bounds__(256) fk_grad_cols(FGeo g, const C32* __restric
   }
   fftr<float, L, +1>(v, G.sm, g.twNy, G.t, G.sync);
   if (!act) return;
-  C32* o = Gc + blockIdx.z * g_ts;
+  C32* o = Gc + blockIdx.z * g_ts + size_t(px) * L;  // column-major [px][y]
 #pragma unroll
-  for (int e = 0; e < E; ++e) o[size_t(G.idx(e)) * (Pm + 1) + px] = v[e];
+  for (int e = 0; e < E; ++e) o[G.idx(e)] = v[e];
 }
 
 }  // namespace lg

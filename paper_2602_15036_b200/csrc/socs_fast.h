@@ -19,7 +19,12 @@ struct FGeo {
   const cx<float>* twNy;
   const cx<float>* twnx;
   const cx<float>* twny;
+  // launch trace (LITHOGPU_TRACE): per-CTA [start, end] %globaltimer of
+  // launch `trace_slot`, kTraceCtas CTAs per slot; null = off
+  unsigned long long* trace = nullptr;
+  int trace_slot = 0;
 };
+constexpr int kTraceCtas = 4096;
 
 using C32 = cx<float>;
 
