@@ -177,6 +177,31 @@ lithogpu_status lithogpu_ilt_get_tile(lithogpu_ilt* ilt, int tile, void* theta, 
 lithogpu_status lithogpu_ilt_get_tiles(lithogpu_ilt* ilt, void* theta, void* mask,
                                        lithogpu_dtype dtype);
 
+/* ---- contours and EPE gauges of a resist image ----
+ * marching_squares (contour.cpp:58-168) of an ny x nx f64 field (host or
+ * device; node (ix,iy) at the pixel centre origin + (i+0.5)*pitch) at
+ * `threshold`.  The loops are bit-identical to the reference ContourSet: same
+ * loop order (ascending smallest grid-edge id), same start point, same point
+ * order and fp64 values.  Non-finite fields and open (border-crossing)
+ * contours fail with LITHOGPU_ERR_DOMAIN, as the reference throws.  The
+ * object keeps the crossing graph on the device for lithogpu_measure_epe. */
+typedef struct lithogpu_contours lithogpu_contours;
+lithogpu_status lithogpu_marching_squares(lithogpu_ctx* ctx, const lithogpu_grid* grid, const double* field,
+                                          double threshold, lithogpu_contours** out);
+lithogpu_status lithogpu_contours_size(const lithogpu_contours* c, int64_t* n_loops, int64_t* n_points);
+/* loop_start[n_loops+1] offsets into xs/ys[n_points] (host or device buffers;
+ * the reference ContourLoop::xs/ys, contour.hpp:13-22) */
+lithogpu_status lithogpu_contours_get(const lithogpu_contours* c, int64_t* loop_start, double* xs, double* ys);
+void lithogpu_contours_destroy(lithogpu_contours* c);
+/* measure_epe (contour.cpp:181-201 over SegmentBvh::nearest_crossing,
+ * bvh.cpp:241-273): gauges are n x {x, y, nx, ny} f64 (site and unit outward
+ * normal, nm; Gauge contour.hpp:30-34, segment ids stay with the caller).
+ * epe_nm[i] = signed distance to the nearest crossing along the normal
+ * (|t| <= search_radius, ties to +t), open[i] = 1 when there is none
+ * (epe 0).  Host or device buffers. */
+lithogpu_status lithogpu_measure_epe(lithogpu_contours* c, const double* gauges, int64_t n,
+                                     double search_radius_nm, double* epe_nm, uint8_t* open);
+
 /* ---- host-side kernel generation (precompute, not on the timed path) ----
  * Replaces build_tcc + decompose_tcc (imaging.cpp:113-216) with the same
  * semantics via the TCC = Q Q^H factorisation (no dense S x S eigensolve, so

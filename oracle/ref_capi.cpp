@@ -4,7 +4,8 @@
 // rasterize_layer (raster.cpp:53-95, heal included), heal (boolean.hpp:40-42),
 // build_tcc/decompose_tcc (imaging.cpp:113-216), image_socs (:218-241),
 // image_hopkins_direct (:243-285), gaussian_blur (:287-314), pupil (:72-84),
-// intensity_gradient (ai.cpp:11-42), z_print/z_round (ai.cpp:76-94).
+// intensity_gradient (ai.cpp:11-42), z_print/z_round (ai.cpp:76-94),
+// marching_squares / measure_epe (contour.cpp:58-201).
 //
 // The ILT pieces the reference lacks (weighted adjoint, sigmoid resist,
 // process-window cost, theta update) are composed
@@ -20,6 +21,7 @@
 
 #include "core/ai.hpp"
 #include "core/boolean.hpp"
+#include "core/contour.hpp"
 #include "core/imaging.hpp"
 #include "core/raster.hpp"
 
@@ -361,6 +363,58 @@ int ref_ilt_iteration(int nx, int ny, double pitch, int F, int K, const double* 
       theta[i] -= step * gt;
     }
     *cost_out = cost;
+  });
+}
+
+// marching_squares (contour.cpp:58-168): the result is kept for ref_ms_get /
+// ref_measure_epe (single-threaded test use)
+namespace {
+litho::ContourSet g_contours;
+}
+
+int ref_marching_squares(int nx, int ny, double pitch, double ox, double oy, const double* field, double thr,
+                         int64_t* n_loops, int64_t* n_points) {
+  return guarded([&] {
+    litho::ResistImage r;
+    r.grid = make_grid(nx, ny, pitch, ox, oy);
+    r.values.assign(field, field + size_t(nx) * ny);
+    g_contours = litho::marching_squares(r, thr);
+    int64_t np = 0;
+    for (const auto& l : g_contours.loops) np += int64_t(l.size());
+    *n_loops = int64_t(g_contours.loops.size());
+    *n_points = np;
+  });
+}
+
+void ref_ms_get(int64_t* loop_start, double* xs, double* ys) {
+  int64_t o = 0, k = 0;
+  for (const auto& l : g_contours.loops) {
+    loop_start[k++] = o;
+    for (size_t i = 0; i < l.size(); ++i, ++o) {
+      xs[o] = l.xs[i];
+      ys[o] = l.ys[i];
+    }
+  }
+  loop_start[k] = o;
+}
+
+// measure_epe (contour.cpp:181-201) on the last marching_squares result;
+// gauges n x {x, y, nx, ny}
+int ref_measure_epe(const double* gauges, int64_t n, double radius, double* epe, uint8_t* open) {
+  return guarded([&] {
+    std::vector<litho::Gauge> gs(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+      gs[i].segment_id = uint32_t(i);
+      gs[i].x = gauges[4 * i];
+      gs[i].y = gauges[4 * i + 1];
+      gs[i].nx = gauges[4 * i + 2];
+      gs[i].ny = gauges[4 * i + 3];
+    }
+    const auto recs = litho::measure_epe(g_contours, gs, radius);
+    for (int64_t i = 0; i < n; ++i) {
+      epe[i] = recs[i].epe_nm;
+      open[i] = recs[i].open ? 1 : 0;
+    }
   });
 }
 

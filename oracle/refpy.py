@@ -216,3 +216,28 @@ def ilt_iteration(theta, target, weights, support, values, focus_weight, params,
                                    _p(fw, C.c_double), _p(pr, C.c_double), _p(t, C.c_double),
                                    _p(theta, C.c_double), C.byref(cost), _p(grad, C.c_double)))
     return cost.value, grad.reshape(ny, nx)
+
+
+def marching_squares(field, threshold, pitch=1.0, ox=0.0, oy=0.0):
+    """reference marching_squares (contour.cpp:58-168): list of (xs, ys) loops."""
+    f = np.ascontiguousarray(field, dtype=np.float64)
+    ny, nx = f.shape
+    nl, npnt = C.c_int64(), C.c_int64()
+    _check(lib().ref_marching_squares(nx, ny, C.c_double(pitch), C.c_double(ox), C.c_double(oy),
+                                      _p(f, C.c_double), C.c_double(threshold), C.byref(nl), C.byref(npnt)))
+    st = np.zeros(nl.value + 1, np.int64)
+    xs = np.zeros(max(npnt.value, 1))
+    ys = np.zeros(max(npnt.value, 1))
+    lib().ref_ms_get(_p(st, C.c_int64), _p(xs, C.c_double), _p(ys, C.c_double))
+    return st, xs[:npnt.value], ys[:npnt.value]
+
+
+def measure_epe(gauges, radius):
+    """reference measure_epe (contour.cpp:181-201) on the last marching_squares result."""
+    g = np.ascontiguousarray(gauges, dtype=np.float64).reshape(-1, 4)
+    n = g.shape[0]
+    epe = np.zeros(max(n, 1))
+    op = np.zeros(max(n, 1), np.uint8)
+    _check(lib().ref_measure_epe(_p(g, C.c_double), C.c_int64(n), C.c_double(radius), _p(epe, C.c_double),
+                                 _p(op, C.c_uint8)))
+    return epe[:n], op[:n].astype(bool)

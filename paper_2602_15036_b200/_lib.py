@@ -72,6 +72,11 @@ _SIGS = {
     "lithogpu_ilt_run": (C.c_int, [_vp, C.c_int, _vp, _vp]),
     "lithogpu_ilt_get_tile": (C.c_int, [_vp, C.c_int, _vp, _vp, C.c_int]),
     "lithogpu_ilt_get_tiles": (C.c_int, [_vp, _vp, _vp, C.c_int]),
+    "lithogpu_marching_squares": (C.c_int, [_vp, C.POINTER(Grid), _vp, C.c_double, C.POINTER(_vp)]),
+    "lithogpu_contours_size": (C.c_int, [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "lithogpu_contours_get": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "lithogpu_contours_destroy": (None, [_vp]),
+    "lithogpu_measure_epe": (C.c_int, [_vp, _vp, C.c_int64, C.c_double, _vp, _vp]),
     "lithogpu_source_annular": (C.c_int, [C.c_double, C.c_double, C.c_int, C.POINTER(C.c_int), _vp]),
     "lithogpu_tcc_support": (C.c_int, [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                        C.c_double, C.POINTER(C.c_int), _vp]),

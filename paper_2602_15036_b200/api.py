@@ -444,6 +444,75 @@ def rasterize_layer(polygons, grid: Grid, dbu_per_nm: float, ctx: Optional[Conte
 
 
 # ---------------------------------------------------------------------------
+# contours and EPE (reference contour.hpp / contour.cpp:58-201)
+# ---------------------------------------------------------------------------
+class ContourSet:
+    """marching_squares result (reference ContourSet, contour.hpp:13-27):
+    loops[i] = (xs, ys) closed polyline in nm, CCW around printed regions.
+    Keeps the device crossing graph for measure_epe."""
+
+    def __init__(self, handle, ctx):
+        self._h = handle
+        self.ctx = ctx
+        nl, npnt = C.c_int64(), C.c_int64()
+        check(lib().lithogpu_contours_size(self._h, C.byref(nl), C.byref(npnt)))
+        self.loop_start = np.zeros(nl.value + 1, np.int64)
+        self.xs = np.zeros(npnt.value, np.float64)
+        self.ys = np.zeros(npnt.value, np.float64)
+        check(lib().lithogpu_contours_get(self._h, self.loop_start.ctypes.data,
+                                          self.xs.ctypes.data if npnt.value else None,
+                                          self.ys.ctypes.data if npnt.value else None))
+
+    @property
+    def loops(self):
+        st = self.loop_start
+        return [(self.xs[st[i]:st[i + 1]], self.ys[st[i]:st[i + 1]]) for i in range(len(st) - 1)]
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().lithogpu_contours_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def marching_squares(field, grid: Grid, threshold: float, ctx: Optional[Context] = None) -> ContourSet:
+    """marching_squares (contour.cpp:58-168) of a resist image (ny x nx f64,
+    numpy or CUDA tensor) at `threshold`; bit-identical loops."""
+    ctx = ctx or default_context()
+    if _is_torch(field):
+        field = field.to(torch.float64)
+    else:
+        field = np.ascontiguousarray(field, np.float64)
+    if tuple(field.shape) != (grid.ny, grid.nx):
+        raise ValueError("marching_squares: field shape does not match the grid")
+    finite = bool(torch.isfinite(field).all()) if _is_torch(field) else bool(np.isfinite(field).all())
+    if not finite:  # reference std::invalid_argument (contour.cpp:62-63)
+        raise ValueError("marching_squares: non-finite field")
+    buf, _, keep = _buf(field)
+    h = C.c_void_p()
+    g = grid.c()
+    check(lib().lithogpu_marching_squares(ctx.handle, C.byref(g), buf, threshold, C.byref(h)))
+    return ContourSet(h, ctx)
+
+
+def measure_epe(contours: ContourSet, gauges, search_radius_nm: float):
+    """measure_epe (contour.cpp:181-201): gauges (n, 4) = x, y, nx, ny (site and
+    unit outward normal, nm).  Returns (epe_nm[n], open[n] bool)."""
+    g = np.ascontiguousarray(gauges, np.float64).reshape(-1, 4)
+    n = g.shape[0]
+    epe = np.zeros(max(n, 1), np.float64)
+    op = np.zeros(max(n, 1), np.uint8)
+    check(lib().lithogpu_measure_epe(contours._h, g.ctypes.data, n, search_radius_nm, epe.ctypes.data,
+                                     op.ctypes.data))
+    return epe[:n], op[:n].astype(bool)
+
+
+# ---------------------------------------------------------------------------
 # ILT
 # ---------------------------------------------------------------------------
 @dataclass

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "../../include/lithogpu.h"
+#include "contour_kernels.cuh"
 #include "raster_kernels.cuh"
 #include "socs_kernels.cuh"
 #include "util_kernels.cuh"
@@ -1828,3 +1829,222 @@ lithogpu_status lithogpu_ilt_get_tiles(lithogpu_ilt* ilt, void* theta, void* mas
 }
 
 }  // extern "C"
+
+// ===========================================================================
+// contours + EPE: contour_kernels.cuh
+// ===========================================================================
+struct lithogpu_contours {
+  lithogpu_ctx* ctx = nullptr;
+  lg::CGeo g{};
+  long long ne = 0;
+  int ncross = 0;
+  long long nloops = 0, npts = 0;
+  DevBuf succ, pt, offsets, xs, ys;
+};
+
+namespace {
+void ms_scan(lithogpu_ctx* ctx, const int* in, int* out, long long n, DevBuf& tmp) {
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, n, ctx->stream);
+  tmp.ensure(std::max<size_t>(tb, 16));
+  cub::DeviceScan::ExclusiveSum(tmp.p, tb, in, out, n, ctx->stream);
+}
+void ms_scan64(lithogpu_ctx* ctx, const int* in, long long* out, long long n, DevBuf& tmp) {
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveScan(nullptr, tb, in, out, cub::Sum(), 0ll, n, ctx->stream);
+  tmp.ensure(std::max<size_t>(tb, 16));
+  cub::DeviceScan::ExclusiveScan(tmp.p, tb, in, out, cub::Sum(), 0ll, n, ctx->stream);
+}
+template <typename T>
+T read_dev(lithogpu_ctx* ctx, const T* p) {
+  T v;
+  LG_CUDA(cudaMemcpyAsync(&v, p, sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+  LG_CUDA(cudaStreamSynchronize(ctx->stream));
+  return v;
+}
+}  // namespace
+
+lithogpu_status lithogpu_marching_squares(lithogpu_ctx* ctx, const lithogpu_grid* grid, const double* field,
+                                          double threshold, lithogpu_contours** out) {
+  if (!ctx || !grid || !field || !out) {
+    g_last_error = "lithogpu_marching_squares: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    ctx->activate();
+    const int nx = grid->nx, ny = grid->ny;
+    if (nx <= 0 || ny <= 0) throw std::invalid_argument("marching_squares: empty grid");
+    auto c = std::make_unique<lithogpu_contours>();
+    c->ctx = ctx;
+    c->g = lg::CGeo{nx, ny, grid->pitch_nm, grid->origin_x_nm, grid->origin_y_nm, (long long)(nx - 1) * ny};
+    c->ne = c->g.nh + (long long)nx * (ny - 1);
+    if (nx < 2 || ny < 2) {  // reference :61
+      c->offsets.ensure(sizeof(long long));
+      LG_CUDA(cudaMemsetAsync(c->offsets.p, 0, sizeof(long long), ctx->stream));
+      *out = c.release();
+      return;
+    }
+    const size_t npix = size_t(nx) * ny;
+    const double* f = stage_in<double>(ctx, field, LITHOGPU_F64, npix, 0);
+    const int nblk = 256;
+    DevBuf part, mm, flags;
+    part.ensure(sizeof(double) * 2 * nblk);
+    mm.ensure(sizeof(double) * 2);
+    flags.ensure(sizeof(int) * 4);
+    LG_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int) * 4, ctx->stream));
+    int* fl = flags.as<int>();  // [0] non-finite, [1] duplicate edge, [2] broken chain
+    lg::k_field_minmax<<<nblk, 256, 0, ctx->stream>>>(f, (long long)npix, part.as<double>(), part.as<double>() + nblk, fl);
+    ctx->check_launch();
+    lg::k_field_minmax_final<<<1, 32, 0, ctx->stream>>>(part.as<double>(), part.as<double>() + nblk, nblk, mm.as<double>());
+    ctx->check_launch();
+    c->succ.ensure(sizeof(int) * c->ne);
+    c->pt.ensure(sizeof(double2) * c->ne);
+    LG_CUDA(cudaMemsetAsync(c->succ.p, 0xff, sizeof(int) * c->ne, ctx->stream));
+    dim3 blk(32, 8), grd(cdiv(nx - 1, 32), cdiv(ny - 1, 8));
+    lg::k_ms_cells<<<grd, blk, 0, ctx->stream>>>(c->g, f, threshold, mm.as<double>(), c->succ.as<int>(),
+                                                 c->pt.as<double2>(), fl + 1);
+    ctx->check_launch();
+    int hf[4];
+    LG_CUDA(cudaMemcpyAsync(hf, fl, sizeof(hf), cudaMemcpyDeviceToHost, ctx->stream));
+    LG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (hf[0]) throw std::invalid_argument("marching_squares: non-finite field");
+    if (hf[1]) throw std::runtime_error("marching_squares: inconsistent contour graph");
+    // compact the crossing edges in edge order
+    DevBuf flag, pos, tmp, idx;
+    flag.ensure(sizeof(int) * (c->ne + 1));
+    pos.ensure(sizeof(int) * (c->ne + 1));
+    idx.ensure(sizeof(int) * c->ne);
+    const int gb = 148 * 8;
+    lg::k_ms_flags<<<gb, 256, 0, ctx->stream>>>(c->succ.as<int>(), c->ne, flag.as<int>());
+    ctx->check_launch();
+    LG_CUDA(cudaMemsetAsync(flag.as<int>() + c->ne, 0, sizeof(int), ctx->stream));
+    ms_scan(ctx, flag.as<int>(), pos.as<int>(), c->ne + 1, tmp);
+    const int n = read_dev(ctx, pos.as<int>() + c->ne);
+    c->ncross = n;
+    if (n == 0) {
+      c->offsets.ensure(sizeof(long long));
+      LG_CUDA(cudaMemsetAsync(c->offsets.p, 0, sizeof(long long), ctx->stream));
+      LG_CUDA(cudaStreamSynchronize(ctx->stream));
+      *out = c.release();
+      return;
+    }
+    DevBuf cedge, csucc, m0, m1, j0, j1, d0, d1, isst, len, lidx, ptoff;
+    cedge.ensure(sizeof(int) * n);
+    csucc.ensure(sizeof(int) * n);
+    for (DevBuf* b : {&m0, &m1, &j0, &j1, &d0, &d1}) b->ensure(sizeof(int) * n);
+    lg::k_ms_compact<<<gb, 256, 0, ctx->stream>>>(c->succ.as<int>(), pos.as<int>(), c->ne, cedge.as<int>(), idx.as<int>());
+    ctx->check_launch();
+    const int tb = cdiv(n, 256);
+    lg::k_ms_link<<<tb, 256, 0, ctx->stream>>>(cedge.as<int>(), c->succ.as<int>(), idx.as<int>(), n, csucc.as<int>(),
+                                               m0.as<int>(), fl + 2);
+    ctx->check_launch();
+    if (read_dev(ctx, fl + 2)) throw std::runtime_error("marching_squares: broken contour chain");
+    int rounds = 1;
+    while ((1 << rounds) < n) ++rounds;
+    // cycle minima
+    LG_CUDA(cudaMemcpyAsync(j0.p, csucc.p, sizeof(int) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    int *mA = m0.as<int>(), *mB = m1.as<int>(), *jA = j0.as<int>(), *jB = j1.as<int>();
+    for (int r = 0; r < rounds; ++r) {
+      lg::k_ms_minjump<<<tb, 256, 0, ctx->stream>>>(mA, jA, n, mB, jB);
+      ctx->check_launch();
+      std::swap(mA, mB);
+      std::swap(jA, jB);
+    }
+    // distance to the end of each cycle cut before its start
+    int *nA = jB, *nB = jA, *dA = d0.as<int>(), *dB = d1.as<int>();
+    lg::k_ms_rank_init<<<tb, 256, 0, ctx->stream>>>(csucc.as<int>(), cedge.as<int>(), mA, n, nA, dA);
+    ctx->check_launch();
+    for (int r = 0; r < rounds; ++r) {
+      lg::k_ms_rank_jump<<<tb, 256, 0, ctx->stream>>>(nA, dA, n, nB, dB);
+      ctx->check_launch();
+      std::swap(nA, nB);
+      std::swap(dA, dB);
+    }
+    isst.ensure(sizeof(int) * (n + 1));
+    len.ensure(sizeof(int) * (n + 1));
+    lidx.ensure(sizeof(int) * (n + 1));
+    ptoff.ensure(sizeof(long long) * (n + 1));
+    lg::k_ms_starts<<<tb, 256, 0, ctx->stream>>>(cedge.as<int>(), mA, dA, n, isst.as<int>(), len.as<int>());
+    ctx->check_launch();
+    LG_CUDA(cudaMemsetAsync(isst.as<int>() + n, 0, sizeof(int), ctx->stream));
+    LG_CUDA(cudaMemsetAsync(len.as<int>() + n, 0, sizeof(int), ctx->stream));
+    ms_scan(ctx, isst.as<int>(), lidx.as<int>(), n + 1, tmp);
+    ms_scan64(ctx, len.as<int>(), ptoff.as<long long>(), n + 1, tmp);
+    c->nloops = read_dev(ctx, lidx.as<int>() + n);
+    c->npts = read_dev(ctx, ptoff.as<long long>() + n);
+    if (c->npts != n) throw std::runtime_error("marching_squares: broken contour chain");
+    c->offsets.ensure(sizeof(long long) * (c->nloops + 1));
+    c->xs.ensure(sizeof(double) * n);
+    c->ys.ensure(sizeof(double) * n);
+    lg::k_ms_offsets<<<tb, 256, 0, ctx->stream>>>(isst.as<int>(), lidx.as<int>(), ptoff.as<long long>(), n,
+                                                  c->offsets.as<long long>(), c->npts);
+    ctx->check_launch();
+    lg::k_ms_scatter<<<tb, 256, 0, ctx->stream>>>(cedge.as<int>(), mA, idx.as<int>(), dA, ptoff.as<long long>(),
+                                                  c->pt.as<double2>(), n, c->xs.as<double>(), c->ys.as<double>());
+    ctx->check_launch();
+    LG_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = c.release();
+  });
+}
+
+lithogpu_status lithogpu_contours_size(const lithogpu_contours* c, int64_t* n_loops, int64_t* n_points) {
+  if (!c || !n_loops || !n_points) {
+    g_last_error = "lithogpu_contours_size: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  *n_loops = c->nloops;
+  *n_points = c->npts;
+  return LITHOGPU_OK;
+}
+
+lithogpu_status lithogpu_contours_get(const lithogpu_contours* c, int64_t* loop_start, double* xs, double* ys) {
+  if (!c || (!loop_start && !xs && !ys)) {
+    g_last_error = "lithogpu_contours_get: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    c->ctx->activate();
+    cudaStream_t s = c->ctx->stream;
+    if (loop_start)
+      LG_CUDA(cudaMemcpyAsync(loop_start, c->offsets.p, sizeof(long long) * (c->nloops + 1), cudaMemcpyDefault, s));
+    if (xs && c->npts) LG_CUDA(cudaMemcpyAsync(xs, c->xs.p, sizeof(double) * c->npts, cudaMemcpyDefault, s));
+    if (ys && c->npts) LG_CUDA(cudaMemcpyAsync(ys, c->ys.p, sizeof(double) * c->npts, cudaMemcpyDefault, s));
+    LG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+void lithogpu_contours_destroy(lithogpu_contours* c) { delete c; }
+
+lithogpu_status lithogpu_measure_epe(lithogpu_contours* c, const double* gauges, int64_t n, double search_radius_nm,
+                                     double* epe_nm, uint8_t* open) {
+  if (!c || (n > 0 && (!gauges || !epe_nm || !open)) || n < 0) {
+    g_last_error = "lithogpu_measure_epe: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    if (n == 0) return;
+    lithogpu_ctx* ctx = c->ctx;
+    ctx->activate();
+    const double* gd = stage_in<double>(ctx, gauges, LITHOGPU_F64, size_t(n) * 4, 0);
+    const bool dev_e = is_device_ptr(epe_nm), dev_o = is_device_ptr(open);
+    DevBuf eb, ob;
+    double* de = epe_nm;
+    unsigned char* dob = open;
+    if (!dev_e) {
+      eb.ensure(sizeof(double) * n);
+      de = eb.as<double>();
+    }
+    if (!dev_o) {
+      ob.ensure(size_t(n));
+      dob = ob.as<unsigned char>();
+    }
+    const bool grid_ok = c->g.nx >= 2 && c->g.ny >= 2;
+    lg::k_epe<<<cdiv(n * 32, 256), 256, 0, ctx->stream>>>(
+        c->g, grid_ok ? c->succ.as<int>() : nullptr, grid_ok ? c->pt.as<double2>() : nullptr, grid_ok ? c->ncross : 0,
+        reinterpret_cast<const lg::Gauge*>(gd), int(n), search_radius_nm, de, dob);
+    ctx->check_launch();
+    if (!dev_e) LG_CUDA(cudaMemcpyAsync(epe_nm, de, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    if (!dev_o) LG_CUDA(cudaMemcpyAsync(open, dob, size_t(n), cudaMemcpyDeviceToHost, ctx->stream));
+    LG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
