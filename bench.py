@@ -397,8 +397,57 @@ def _c1_forward(ctx, stream):
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
+    contours = _contours_c1(ctx, stream, dk, m32, grid)
     return {"workload": desc, "ms_per_image": ms, "mpix_s": grid.nx * grid.ny / (ms * 1e-3) / 1e6,
+            "contours": contours,
             "outputs": "aerial f32 + resist f32 + print u8", "l2": "warm (repeated image)"}
+
+
+def _contours_c1(ctx, stream, dk, m32, grid, n_gauges=4096, radius=20.0):
+    """SURVEY §8f rank 1 stage on the C1 resist image: GPU marching squares +
+    EPE gauges (device-resident field, host-synchronised result sizes, as the
+    API returns them) against the reference contour.cpp on one host core."""
+    import torch
+    import paper_2602_15036_b200 as L
+    res = dk.image(m32, sigma_nm=2.0, want=("resist",))["resist"].to(torch.float64)
+    res[:2, :] = 0.0  # clear the tile frame (halo): contours must close inside the tile
+    res[-2:, :] = 0.0
+    res[:, :2] = 0.0
+    res[:, -2:] = 0.0
+    rng = np.random.default_rng(7)
+    ang = rng.uniform(0, 2 * np.pi, n_gauges)
+    gauges = np.column_stack([rng.uniform(0, grid.nx, n_gauges), rng.uniform(0, grid.ny, n_gauges),
+                              np.cos(ang), np.sin(ang)])
+    for _ in range(2):
+        cs = L.marching_squares(res, grid, ILT["threshold"], ctx)
+        L.measure_epe(cs, gauges, radius)
+    torch.cuda.synchronize()
+    reps = 10
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        cs = L.marching_squares(res, grid, ILT["threshold"], ctx)
+    t1 = time.perf_counter()
+    for _ in range(reps):
+        epe, op = L.measure_epe(cs, gauges, radius)
+    t2 = time.perf_counter()
+    out = {"stage": "marching_squares + measure_epe (contour.cpp:58-201) on the C1 resist image",
+           "loops": len(cs.loop_start) - 1, "points": int(len(cs.xs)), "gauges": n_gauges,
+           "gpu_ms_contours": (t1 - t0) / reps * 1e3, "gpu_ms_epe": (t2 - t1) / reps * 1e3,
+           "timer": "host perf_counter around the synchronous API call (device field, host result)"}
+    try:
+        from oracle import refpy as R
+        if R.available():
+            f = res.cpu().numpy()
+            t0 = time.perf_counter()
+            R.marching_squares(f, ILT["threshold"], grid.pitch_nm, grid.origin_x_nm, grid.origin_y_nm)
+            t1 = time.perf_counter()
+            R.measure_epe(gauges, radius)
+            t2 = time.perf_counter()
+            out.update({"ref_cpu_ms_contours": (t1 - t0) * 1e3, "ref_cpu_ms_epe": (t2 - t1) * 1e3,
+                        "ref_cores": 1})
+    except Exception as e:  # the reference arm is optional here
+        out["ref_error"] = str(e)[:200]
+    return out
 
 
 def _batched_ilt(ctx, stream, dk, target32, theta0, prm, iters, tiles=8):

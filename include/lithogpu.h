@@ -202,6 +202,15 @@ void lithogpu_contours_destroy(lithogpu_contours* c);
 lithogpu_status lithogpu_measure_epe(lithogpu_contours* c, const double* gauges, int64_t n,
                                      double search_radius_nm, double* epe_nm, uint8_t* open);
 
+/* measure_epe on an arbitrary ContourSet given as loops (loop_start[n_loops+1]
+ * offsets into xs/ys, host or device): segments in loop order as the
+ * reference build_contour_bvh (contour.cpp:170-178), every segment scanned on
+ * the GPU; same records as lithogpu_measure_epe on a marching-squares set. */
+lithogpu_status lithogpu_measure_epe_loops(lithogpu_ctx* ctx, const int64_t* loop_start, int64_t n_loops,
+                                           const double* xs, const double* ys, const double* gauges,
+                                           int64_t n, double search_radius_nm, double* epe_nm,
+                                           uint8_t* open);
+
 /* ---- host-side kernel generation (precompute, not on the timed path) ----
  * Replaces build_tcc + decompose_tcc (imaging.cpp:113-216) with the same
  * semantics via the TCC = Q Q^H factorisation (no dense S x S eigensolve, so

@@ -1833,26 +1833,67 @@ lithogpu_status lithogpu_ilt_get_tiles(lithogpu_ilt* ilt, void* theta, void* mas
 // ===========================================================================
 // contours + EPE: contour_kernels.cuh
 // ===========================================================================
+// Stream-ordered pool allocation (cudaMallocAsync): the contour path runs
+// once per resist image, so its grid-sized scratch must not pay cudaMalloc /
+// cudaFree (milliseconds) on every call.
+struct PoolBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaStream_t s = nullptr;
+  PoolBuf() = default;
+  PoolBuf(const PoolBuf&) = delete;
+  PoolBuf& operator=(const PoolBuf&) = delete;
+  ~PoolBuf() { release(); }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    bytes = 0;
+  }
+  void ensure(size_t b, cudaStream_t st) {
+    if (b <= bytes && st == s) return;
+    release();
+    s = st;
+    if (b == 0) return;
+    static const bool pool_init = [] {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        unsigned long long keep = ~0ull;  // keep freed blocks for reuse
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      return true;
+    }();
+    (void)pool_init;
+    LG_CUDA(cudaMallocAsync(&p, b, s));
+    bytes = b;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
 struct lithogpu_contours {
   lithogpu_ctx* ctx = nullptr;
   lg::CGeo g{};
   long long ne = 0;
   int ncross = 0;
   long long nloops = 0, npts = 0;
-  DevBuf succ, pt, offsets, xs, ys;
+  PoolBuf succ, pt, offsets, xs, ys;
 };
 
 namespace {
-void ms_scan(lithogpu_ctx* ctx, const int* in, int* out, long long n, DevBuf& tmp) {
+void ms_scan(lithogpu_ctx* ctx, const int* in, int* out, long long n, PoolBuf& tmp) {
   size_t tb = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, n, ctx->stream);
-  tmp.ensure(std::max<size_t>(tb, 16));
+  tmp.ensure(std::max<size_t>(tb, 16), ctx->stream);
   cub::DeviceScan::ExclusiveSum(tmp.p, tb, in, out, n, ctx->stream);
 }
-void ms_scan64(lithogpu_ctx* ctx, const int* in, long long* out, long long n, DevBuf& tmp) {
+void ms_scan64(lithogpu_ctx* ctx, const int* in, long long* out, long long n, PoolBuf& tmp) {
   size_t tb = 0;
   cub::DeviceScan::ExclusiveScan(nullptr, tb, in, out, cub::Sum(), 0ll, n, ctx->stream);
-  tmp.ensure(std::max<size_t>(tb, 16));
+  tmp.ensure(std::max<size_t>(tb, 16), ctx->stream);
   cub::DeviceScan::ExclusiveScan(tmp.p, tb, in, out, cub::Sum(), 0ll, n, ctx->stream);
 }
 template <typename T>
@@ -1879,7 +1920,7 @@ lithogpu_status lithogpu_marching_squares(lithogpu_ctx* ctx, const lithogpu_grid
     c->g = lg::CGeo{nx, ny, grid->pitch_nm, grid->origin_x_nm, grid->origin_y_nm, (long long)(nx - 1) * ny};
     c->ne = c->g.nh + (long long)nx * (ny - 1);
     if (nx < 2 || ny < 2) {  // reference :61
-      c->offsets.ensure(sizeof(long long));
+      c->offsets.ensure(sizeof(long long), ctx->stream);
       LG_CUDA(cudaMemsetAsync(c->offsets.p, 0, sizeof(long long), ctx->stream));
       *out = c.release();
       return;
@@ -1887,18 +1928,18 @@ lithogpu_status lithogpu_marching_squares(lithogpu_ctx* ctx, const lithogpu_grid
     const size_t npix = size_t(nx) * ny;
     const double* f = stage_in<double>(ctx, field, LITHOGPU_F64, npix, 0);
     const int nblk = 256;
-    DevBuf part, mm, flags;
-    part.ensure(sizeof(double) * 2 * nblk);
-    mm.ensure(sizeof(double) * 2);
-    flags.ensure(sizeof(int) * 4);
+    PoolBuf part, mm, flags;
+    part.ensure(sizeof(double) * 2 * nblk, ctx->stream);
+    mm.ensure(sizeof(double) * 2, ctx->stream);
+    flags.ensure(sizeof(int) * 4, ctx->stream);
     LG_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int) * 4, ctx->stream));
     int* fl = flags.as<int>();  // [0] non-finite, [1] duplicate edge, [2] broken chain
     lg::k_field_minmax<<<nblk, 256, 0, ctx->stream>>>(f, (long long)npix, part.as<double>(), part.as<double>() + nblk, fl);
     ctx->check_launch();
     lg::k_field_minmax_final<<<1, 32, 0, ctx->stream>>>(part.as<double>(), part.as<double>() + nblk, nblk, mm.as<double>());
     ctx->check_launch();
-    c->succ.ensure(sizeof(int) * c->ne);
-    c->pt.ensure(sizeof(double2) * c->ne);
+    c->succ.ensure(sizeof(int) * c->ne, ctx->stream);
+    c->pt.ensure(sizeof(double2) * c->ne, ctx->stream);
     LG_CUDA(cudaMemsetAsync(c->succ.p, 0xff, sizeof(int) * c->ne, ctx->stream));
     dim3 blk(32, 8), grd(cdiv(nx - 1, 32), cdiv(ny - 1, 8));
     lg::k_ms_cells<<<grd, blk, 0, ctx->stream>>>(c->g, f, threshold, mm.as<double>(), c->succ.as<int>(),
@@ -1910,10 +1951,10 @@ lithogpu_status lithogpu_marching_squares(lithogpu_ctx* ctx, const lithogpu_grid
     if (hf[0]) throw std::invalid_argument("marching_squares: non-finite field");
     if (hf[1]) throw std::runtime_error("marching_squares: inconsistent contour graph");
     // compact the crossing edges in edge order
-    DevBuf flag, pos, tmp, idx;
-    flag.ensure(sizeof(int) * (c->ne + 1));
-    pos.ensure(sizeof(int) * (c->ne + 1));
-    idx.ensure(sizeof(int) * c->ne);
+    PoolBuf flag, pos, tmp, idx;
+    flag.ensure(sizeof(int) * (c->ne + 1), ctx->stream);
+    pos.ensure(sizeof(int) * (c->ne + 1), ctx->stream);
+    idx.ensure(sizeof(int) * c->ne, ctx->stream);
     const int gb = 148 * 8;
     lg::k_ms_flags<<<gb, 256, 0, ctx->stream>>>(c->succ.as<int>(), c->ne, flag.as<int>());
     ctx->check_launch();
@@ -1922,16 +1963,16 @@ lithogpu_status lithogpu_marching_squares(lithogpu_ctx* ctx, const lithogpu_grid
     const int n = read_dev(ctx, pos.as<int>() + c->ne);
     c->ncross = n;
     if (n == 0) {
-      c->offsets.ensure(sizeof(long long));
+      c->offsets.ensure(sizeof(long long), ctx->stream);
       LG_CUDA(cudaMemsetAsync(c->offsets.p, 0, sizeof(long long), ctx->stream));
       LG_CUDA(cudaStreamSynchronize(ctx->stream));
       *out = c.release();
       return;
     }
-    DevBuf cedge, csucc, m0, m1, j0, j1, d0, d1, isst, len, lidx, ptoff;
-    cedge.ensure(sizeof(int) * n);
-    csucc.ensure(sizeof(int) * n);
-    for (DevBuf* b : {&m0, &m1, &j0, &j1, &d0, &d1}) b->ensure(sizeof(int) * n);
+    PoolBuf cedge, csucc, m0, m1, j0, j1, d0, d1, isst, len, lidx, ptoff;
+    cedge.ensure(sizeof(int) * n, ctx->stream);
+    csucc.ensure(sizeof(int) * n, ctx->stream);
+    for (PoolBuf* b : {&m0, &m1, &j0, &j1, &d0, &d1}) b->ensure(sizeof(int) * n, ctx->stream);
     lg::k_ms_compact<<<gb, 256, 0, ctx->stream>>>(c->succ.as<int>(), pos.as<int>(), c->ne, cedge.as<int>(), idx.as<int>());
     ctx->check_launch();
     const int tb = cdiv(n, 256);
@@ -1960,10 +2001,10 @@ lithogpu_status lithogpu_marching_squares(lithogpu_ctx* ctx, const lithogpu_grid
       std::swap(nA, nB);
       std::swap(dA, dB);
     }
-    isst.ensure(sizeof(int) * (n + 1));
-    len.ensure(sizeof(int) * (n + 1));
-    lidx.ensure(sizeof(int) * (n + 1));
-    ptoff.ensure(sizeof(long long) * (n + 1));
+    isst.ensure(sizeof(int) * (n + 1), ctx->stream);
+    len.ensure(sizeof(int) * (n + 1), ctx->stream);
+    lidx.ensure(sizeof(int) * (n + 1), ctx->stream);
+    ptoff.ensure(sizeof(long long) * (n + 1), ctx->stream);
     lg::k_ms_starts<<<tb, 256, 0, ctx->stream>>>(cedge.as<int>(), mA, dA, n, isst.as<int>(), len.as<int>());
     ctx->check_launch();
     LG_CUDA(cudaMemsetAsync(isst.as<int>() + n, 0, sizeof(int), ctx->stream));
@@ -1973,9 +2014,9 @@ lithogpu_status lithogpu_marching_squares(lithogpu_ctx* ctx, const lithogpu_grid
     c->nloops = read_dev(ctx, lidx.as<int>() + n);
     c->npts = read_dev(ctx, ptoff.as<long long>() + n);
     if (c->npts != n) throw std::runtime_error("marching_squares: broken contour chain");
-    c->offsets.ensure(sizeof(long long) * (c->nloops + 1));
-    c->xs.ensure(sizeof(double) * n);
-    c->ys.ensure(sizeof(double) * n);
+    c->offsets.ensure(sizeof(long long) * (c->nloops + 1), ctx->stream);
+    c->xs.ensure(sizeof(double) * n, ctx->stream);
+    c->ys.ensure(sizeof(double) * n, ctx->stream);
     lg::k_ms_offsets<<<tb, 256, 0, ctx->stream>>>(isst.as<int>(), lidx.as<int>(), ptoff.as<long long>(), n,
                                                   c->offsets.as<long long>(), c->npts);
     ctx->check_launch();
@@ -2027,21 +2068,74 @@ lithogpu_status lithogpu_measure_epe(lithogpu_contours* c, const double* gauges,
     ctx->activate();
     const double* gd = stage_in<double>(ctx, gauges, LITHOGPU_F64, size_t(n) * 4, 0);
     const bool dev_e = is_device_ptr(epe_nm), dev_o = is_device_ptr(open);
-    DevBuf eb, ob;
+    PoolBuf eb, ob;
     double* de = epe_nm;
     unsigned char* dob = open;
     if (!dev_e) {
-      eb.ensure(sizeof(double) * n);
+      eb.ensure(sizeof(double) * n, ctx->stream);
       de = eb.as<double>();
     }
     if (!dev_o) {
-      ob.ensure(size_t(n));
+      ob.ensure(size_t(n), ctx->stream);
       dob = ob.as<unsigned char>();
     }
     const bool grid_ok = c->g.nx >= 2 && c->g.ny >= 2;
     lg::k_epe<<<cdiv(n * 32, 256), 256, 0, ctx->stream>>>(
         c->g, grid_ok ? c->succ.as<int>() : nullptr, grid_ok ? c->pt.as<double2>() : nullptr, grid_ok ? c->ncross : 0,
         reinterpret_cast<const lg::Gauge*>(gd), int(n), search_radius_nm, de, dob);
+    ctx->check_launch();
+    if (!dev_e) LG_CUDA(cudaMemcpyAsync(epe_nm, de, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    if (!dev_o) LG_CUDA(cudaMemcpyAsync(open, dob, size_t(n), cudaMemcpyDeviceToHost, ctx->stream));
+    LG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+lithogpu_status lithogpu_measure_epe_loops(lithogpu_ctx* ctx, const int64_t* loop_start, int64_t n_loops,
+                                           const double* xs, const double* ys, const double* gauges,
+                                           int64_t n, double search_radius_nm, double* epe_nm, uint8_t* open) {
+  if (!ctx || n_loops < 0 || n < 0 || (n_loops > 0 && !loop_start) || (n > 0 && (!gauges || !epe_nm || !open))) {
+    g_last_error = "lithogpu_measure_epe_loops: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    if (n == 0) return;
+    ctx->activate();
+    // segments on the host in loop order (cheap: O(points)), then the GPU scan
+    std::vector<int64_t> st(size_t(n_loops) + 1, 0);
+    if (n_loops > 0)
+      LG_CUDA(cudaMemcpy(st.data(), loop_start, sizeof(int64_t) * (n_loops + 1), cudaMemcpyDefault));
+    const int64_t np = n_loops > 0 ? st[n_loops] : 0;
+    std::vector<double> hx(size_t(std::max<int64_t>(np, 1))), hy(hx.size());
+    if (np > 0) {
+      LG_CUDA(cudaMemcpy(hx.data(), xs, sizeof(double) * np, cudaMemcpyDefault));
+      LG_CUDA(cudaMemcpy(hy.data(), ys, sizeof(double) * np, cudaMemcpyDefault));
+    }
+    std::vector<double4> segs;
+    segs.reserve(size_t(np));
+    for (int64_t l = 0; l < n_loops; ++l)
+      for (int64_t i = st[l]; i < st[l + 1]; ++i) {
+        const int64_t j = i + 1 < st[l + 1] ? i + 1 : st[l];
+        segs.push_back(make_double4(hx[i], hy[i], hx[j], hy[j]));
+      }
+    PoolBuf ds, eb, ob;
+    ds.ensure(sizeof(double4) * std::max<size_t>(segs.size(), 1), ctx->stream);
+    if (!segs.empty())
+      LG_CUDA(cudaMemcpyAsync(ds.p, segs.data(), sizeof(double4) * segs.size(), cudaMemcpyHostToDevice, ctx->stream));
+    const double* gd = stage_in<double>(ctx, gauges, LITHOGPU_F64, size_t(n) * 4, 0);
+    const bool dev_e = is_device_ptr(epe_nm), dev_o = is_device_ptr(open);
+    double* de = epe_nm;
+    unsigned char* dob = open;
+    if (!dev_e) {
+      eb.ensure(sizeof(double) * n, ctx->stream);
+      de = eb.as<double>();
+    }
+    if (!dev_o) {
+      ob.ensure(size_t(n), ctx->stream);
+      dob = ob.as<unsigned char>();
+    }
+    lg::k_epe_segments<<<cdiv(n * 32, 256), 256, 0, ctx->stream>>>(
+        ds.as<double4>(), (long long)segs.size(), reinterpret_cast<const lg::Gauge*>(gd), int(n), search_radius_nm,
+        de, dob);
     ctx->check_launch();
     if (!dev_e) LG_CUDA(cudaMemcpyAsync(epe_nm, de, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
     if (!dev_o) LG_CUDA(cudaMemcpyAsync(open, dob, size_t(n), cudaMemcpyDeviceToHost, ctx->stream));

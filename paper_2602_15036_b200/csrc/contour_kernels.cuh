@@ -319,4 +319,44 @@ __global__ void k_epe(CGeo g, const int* __restrict__ succ, const double2* __res
   }
 }
 
+// EPE against an arbitrary segment list (ContourSet not produced by the GPU
+// marching squares): one warp per gauge scans every segment (x0, y0, x1, y1)
+// with the same arithmetic and tie rule as k_epe.
+__global__ void k_epe_segments(const double4* __restrict__ segs, long long ns, const Gauge* __restrict__ gauges,
+                               int ng, double r, double* __restrict__ epe, unsigned char* __restrict__ open) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= ng) return;
+  const Gauge q = gauges[warp];
+  bool have = false;
+  double best = 0.0;
+  if (r > 0.0) {
+    for (long long k = lane; k < ns; k += 32) {
+      const double4 s = segs[k];
+      const double sx = __dadd_rn(s.z, -s.x), sy = __dadd_rn(s.w, -s.y);
+      const double denom = __dadd_rn(__dmul_rn(q.nx, sy), -__dmul_rn(q.ny, sx));
+      if (denom == 0.0) continue;
+      const double rx = __dadd_rn(s.x, -q.x), ry = __dadd_rn(s.y, -q.y);
+      const double t = __ddiv_rn(__dadd_rn(__dmul_rn(rx, sy), -__dmul_rn(ry, sx)), denom);
+      const double u = __ddiv_rn(__dadd_rn(__dmul_rn(rx, q.ny), -__dmul_rn(ry, q.nx)), denom);
+      if (u < 0.0 || u > 1.0 || fabs(t) > r) continue;
+      if (epe_better(t, best, have)) {
+        best = t;
+        have = true;
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_down_sync(0xffffffffu, best, o);
+    const bool oh = __shfl_down_sync(0xffffffffu, have, o);
+    if (oh && epe_better(ob, best, have)) {
+      best = ob;
+      have = true;
+    }
+  }
+  if (lane == 0) {
+    epe[warp] = have ? best : 0.0;
+    open[warp] = have ? 0 : 1;
+  }
+}
+
 }  // namespace lg

@@ -1,8 +1,8 @@
 """GPU: the reference's OWN unmodified C++ test suites (test_imaging,
-test_geometry, test_opc_ai from /root/reference, built by
+test_geometry, test_opc_ai, test_contour from /root/reference, built by
 tests/cpp/build_dropin_tests.sh) linked against the drop-in
-(host/litho_dropin.cpp replaces imaging.cpp + raster.cpp; everything else is
-the reference).  Every TEST_CASE runs its imaging / rasterization on the B200
+(host/litho_dropin.cpp replaces imaging.cpp + raster.cpp and contour.cpp's
+marching_squares / measure_epe; everything else is the reference).  Every TEST_CASE runs its imaging / rasterization on the B200
 through the C ABI, at the reference's own fp64 tolerances."""
 import os
 import subprocess
@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 BIN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp", "_bin")
 
 
-@pytest.mark.parametrize("suite", ["test_imaging", "test_geometry", "test_opc_ai"])
+@pytest.mark.parametrize("suite", ["test_imaging", "test_geometry", "test_opc_ai", "test_contour"])
 def test_reference_suite_on_dropin(suite):
     exe = os.path.join(BIN, suite)
     if not os.path.exists(exe):
