@@ -211,6 +211,18 @@ lithogpu_status lithogpu_measure_epe_loops(lithogpu_ctx* ctx, const int64_t* loo
                                            int64_t n, double search_radius_nm, double* epe_nm,
                                            uint8_t* open);
 
+/* evaluate_epe (opc.cpp:140-151) without leaving the
+ * device: n_masks mask rasters (n_masks x ny x nx, host or device, f32/f64;
+ * e.g. the MEEF probe batches of estimate_meef, opc.cpp:153-202) are imaged
+ * in ONE batched launch sequence on focus stack `focus`, resist-filtered
+ * (gaussian blur sigma_nm), contoured at t_eff (marching_squares) and gauged
+ * (measure_epe) with the same n_gauges gauges {x, y, nx, ny}.  epe_nm / open:
+ * n_masks x n_gauges; resist (nullable): n_masks x ny x nx f64. */
+lithogpu_status lithogpu_evaluate_epe(lithogpu_kernels* ks, int focus, int n_masks, const void* masks,
+                                      lithogpu_dtype mask_dtype, double dose, double sigma_nm, double t_eff,
+                                      const double* gauges, int64_t n_gauges, double search_radius_nm,
+                                      double* epe_nm, uint8_t* open, double* resist);
+
 /* ---- host-side kernel generation (precompute, not on the timed path) ----
  * Replaces build_tcc + decompose_tcc (imaging.cpp:113-216) with the same
  * semantics via the TCC = Q Q^H factorisation (no dense S x S eigensolve, so

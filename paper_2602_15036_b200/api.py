@@ -512,6 +512,35 @@ def measure_epe(contours: ContourSet, gauges, search_radius_nm: float):
     return epe[:n], op[:n].astype(bool)
 
 
+def evaluate_epe(masks, kernels, gauges, dose: float, sigma_nm: float, t_eff: float, search_radius_nm: float,
+                 focus: int = 0, precision: str = "f64", ctx: Optional[Context] = None, want_resist: bool = False):
+    """evaluate_epe (opc.cpp:140-151) on the device for one mask raster or a
+    batch (m, ny, nx) — e.g. the MEEF probe batches of estimate_meef
+    (opc.cpp:153-202): image -> resist_filter -> marching_squares ->
+    measure_epe, imaged in one batched launch sequence.
+    Returns (epe [m, n], open [m, n] bool[, resist [m, ny, nx]])."""
+    dk = _kernels_on_device(kernels, precision, ctx)
+    single = np.ndim(masks) == 2
+    m = np.ascontiguousarray(masks, np.float64)
+    if single:
+        m = m[None]
+    nm = m.shape[0]
+    g = np.ascontiguousarray(gauges, np.float64).reshape(-1, 4)
+    n = g.shape[0]
+    epe = np.zeros((nm, max(n, 1)), np.float64)
+    op = np.zeros((nm, max(n, 1)), np.uint8)
+    res = np.zeros(m.shape, np.float64) if want_resist else None
+    check(lib().lithogpu_evaluate_epe(dk.handle, focus, nm, m.ctypes.data, F64, dose, sigma_nm, t_eff,
+                                      g.ctypes.data if n else None, n, search_radius_nm, epe.ctypes.data,
+                                      op.ctypes.data, res.ctypes.data if want_resist else None))
+    out = (epe[:, :n], op[:, :n].astype(bool))
+    if single:
+        out = (out[0][0], out[1][0])
+    if want_resist:
+        out = out + ((res[0] if single else res),)
+    return out
+
+
 # ---------------------------------------------------------------------------
 # ILT
 # ---------------------------------------------------------------------------

@@ -1905,6 +1905,121 @@ T read_dev(lithogpu_ctx* ctx, const T* p) {
 }
 }  // namespace
 
+// marching squares of a DEVICE f64 field (internal; see lithogpu_marching_squares)
+static std::unique_ptr<lithogpu_contours> ms_build(lithogpu_ctx* ctx, const lithogpu_grid* grid, const double* field,
+                                            double threshold) {
+  const int nx = grid->nx, ny = grid->ny;
+  if (nx <= 0 || ny <= 0) throw std::invalid_argument("marching_squares: empty grid");
+  auto c = std::make_unique<lithogpu_contours>();
+  c->ctx = ctx;
+  c->g = lg::CGeo{nx, ny, grid->pitch_nm, grid->origin_x_nm, grid->origin_y_nm, (long long)(nx - 1) * ny};
+  c->ne = c->g.nh + (long long)nx * (ny - 1);
+  if (nx < 2 || ny < 2) {  // reference :61
+    c->offsets.ensure(sizeof(long long), ctx->stream);
+    LG_CUDA(cudaMemsetAsync(c->offsets.p, 0, sizeof(long long), ctx->stream));
+    return c;
+  }
+  const double* f = field;  // device
+  const size_t npix = size_t(nx) * ny;
+  const int nblk = 256;
+  PoolBuf part, mm, flags;
+  part.ensure(sizeof(double) * 2 * nblk, ctx->stream);
+  mm.ensure(sizeof(double) * 2, ctx->stream);
+  flags.ensure(sizeof(int) * 4, ctx->stream);
+  LG_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int) * 4, ctx->stream));
+  int* fl = flags.as<int>();  // [0] non-finite, [1] duplicate edge, [2] broken chain
+  lg::k_field_minmax<<<nblk, 256, 0, ctx->stream>>>(f, (long long)npix, part.as<double>(), part.as<double>() + nblk, fl);
+  ctx->check_launch();
+  lg::k_field_minmax_final<<<1, 32, 0, ctx->stream>>>(part.as<double>(), part.as<double>() + nblk, nblk, mm.as<double>());
+  ctx->check_launch();
+  c->succ.ensure(sizeof(int) * c->ne, ctx->stream);
+  c->pt.ensure(sizeof(double2) * c->ne, ctx->stream);
+  LG_CUDA(cudaMemsetAsync(c->succ.p, 0xff, sizeof(int) * c->ne, ctx->stream));
+  dim3 blk(32, 8), grd(cdiv(nx - 1, 32), cdiv(ny - 1, 8));
+  lg::k_ms_cells<<<grd, blk, 0, ctx->stream>>>(c->g, f, threshold, mm.as<double>(), c->succ.as<int>(),
+                                             c->pt.as<double2>(), fl + 1);
+  ctx->check_launch();
+  int hf[4];
+  LG_CUDA(cudaMemcpyAsync(hf, fl, sizeof(hf), cudaMemcpyDeviceToHost, ctx->stream));
+  LG_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (hf[0]) throw std::invalid_argument("marching_squares: non-finite field");
+  if (hf[1]) throw std::runtime_error("marching_squares: inconsistent contour graph");
+  // compact the crossing edges in edge order
+  PoolBuf flag, pos, tmp, idx;
+  flag.ensure(sizeof(int) * (c->ne + 1), ctx->stream);
+  pos.ensure(sizeof(int) * (c->ne + 1), ctx->stream);
+  idx.ensure(sizeof(int) * c->ne, ctx->stream);
+  const int gb = 148 * 8;
+  lg::k_ms_flags<<<gb, 256, 0, ctx->stream>>>(c->succ.as<int>(), c->ne, flag.as<int>());
+  ctx->check_launch();
+  LG_CUDA(cudaMemsetAsync(flag.as<int>() + c->ne, 0, sizeof(int), ctx->stream));
+  ms_scan(ctx, flag.as<int>(), pos.as<int>(), c->ne + 1, tmp);
+  const int n = read_dev(ctx, pos.as<int>() + c->ne);
+  c->ncross = n;
+  if (n == 0) {
+    c->offsets.ensure(sizeof(long long), ctx->stream);
+    LG_CUDA(cudaMemsetAsync(c->offsets.p, 0, sizeof(long long), ctx->stream));
+    LG_CUDA(cudaStreamSynchronize(ctx->stream));
+    return c;
+  }
+  PoolBuf cedge, csucc, m0, m1, j0, j1, d0, d1, isst, len, lidx, ptoff;
+  cedge.ensure(sizeof(int) * n, ctx->stream);
+  csucc.ensure(sizeof(int) * n, ctx->stream);
+  for (PoolBuf* b : {&m0, &m1, &j0, &j1, &d0, &d1}) b->ensure(sizeof(int) * n, ctx->stream);
+  lg::k_ms_compact<<<gb, 256, 0, ctx->stream>>>(c->succ.as<int>(), pos.as<int>(), c->ne, cedge.as<int>(), idx.as<int>());
+  ctx->check_launch();
+  const int tb = cdiv(n, 256);
+  lg::k_ms_link<<<tb, 256, 0, ctx->stream>>>(cedge.as<int>(), c->succ.as<int>(), idx.as<int>(), n, csucc.as<int>(),
+                                           m0.as<int>(), fl + 2);
+  ctx->check_launch();
+  if (read_dev(ctx, fl + 2)) throw std::runtime_error("marching_squares: broken contour chain");
+  int rounds = 1;
+  while ((1 << rounds) < n) ++rounds;
+  // cycle minima
+  LG_CUDA(cudaMemcpyAsync(j0.p, csucc.p, sizeof(int) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  int *mA = m0.as<int>(), *mB = m1.as<int>(), *jA = j0.as<int>(), *jB = j1.as<int>();
+  for (int r = 0; r < rounds; ++r) {
+    lg::k_ms_minjump<<<tb, 256, 0, ctx->stream>>>(mA, jA, n, mB, jB);
+    ctx->check_launch();
+    std::swap(mA, mB);
+    std::swap(jA, jB);
+  }
+  // distance to the end of each cycle cut before its start
+  int *nA = jB, *nB = jA, *dA = d0.as<int>(), *dB = d1.as<int>();
+  lg::k_ms_rank_init<<<tb, 256, 0, ctx->stream>>>(csucc.as<int>(), cedge.as<int>(), mA, n, nA, dA);
+  ctx->check_launch();
+  for (int r = 0; r < rounds; ++r) {
+    lg::k_ms_rank_jump<<<tb, 256, 0, ctx->stream>>>(nA, dA, n, nB, dB);
+    ctx->check_launch();
+    std::swap(nA, nB);
+    std::swap(dA, dB);
+  }
+  isst.ensure(sizeof(int) * (n + 1), ctx->stream);
+  len.ensure(sizeof(int) * (n + 1), ctx->stream);
+  lidx.ensure(sizeof(int) * (n + 1), ctx->stream);
+  ptoff.ensure(sizeof(long long) * (n + 1), ctx->stream);
+  lg::k_ms_starts<<<tb, 256, 0, ctx->stream>>>(cedge.as<int>(), mA, dA, n, isst.as<int>(), len.as<int>());
+  ctx->check_launch();
+  LG_CUDA(cudaMemsetAsync(isst.as<int>() + n, 0, sizeof(int), ctx->stream));
+  LG_CUDA(cudaMemsetAsync(len.as<int>() + n, 0, sizeof(int), ctx->stream));
+  ms_scan(ctx, isst.as<int>(), lidx.as<int>(), n + 1, tmp);
+  ms_scan64(ctx, len.as<int>(), ptoff.as<long long>(), n + 1, tmp);
+  c->nloops = read_dev(ctx, lidx.as<int>() + n);
+  c->npts = read_dev(ctx, ptoff.as<long long>() + n);
+  if (c->npts != n) throw std::runtime_error("marching_squares: broken contour chain");
+  c->offsets.ensure(sizeof(long long) * (c->nloops + 1), ctx->stream);
+  c->xs.ensure(sizeof(double) * n, ctx->stream);
+  c->ys.ensure(sizeof(double) * n, ctx->stream);
+  lg::k_ms_offsets<<<tb, 256, 0, ctx->stream>>>(isst.as<int>(), lidx.as<int>(), ptoff.as<long long>(), n,
+                                              c->offsets.as<long long>(), c->npts);
+  ctx->check_launch();
+  lg::k_ms_scatter<<<tb, 256, 0, ctx->stream>>>(cedge.as<int>(), mA, idx.as<int>(), dA, ptoff.as<long long>(),
+                                              c->pt.as<double2>(), n, c->xs.as<double>(), c->ys.as<double>());
+  ctx->check_launch();
+  LG_CUDA(cudaStreamSynchronize(ctx->stream));
+  return c;
+}
+
 lithogpu_status lithogpu_marching_squares(lithogpu_ctx* ctx, const lithogpu_grid* grid, const double* field,
                                           double threshold, lithogpu_contours** out) {
   if (!ctx || !grid || !field || !out) {
@@ -1913,118 +2028,9 @@ lithogpu_status lithogpu_marching_squares(lithogpu_ctx* ctx, const lithogpu_grid
   }
   return guarded([&] {
     ctx->activate();
-    const int nx = grid->nx, ny = grid->ny;
-    if (nx <= 0 || ny <= 0) throw std::invalid_argument("marching_squares: empty grid");
-    auto c = std::make_unique<lithogpu_contours>();
-    c->ctx = ctx;
-    c->g = lg::CGeo{nx, ny, grid->pitch_nm, grid->origin_x_nm, grid->origin_y_nm, (long long)(nx - 1) * ny};
-    c->ne = c->g.nh + (long long)nx * (ny - 1);
-    if (nx < 2 || ny < 2) {  // reference :61
-      c->offsets.ensure(sizeof(long long), ctx->stream);
-      LG_CUDA(cudaMemsetAsync(c->offsets.p, 0, sizeof(long long), ctx->stream));
-      *out = c.release();
-      return;
-    }
-    const size_t npix = size_t(nx) * ny;
-    const double* f = stage_in<double>(ctx, field, LITHOGPU_F64, npix, 0);
-    const int nblk = 256;
-    PoolBuf part, mm, flags;
-    part.ensure(sizeof(double) * 2 * nblk, ctx->stream);
-    mm.ensure(sizeof(double) * 2, ctx->stream);
-    flags.ensure(sizeof(int) * 4, ctx->stream);
-    LG_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int) * 4, ctx->stream));
-    int* fl = flags.as<int>();  // [0] non-finite, [1] duplicate edge, [2] broken chain
-    lg::k_field_minmax<<<nblk, 256, 0, ctx->stream>>>(f, (long long)npix, part.as<double>(), part.as<double>() + nblk, fl);
-    ctx->check_launch();
-    lg::k_field_minmax_final<<<1, 32, 0, ctx->stream>>>(part.as<double>(), part.as<double>() + nblk, nblk, mm.as<double>());
-    ctx->check_launch();
-    c->succ.ensure(sizeof(int) * c->ne, ctx->stream);
-    c->pt.ensure(sizeof(double2) * c->ne, ctx->stream);
-    LG_CUDA(cudaMemsetAsync(c->succ.p, 0xff, sizeof(int) * c->ne, ctx->stream));
-    dim3 blk(32, 8), grd(cdiv(nx - 1, 32), cdiv(ny - 1, 8));
-    lg::k_ms_cells<<<grd, blk, 0, ctx->stream>>>(c->g, f, threshold, mm.as<double>(), c->succ.as<int>(),
-                                                 c->pt.as<double2>(), fl + 1);
-    ctx->check_launch();
-    int hf[4];
-    LG_CUDA(cudaMemcpyAsync(hf, fl, sizeof(hf), cudaMemcpyDeviceToHost, ctx->stream));
-    LG_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (hf[0]) throw std::invalid_argument("marching_squares: non-finite field");
-    if (hf[1]) throw std::runtime_error("marching_squares: inconsistent contour graph");
-    // compact the crossing edges in edge order
-    PoolBuf flag, pos, tmp, idx;
-    flag.ensure(sizeof(int) * (c->ne + 1), ctx->stream);
-    pos.ensure(sizeof(int) * (c->ne + 1), ctx->stream);
-    idx.ensure(sizeof(int) * c->ne, ctx->stream);
-    const int gb = 148 * 8;
-    lg::k_ms_flags<<<gb, 256, 0, ctx->stream>>>(c->succ.as<int>(), c->ne, flag.as<int>());
-    ctx->check_launch();
-    LG_CUDA(cudaMemsetAsync(flag.as<int>() + c->ne, 0, sizeof(int), ctx->stream));
-    ms_scan(ctx, flag.as<int>(), pos.as<int>(), c->ne + 1, tmp);
-    const int n = read_dev(ctx, pos.as<int>() + c->ne);
-    c->ncross = n;
-    if (n == 0) {
-      c->offsets.ensure(sizeof(long long), ctx->stream);
-      LG_CUDA(cudaMemsetAsync(c->offsets.p, 0, sizeof(long long), ctx->stream));
-      LG_CUDA(cudaStreamSynchronize(ctx->stream));
-      *out = c.release();
-      return;
-    }
-    PoolBuf cedge, csucc, m0, m1, j0, j1, d0, d1, isst, len, lidx, ptoff;
-    cedge.ensure(sizeof(int) * n, ctx->stream);
-    csucc.ensure(sizeof(int) * n, ctx->stream);
-    for (PoolBuf* b : {&m0, &m1, &j0, &j1, &d0, &d1}) b->ensure(sizeof(int) * n, ctx->stream);
-    lg::k_ms_compact<<<gb, 256, 0, ctx->stream>>>(c->succ.as<int>(), pos.as<int>(), c->ne, cedge.as<int>(), idx.as<int>());
-    ctx->check_launch();
-    const int tb = cdiv(n, 256);
-    lg::k_ms_link<<<tb, 256, 0, ctx->stream>>>(cedge.as<int>(), c->succ.as<int>(), idx.as<int>(), n, csucc.as<int>(),
-                                               m0.as<int>(), fl + 2);
-    ctx->check_launch();
-    if (read_dev(ctx, fl + 2)) throw std::runtime_error("marching_squares: broken contour chain");
-    int rounds = 1;
-    while ((1 << rounds) < n) ++rounds;
-    // cycle minima
-    LG_CUDA(cudaMemcpyAsync(j0.p, csucc.p, sizeof(int) * n, cudaMemcpyDeviceToDevice, ctx->stream));
-    int *mA = m0.as<int>(), *mB = m1.as<int>(), *jA = j0.as<int>(), *jB = j1.as<int>();
-    for (int r = 0; r < rounds; ++r) {
-      lg::k_ms_minjump<<<tb, 256, 0, ctx->stream>>>(mA, jA, n, mB, jB);
-      ctx->check_launch();
-      std::swap(mA, mB);
-      std::swap(jA, jB);
-    }
-    // distance to the end of each cycle cut before its start
-    int *nA = jB, *nB = jA, *dA = d0.as<int>(), *dB = d1.as<int>();
-    lg::k_ms_rank_init<<<tb, 256, 0, ctx->stream>>>(csucc.as<int>(), cedge.as<int>(), mA, n, nA, dA);
-    ctx->check_launch();
-    for (int r = 0; r < rounds; ++r) {
-      lg::k_ms_rank_jump<<<tb, 256, 0, ctx->stream>>>(nA, dA, n, nB, dB);
-      ctx->check_launch();
-      std::swap(nA, nB);
-      std::swap(dA, dB);
-    }
-    isst.ensure(sizeof(int) * (n + 1), ctx->stream);
-    len.ensure(sizeof(int) * (n + 1), ctx->stream);
-    lidx.ensure(sizeof(int) * (n + 1), ctx->stream);
-    ptoff.ensure(sizeof(long long) * (n + 1), ctx->stream);
-    lg::k_ms_starts<<<tb, 256, 0, ctx->stream>>>(cedge.as<int>(), mA, dA, n, isst.as<int>(), len.as<int>());
-    ctx->check_launch();
-    LG_CUDA(cudaMemsetAsync(isst.as<int>() + n, 0, sizeof(int), ctx->stream));
-    LG_CUDA(cudaMemsetAsync(len.as<int>() + n, 0, sizeof(int), ctx->stream));
-    ms_scan(ctx, isst.as<int>(), lidx.as<int>(), n + 1, tmp);
-    ms_scan64(ctx, len.as<int>(), ptoff.as<long long>(), n + 1, tmp);
-    c->nloops = read_dev(ctx, lidx.as<int>() + n);
-    c->npts = read_dev(ctx, ptoff.as<long long>() + n);
-    if (c->npts != n) throw std::runtime_error("marching_squares: broken contour chain");
-    c->offsets.ensure(sizeof(long long) * (c->nloops + 1), ctx->stream);
-    c->xs.ensure(sizeof(double) * n, ctx->stream);
-    c->ys.ensure(sizeof(double) * n, ctx->stream);
-    lg::k_ms_offsets<<<tb, 256, 0, ctx->stream>>>(isst.as<int>(), lidx.as<int>(), ptoff.as<long long>(), n,
-                                                  c->offsets.as<long long>(), c->npts);
-    ctx->check_launch();
-    lg::k_ms_scatter<<<tb, 256, 0, ctx->stream>>>(cedge.as<int>(), mA, idx.as<int>(), dA, ptoff.as<long long>(),
-                                                  c->pt.as<double2>(), n, c->xs.as<double>(), c->ys.as<double>());
-    ctx->check_launch();
-    LG_CUDA(cudaStreamSynchronize(ctx->stream));
-    *out = c.release();
+    if (grid->nx <= 0 || grid->ny <= 0) throw std::invalid_argument("marching_squares: empty grid");
+    const double* f = stage_in<double>(ctx, field, LITHOGPU_F64, size_t(grid->nx) * grid->ny, 0);
+    *out = ms_build(ctx, grid, f, threshold).release();
   });
 }
 
@@ -2056,6 +2062,17 @@ lithogpu_status lithogpu_contours_get(const lithogpu_contours* c, int64_t* loop_
 
 void lithogpu_contours_destroy(lithogpu_contours* c) { delete c; }
 
+// EPE of DEVICE gauges into DEVICE outputs (internal)
+static void epe_run(const lithogpu_contours* c, const double* gauges_dev, int64_t n, double radius, double* epe_dev,
+             unsigned char* open_dev) {
+  if (n == 0) return;
+  const bool grid_ok = c->g.nx >= 2 && c->g.ny >= 2;
+  lg::k_epe<<<cdiv(n * 32, 256), 256, 0, c->ctx->stream>>>(
+      c->g, grid_ok ? c->succ.as<int>() : nullptr, grid_ok ? c->pt.as<double2>() : nullptr, grid_ok ? c->ncross : 0,
+      reinterpret_cast<const lg::Gauge*>(gauges_dev), int(n), radius, epe_dev, open_dev);
+  c->ctx->check_launch();
+}
+
 lithogpu_status lithogpu_measure_epe(lithogpu_contours* c, const double* gauges, int64_t n, double search_radius_nm,
                                      double* epe_nm, uint8_t* open) {
   if (!c || (n > 0 && (!gauges || !epe_nm || !open)) || n < 0) {
@@ -2079,11 +2096,7 @@ lithogpu_status lithogpu_measure_epe(lithogpu_contours* c, const double* gauges,
       ob.ensure(size_t(n), ctx->stream);
       dob = ob.as<unsigned char>();
     }
-    const bool grid_ok = c->g.nx >= 2 && c->g.ny >= 2;
-    lg::k_epe<<<cdiv(n * 32, 256), 256, 0, ctx->stream>>>(
-        c->g, grid_ok ? c->succ.as<int>() : nullptr, grid_ok ? c->pt.as<double2>() : nullptr, grid_ok ? c->ncross : 0,
-        reinterpret_cast<const lg::Gauge*>(gd), int(n), search_radius_nm, de, dob);
-    ctx->check_launch();
+    epe_run(c, gd, n, search_radius_nm, de, dob);
     if (!dev_e) LG_CUDA(cudaMemcpyAsync(epe_nm, de, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
     if (!dev_o) LG_CUDA(cudaMemcpyAsync(open, dob, size_t(n), cudaMemcpyDeviceToHost, ctx->stream));
     LG_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -2140,5 +2153,73 @@ lithogpu_status lithogpu_measure_epe_loops(lithogpu_ctx* ctx, const int64_t* loo
     if (!dev_e) LG_CUDA(cudaMemcpyAsync(epe_nm, de, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
     if (!dev_o) LG_CUDA(cudaMemcpyAsync(open, dob, size_t(n), cudaMemcpyDeviceToHost, ctx->stream));
     LG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+// ---- evaluate_epe (opc.cpp:140-151) fused on the device ------------------
+namespace {
+template <typename T>
+void evaluate_epe_impl(lithogpu_kernels* ks, int focus, int nm, const void* masks, lithogpu_dtype mdt, double dose,
+                       double sigma, double t_eff, const double* gauges, int64_t n, double radius, double* epe_nm,
+                       uint8_t* open, double* resist) {
+  Plan<T>& P = ks->p<T>();
+  lithogpu_ctx* ctx = ks->ctx;
+  const long long NN = (long long)P.g.ax.N * P.g.ay.N;
+  const T* m = stage_in<T>(ctx, masks, mdt, size_t(nm) * NN, 0);
+  P.set_sigma(sigma);
+  P.forward(m, NN, nm, T(dose), false, true);  // all tiles in one launch sequence (blockIdx.z)
+  PoolBuf fullR, r64, gd, eb, ob;
+  fullR.ensure(sizeof(T) * size_t(nm) * P.F * NN, ctx->stream);
+  P.template out_rows<T>(false, true, nullptr, fullR.as<T>(), nullptr, (long long)P.F * NN, T(t_eff), nm);
+  if (n > 0) {
+    gd.ensure(sizeof(double) * 4 * n, ctx->stream);
+    LG_CUDA(cudaMemcpyAsync(gd.p, gauges, sizeof(double) * 4 * n, cudaMemcpyDefault, ctx->stream));
+    eb.ensure(sizeof(double) * n * nm, ctx->stream);
+    ob.ensure(size_t(n) * nm, ctx->stream);
+  }
+  r64.ensure(sizeof(double) * NN, ctx->stream);
+  const lithogpu_grid grid = ks->grid;
+  for (int t = 0; t < nm; ++t) {
+    const T* rt = fullR.as<T>() + (size_t(t) * P.F + focus) * NN;
+    const double* f64;
+    if constexpr (std::is_same<T, double>::value) {
+      f64 = rt;
+    } else {
+      convert_dev(ctx, rt, r64.as<double>(), size_t(NN));
+      f64 = r64.as<double>();
+    }
+    if (resist)
+      LG_CUDA(cudaMemcpyAsync(resist + size_t(t) * NN, f64, sizeof(double) * NN, cudaMemcpyDefault, ctx->stream));
+    auto c = ms_build(ctx, &grid, f64, t_eff);
+    if (n > 0) epe_run(c.get(), gd.as<double>(), n, radius, eb.as<double>() + size_t(t) * n,
+                       ob.as<unsigned char>() + size_t(t) * n);
+  }
+  if (n > 0) {
+    LG_CUDA(cudaMemcpyAsync(epe_nm, eb.p, sizeof(double) * n * nm, cudaMemcpyDefault, ctx->stream));
+    LG_CUDA(cudaMemcpyAsync(open, ob.p, size_t(n) * nm, cudaMemcpyDefault, ctx->stream));
+  }
+  LG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+}  // namespace
+
+lithogpu_status lithogpu_evaluate_epe(lithogpu_kernels* ks, int focus, int n_masks, const void* masks,
+                                      lithogpu_dtype mask_dtype, double dose, double sigma_nm, double t_eff,
+                                      const double* gauges, int64_t n_gauges, double search_radius_nm,
+                                      double* epe_nm, uint8_t* open, double* resist) {
+  if (!ks || !masks || n_masks <= 0 || n_gauges < 0 || (n_gauges > 0 && (!gauges || !epe_nm || !open))) {
+    g_last_error = "lithogpu_evaluate_epe: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    if (focus < 0 || focus >= ks->F) throw UsageError("lithogpu_evaluate_epe: focus index out of range");
+    if (sigma_nm < 0) throw std::invalid_argument("gaussian_blur: negative sigma");
+    dtype_size(mask_dtype);
+    ks->ctx->activate();
+    if (ks->precision == LITHOGPU_F32)
+      evaluate_epe_impl<float>(ks, focus, n_masks, masks, mask_dtype, dose, sigma_nm, t_eff, gauges, n_gauges,
+                               search_radius_nm, epe_nm, open, resist);
+    else
+      evaluate_epe_impl<double>(ks, focus, n_masks, masks, mask_dtype, dose, sigma_nm, t_eff, gauges, n_gauges,
+                                search_radius_nm, epe_nm, open, resist);
   });
 }

@@ -121,3 +121,41 @@ def test_contour_edge_cases(ctx):
         L.marching_squares(openf, g, 0.5, ctx)
     with pytest.raises(RuntimeError):
         R.marching_squares(openf, 0.5)
+
+
+def test_evaluate_epe_fused_batch(ctx):
+    """evaluate_epe (opc.cpp:140-151) on the device for a batch of masks (MEEF
+    probe style): bit-identical to the unfused GPU steps, and equal to the
+    reference pipeline (image_socs -> gaussian_blur -> marching_squares ->
+    measure_epe, oracle/_ref) to fp64 FFT rounding."""
+    from paper_2602_15036_b200 import layouts as LY
+    n = 192
+    grid = L.Grid(n, n, 1.0)
+    base = L.rasterize_layer(LY.line_space_contacts(n, n, seed=8), grid, 1.0, ctx)
+    base[:16, :] = base[-16:, :] = 0.0
+    base[:, :16] = base[:, -16:] = 0.0
+    masks = np.stack([base, np.roll(base, 1, axis=1), np.roll(base, -2, axis=0)])
+    model = L.OpticalModel(source=L.make_annular_source(0.4, 0.8, 21))
+    ks = L.build_socs_kernels(model, grid, [-40.0, 0.0, 40.0], k_fixed=6)
+    rng = np.random.default_rng(21)
+    k = 400
+    ang = rng.choice([0.0, np.pi / 2, np.pi, 1.5 * np.pi], k)
+    gauges = np.column_stack([rng.uniform(20, n - 20, k), rng.uniform(20, n - 20, k), np.cos(ang), np.sin(ang)])
+    dk = L.DeviceKernels(ks, "f64", ctx)
+    epe, op, res = L.evaluate_epe(masks, dk, gauges, 1.0, 2.0, 0.25, 12.0, focus=1, want_resist=True)
+    assert epe.shape == (3, k) and res.shape == (3, n, n)
+    for t in range(3):
+        r1 = np.asarray(dk.image(masks[t], focus=1, sigma_nm=2.0, want=("resist",))["resist"])
+        assert np.array_equal(res[t], r1)
+        cs = L.marching_squares(r1, grid, 0.25, ctx)
+        e1, o1 = L.measure_epe(cs, gauges, 12.0)
+        assert np.array_equal(epe[t], e1) and np.array_equal(op[t], o1)
+        # reference pipeline
+        I = R.image_socs(masks[t], ks.weights[1], ks.support, ks.values[1])
+        rr = R.gaussian_blur(I, 2.0, 1.0)
+        assert np.abs(rr - r1).max() <= 1e-10 * np.abs(rr).max()
+        R.marching_squares(rr, 0.25)
+        re, ro = R.measure_epe(gauges, 12.0)
+        assert np.array_equal(ro, op[t])
+        assert np.abs(re - epe[t]).max() < 1e-6
+    assert op.sum() < op.size  # most gauges see an edge
