@@ -245,6 +245,21 @@ lithogpu_status lithogpu_socs_kernels(int nx, int ny, double pitch_nm, double wa
                                       int max_order, int* out_order, double* out_captured,
                                       double* out_weights, double* out_values);
 
+/* GPU kernel generation: lithogpu_socs_kernels for
+ * n_focus focus planes in one call (fp64; cuBLAS Gram + cuSOLVER eigensolve
+ * + cuBLAS kernel assembly).  Same support, ordering, truncation and phase
+ * rules; eigenvectors of degenerate eigenvalues may differ by a unitary mix,
+ * which leaves the full image unchanged.  Outputs per focus f:
+ * out_order[f], out_captured[f] (nullable), out_weights[f*max_order + k],
+ * out_values[(f*max_order + k)*n_support*2 ..] (re, im).  Error text:
+ * lithogpu_last_error(). */
+lithogpu_status lithogpu_socs_kernels_gpu(lithogpu_ctx* ctx, int nx, int ny, double pitch_nm,
+                                          double wavelength_nm, double na, int high_na,
+                                          const double* source_xyw, int n_source, int n_focus,
+                                          const double* focus_nm, int n_support, const int32_t* support,
+                                          int k_fixed, double energy_floor, int max_order, int* out_order,
+                                          double* out_captured, double* out_weights, double* out_values);
+
 #ifdef __cplusplus
 }
 #endif

@@ -81,6 +81,9 @@ _SIGS = {
                                              _vp]),
     "lithogpu_evaluate_epe": (C.c_int, [_vp, C.c_int, C.c_int, _vp, C.c_int, C.c_double, C.c_double, C.c_double,
                                         _vp, C.c_int64, C.c_double, _vp, _vp, _vp]),
+    "lithogpu_socs_kernels_gpu": (C.c_int, [_vp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int,
+                                            _vp, C.c_int, C.c_int, _vp, C.c_int, _vp, C.c_int, C.c_double, C.c_int,
+                                            _vp, _vp, _vp, _vp]),
     "lithogpu_source_annular": (C.c_int, [C.c_double, C.c_double, C.c_int, C.POINTER(C.c_int), _vp]),
     "lithogpu_tcc_support": (C.c_int, [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                        C.c_double, C.POINTER(C.c_int), _vp]),

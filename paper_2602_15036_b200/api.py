@@ -140,16 +140,41 @@ def tcc_support(model: OpticalModel, grid: Grid) -> np.ndarray:
 
 
 def build_socs_kernels(model: OpticalModel, grid: Grid, focus_nm: Sequence[float] = (0.0,),
-                       k_fixed: int = 0, energy_floor: float = 0.995) -> SocsKernelSet:
+                       k_fixed: int = 0, energy_floor: float = 0.995, backend: str = "host",
+                       ctx: Optional["Context"] = None) -> SocsKernelSet:
     """build_tcc + decompose_tcc (imaging.cpp:113-216) for each focus plane,
-    via the TCC = Q Q^H factorisation (host, fp64).  All stacks are padded to
-    the same order K (the max over foci; missing kernels have weight 0)."""
+    via the TCC = Q Q^H factorisation (fp64).  backend "host" (OpenMP, Jacobi
+    eigensolve) or "gpu" (cuBLAS Gram + cuSOLVER eigensolve, all foci in one
+    call).  All stacks are padded to the same order K (the max over foci;
+    missing kernels have weight 0)."""
     support = tcc_support(model, grid)
     S = len(support)
     if S == 0:
         raise ValueError("decompose_tcc: empty support")
     src = np.ascontiguousarray(model.source, np.float64)
     cap = k_fixed if k_fixed > 0 else len(src)
+    if backend == "gpu":
+        ctx = ctx or default_context()
+        nf = len(focus_nm)
+        foc = np.ascontiguousarray(focus_nm, np.float64)
+        order = np.zeros(nf, np.int32)
+        capd = np.zeros(nf)
+        w = np.zeros((nf, cap))
+        v = np.zeros((nf, cap, S, 2))
+        check(lib().lithogpu_socs_kernels_gpu(ctx.handle, grid.nx, grid.ny, grid.pitch_nm, model.wavelength_nm,
+                                              model.na, int(model.high_na_defocus), src.ctypes.data, len(src), nf,
+                                              foc.ctypes.data, S, support.ctypes.data, int(k_fixed),
+                                              float(energy_floor), cap, order.ctypes.data, capd.ctypes.data,
+                                              w.ctypes.data, v.ctypes.data))
+        K = int(order.max())
+        V = v[:, :K, :, 0] + 1j * v[:, :K, :, 1]
+        W = w[:, :K].copy()
+        for f in range(nf):  # padding kernels of lower-rank stacks: weight 0
+            W[f, order[f]:] = 0.0
+            V[f, order[f]:] = 0.0
+        return SocsKernelSet(grid, list(focus_nm), W, support, V, list(capd))
+    if backend != "host":
+        raise ValueError("build_socs_kernels: backend must be 'host' or 'gpu'")
     ws, vs, caps = [], [], []
     for f in focus_nm:
         K = C.c_int()

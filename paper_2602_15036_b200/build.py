@@ -18,11 +18,11 @@ OBJ = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU_SOURCES = ["csrc/capi.cu", "csrc/fast_rows.cu", "csrc/fast_cols.cu"]
+CU_SOURCES = ["csrc/capi.cu", "csrc/fast_rows.cu", "csrc/fast_cols.cu", "csrc/kernelgen.cu"]
 CPP_SOURCES = ["host/socs_kernels.cpp"]
 DEPS = ["csrc/fft.cuh", "csrc/geom.h", "csrc/socs_kernels.cuh", "csrc/raster_kernels.cuh",
         "csrc/util_kernels.cuh", "csrc/fftr.cuh", "csrc/socs_fast.h", "csrc/socs_fast.cuh",
-        "csrc/fast_common.cuh", "../include/lithogpu.h"]
+        "csrc/fast_common.cuh", "csrc/contour_kernels.cuh", "../include/lithogpu.h"]
 
 
 def _newer(target, sources):
@@ -61,7 +61,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             if verbose:
                 sys.stderr.write(r.stderr)
     if force or jobs or not os.path.exists(OUT):
-        _run([NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lgomp", "-lcudart"])
+        _run([NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lgomp", "-lcudart", "-lcublas", "-lcusolver"])
     return OUT
 
 

@@ -2223,3 +2223,11 @@ lithogpu_status lithogpu_evaluate_epe(lithogpu_kernels* ks, int focus, int n_mas
                                 search_radius_nm, epe_nm, open, resist);
   });
 }
+
+// ---- internal hooks for the other translation units (kernelgen.cu) --------
+namespace lg_internal {
+cudaStream_t ctx_stream(lithogpu_ctx* ctx) { return ctx->stream; }
+void ctx_activate(lithogpu_ctx* ctx) { ctx->activate(); }
+void ctx_count_launch(lithogpu_ctx* ctx) { ctx->check_launch(); }
+void set_error(const char* msg) { g_last_error = msg ? msg : ""; }
+}  // namespace lg_internal

@@ -230,3 +230,43 @@ def test_ilt_stored_fields_bit_identical(ctx, monkeypatch):
         solver.close()
     assert np.array_equal(out[0][0], out[1][0])
     assert np.array_equal(out[0][1], out[1][1])
+
+
+@pytest.mark.parametrize("n,K,foci", [(256, 12, (0.0,)), (256, 0, (-40.0, 0.0, 40.0)), (2048, 16, (0.0, 40.0))])
+def test_gpu_kernel_generation_vs_host(ctx, n, K, foci):
+    """GPU Abbe-SVD (cuBLAS + cuSOLVER) against the host
+    generator: same eigenvalues, eigenvectors of the TCC with the reference
+    phase rule, and (full rank) the same image."""
+    model = euv(21)
+    grid = L.Grid(n, n, 1.0)
+    host = L.build_socs_kernels(model, grid, list(foci), k_fixed=K)
+    gpu = L.build_socs_kernels(model, grid, list(foci), k_fixed=K, backend="gpu", ctx=ctx)
+    assert np.array_equal(host.support, gpu.support)
+    assert gpu.weights.shape == host.weights.shape
+    assert np.abs(gpu.weights - host.weights).max() <= 1e-10 * host.weights.max()
+    S = len(host.support)
+    src = np.asarray(model.source)
+    fc = model.na / model.wavelength_nm
+    fx = host.support[:, 0] / (n * 1.0)
+    fy = host.support[:, 1] / (n * 1.0)
+    for f, foc in enumerate(foci):
+        # Q[i][s] = sqrt(w_s) P(f_i + s fc)
+        gx = fx[:, None] + src[None, :, 0] * fc
+        gy = fy[:, None] + src[None, :, 1] * fc
+        f2 = gx ** 2 + gy ** 2
+        Q = np.where(f2 <= fc * fc, np.exp(-1j * np.pi * model.wavelength_nm * foc * f2), 0.0) * np.sqrt(src[:, 2])
+        for k in range(min(4, gpu.weights.shape[1])):
+            u, lam = gpu.values[f, k], gpu.weights[f, k]
+            if lam == 0:
+                continue
+            r = Q @ (Q.conj().T @ u) - lam * u
+            assert np.abs(r).max() <= 1e-9 * lam * np.abs(u).max()
+            i = int(np.argmax(np.abs(u)))
+            assert abs(u[i].imag) <= 1e-12 * abs(u[i]) and u[i].real > 0
+    if n == 256 and K == 0:  # energy-floor truncation: images agree
+        rng = np.random.default_rng(4)
+        mask = rng.random((n, n))
+        for f in range(len(foci)):
+            a = O.image_socs(mask, host.weights[f], host.support, host.values[f])
+            b = O.image_socs(mask, gpu.weights[f], gpu.support, gpu.values[f])
+            assert rel_linf(b, a) < 1e-6
