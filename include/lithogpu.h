@@ -245,6 +245,19 @@ lithogpu_status lithogpu_socs_kernels(int nx, int ny, double pitch_nm, double wa
                                       int max_order, int* out_order, double* out_captured,
                                       double* out_weights, double* out_values);
 
+/* ---- AIMG tile I/O --------------------------------
+ * write_aimg (io.cpp:317-330), byte-identical files: "AIMG", u32 nx, u32 ny,
+ * f64 pitch, row-major f64 payload (origin not stored, io.cpp:346).  values:
+ * n_tiles x ny x nx of `dtype` (host or device; F32/U8 become f64), one path
+ * per tile.  Device tiles go through a pinned double buffer: the D2H copy of
+ * tile t+1 overlaps the file write of tile t. */
+lithogpu_status lithogpu_write_aimg(lithogpu_ctx* ctx, const lithogpu_grid* grid, int n_tiles,
+                                    const char* const* paths, const void* values, lithogpu_dtype dtype);
+/* read_aimg (io.cpp:332-350): header into nx/ny/pitch; values (host or device
+ * f64, nx*ny; NULL = header only).  Reference error messages. */
+lithogpu_status lithogpu_read_aimg(lithogpu_ctx* ctx, const char* path, int* nx, int* ny, double* pitch_nm,
+                                   double* values);
+
 /* GPU kernel generation: lithogpu_socs_kernels for
  * n_focus focus planes in one call (fp64; cuBLAS Gram + cuSOLVER eigensolve
  * + cuBLAS kernel assembly).  Same support, ordering, truncation and phase

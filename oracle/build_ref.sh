@@ -14,8 +14,9 @@ if [ ! -d "$REF/src/core" ]; then
   exit 0
 fi
 mkdir -p "$OUT/obj"
-SRCS="geometry bvh boolean raster imaging ai contour segment mrc"
-CXXFLAGS="-O2 -std=c++20 -fPIC -fopenmp -I$HERE/shim -I$REF/src -I$REF/src/core"
+SRCS="geometry bvh boolean raster imaging ai contour segment mrc io"
+JSON_INC="${LITHO_JSON_INC:-/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann}"
+CXXFLAGS="-O2 -std=c++20 -fPIC -fopenmp -I$HERE/shim -I$REF/src -I$REF/src/core -I$JSON_INC"
 pids=()
 for s in $SRCS; do
   g++ $CXXFLAGS -c "$REF/src/core/$s.cpp" -o "$OUT/obj/$s.o" & pids+=($!)

@@ -22,6 +22,7 @@
 #include "core/ai.hpp"
 #include "core/boolean.hpp"
 #include "core/contour.hpp"
+#include "core/io.hpp"
 #include "core/imaging.hpp"
 #include "core/raster.hpp"
 
@@ -415,6 +416,25 @@ int ref_measure_epe(const double* gauges, int64_t n, double radius, double* epe,
       epe[i] = recs[i].epe_nm;
       open[i] = recs[i].open ? 1 : 0;
     }
+  });
+}
+
+// write_aimg / read_aimg (io.cpp:317-350)
+int ref_write_aimg(const char* path, int nx, int ny, double pitch, const double* values) {
+  return guarded([&] {
+    litho::write_aimg(path, make_grid(nx, ny, pitch, 0, 0), std::vector<double>(values, values + size_t(nx) * ny));
+  });
+}
+
+int ref_read_aimg(const char* path, int* nx, int* ny, double* pitch, double* values, int64_t cap) {
+  return guarded([&] {
+    litho::Grid g;
+    std::vector<double> v;
+    litho::read_aimg(path, g, v);
+    *nx = g.nx;
+    *ny = g.ny;
+    *pitch = g.pitch_nm;
+    if (values && int64_t(v.size()) <= cap) std::memcpy(values, v.data(), v.size() * sizeof(double));
   });
 }
 

@@ -241,3 +241,20 @@ def measure_epe(gauges, radius):
     _check(lib().ref_measure_epe(_p(g, C.c_double), C.c_int64(n), C.c_double(radius), _p(epe, C.c_double),
                                  _p(op, C.c_uint8)))
     return epe[:n], op[:n].astype(bool)
+
+
+def write_aimg(path, values, pitch=1.0):
+    """reference write_aimg (io.cpp:317-330)."""
+    v = np.ascontiguousarray(values, np.float64)
+    ny, nx = v.shape
+    _check(lib().ref_write_aimg(path.encode(), nx, ny, C.c_double(pitch), _p(v, C.c_double)))
+
+
+def read_aimg(path, cap=1 << 26):
+    """reference read_aimg (io.cpp:332-350): (nx, ny, pitch, values)."""
+    nx, ny, p = C.c_int(), C.c_int(), C.c_double()
+    _check(lib().ref_read_aimg(path.encode(), C.byref(nx), C.byref(ny), C.byref(p), None, C.c_int64(0)))
+    out = np.zeros((ny.value, nx.value))
+    _check(lib().ref_read_aimg(path.encode(), C.byref(nx), C.byref(ny), C.byref(p), _p(out, C.c_double),
+                               C.c_int64(out.size)))
+    return nx.value, ny.value, p.value, out

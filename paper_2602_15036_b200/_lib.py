@@ -84,6 +84,9 @@ _SIGS = {
     "lithogpu_socs_kernels_gpu": (C.c_int, [_vp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int,
                                             _vp, C.c_int, C.c_int, _vp, C.c_int, _vp, C.c_int, C.c_double, C.c_int,
                                             _vp, _vp, _vp, _vp]),
+    "lithogpu_write_aimg": (C.c_int, [_vp, C.POINTER(Grid), C.c_int, _vp, _vp, C.c_int]),
+    "lithogpu_read_aimg": (C.c_int, [_vp, C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_double),
+                                     _vp]),
     "lithogpu_source_annular": (C.c_int, [C.c_double, C.c_double, C.c_int, C.POINTER(C.c_int), _vp]),
     "lithogpu_tcc_support": (C.c_int, [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                        C.c_double, C.POINTER(C.c_int), _vp]),

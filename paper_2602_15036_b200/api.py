@@ -567,6 +567,33 @@ def evaluate_epe(masks, kernels, gauges, dose: float, sigma_nm: float, t_eff: fl
 
 
 # ---------------------------------------------------------------------------
+# AIMG tile I/O (reference io.hpp:39-43 / io.cpp:317-350)
+# ---------------------------------------------------------------------------
+def write_aimg(paths, grid: Grid, values, ctx: Optional[Context] = None) -> None:
+    """write_aimg for one image (path str, (ny, nx)) or a batch of tiles
+    (list of paths, (t, ny, nx)); numpy or CUDA tensors (f32/f64).  Device
+    tiles stream through a pinned double buffer."""
+    ctx = ctx or default_context()
+    single = isinstance(paths, (str, bytes))
+    plist = [paths] if single else list(paths)
+    ptr, dt, keep = _buf(values)
+    arr = (C.c_char_p * len(plist))(*[p.encode() if isinstance(p, str) else p for p in plist])
+    g = grid.c()
+    check(lib().lithogpu_write_aimg(ctx.handle, C.byref(g), len(plist), C.cast(arr, C.c_void_p), ptr, dt))
+
+
+def read_aimg(path: str, ctx: Optional[Context] = None):
+    """read_aimg: (Grid (origin 0, as the reference), values (ny, nx) f64)."""
+    ctx = ctx or default_context()
+    nx, ny, p = C.c_int(), C.c_int(), C.c_double()
+    check(lib().lithogpu_read_aimg(ctx.handle, path.encode(), C.byref(nx), C.byref(ny), C.byref(p), None))
+    out = np.empty((ny.value, nx.value), np.float64)
+    check(lib().lithogpu_read_aimg(ctx.handle, path.encode(), C.byref(nx), C.byref(ny), C.byref(p),
+                                   out.ctypes.data))
+    return Grid(nx.value, ny.value, p.value), out
+
+
+# ---------------------------------------------------------------------------
 # ILT
 # ---------------------------------------------------------------------------
 @dataclass

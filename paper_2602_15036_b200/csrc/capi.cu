@@ -124,6 +124,20 @@ struct lithogpu_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   long long launches = 0;
+  // pinned double buffer for tile I/O (lithogpu_write_aimg)
+  void* pinned[2] = {nullptr, nullptr};
+  size_t pinned_bytes = 0;
+  void pinned_ensure(size_t b) {
+    if (b <= pinned_bytes) return;
+    for (auto& p : pinned) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+    }
+    pinned_bytes = 0;
+    for (auto& p : pinned) LG_CUDA(cudaMallocHost(&p, b));
+    pinned_bytes = b;
+  }
+
   std::vector<std::unique_ptr<DevBuf>> scratch;  // staging pool (per call slots)
   DevBuf raster_tmp;
   std::unordered_map<const void*, int> smem_set;
@@ -181,6 +195,8 @@ struct lithogpu_ctx {
       cudaEventDestroy(r.b);
     }
     for (auto e : pool) cudaEventDestroy(e);
+    for (auto& p : pinned)
+      if (p) cudaFreeHost(p);
   }
 
   DevBuf& slot(size_t i) {
@@ -2231,3 +2247,110 @@ void ctx_activate(lithogpu_ctx* ctx) { ctx->activate(); }
 void ctx_count_launch(lithogpu_ctx* ctx) { ctx->check_launch(); }
 void set_error(const char* msg) { g_last_error = msg ? msg : ""; }
 }  // namespace lg_internal
+
+// ---- AIMG tile I/O (io.cpp:317-350) -----------------
+lithogpu_status lithogpu_write_aimg(lithogpu_ctx* ctx, const lithogpu_grid* grid, int n_tiles,
+                                    const char* const* paths, const void* values, lithogpu_dtype dtype) {
+  if (!ctx || !grid || !paths || !values || n_tiles < 0) {
+    g_last_error = "lithogpu_write_aimg: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    const size_t n = size_t(grid->nx) * size_t(grid->ny);
+    const size_t es = dtype_size(dtype);
+    if (grid->nx <= 0 || grid->ny <= 0) throw std::invalid_argument("write_aimg: size mismatch");
+    ctx->activate();
+    const bool dev = is_device_ptr(values);
+    if (dev) ctx->pinned_ensure(n * sizeof(double));
+    DevBuf conv;
+    // tile t: D2H (converted to f64 on the device) into pinned buffer t%2; the
+    // host writes tile t while tile t+1's copy is in flight
+    cudaEvent_t done[2];
+    LG_CUDA(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
+    LG_CUDA(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
+    struct Ev {
+      cudaEvent_t* e;
+      ~Ev() {
+        cudaEventDestroy(e[0]);
+        cudaEventDestroy(e[1]);
+      }
+    } guard{done};
+    auto enqueue = [&](int t) {
+      const char* src = static_cast<const char*>(values) + size_t(t) * n * es;
+      void* dst = ctx->pinned[t & 1];
+      if (dtype == LITHOGPU_F64) {
+        LG_CUDA(cudaMemcpyAsync(dst, src, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+      } else {
+        conv.ensure(n * sizeof(double));
+        convert_from(ctx, src, dtype, conv.as<double>(), n);
+        LG_CUDA(cudaMemcpyAsync(dst, conv.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+      }
+      LG_CUDA(cudaEventRecord(done[t & 1], ctx->stream));
+    };
+    std::vector<double> host_tile;
+    if (dev && n_tiles > 0) enqueue(0);
+    for (int t = 0; t < n_tiles; ++t) {
+      const double* payload;
+      if (dev) {
+        LG_CUDA(cudaEventSynchronize(done[t & 1]));
+        if (t + 1 < n_tiles) enqueue(t + 1);  // overlaps the file write below
+        payload = static_cast<const double*>(ctx->pinned[t & 1]);
+      } else if (dtype == LITHOGPU_F64) {
+        payload = static_cast<const double*>(values) + size_t(t) * n;
+      } else {
+        host_tile.resize(n);
+        const char* b = static_cast<const char*>(values) + size_t(t) * n * es;
+        for (size_t i = 0; i < n; ++i)
+          host_tile[i] = dtype == LITHOGPU_F32 ? double(reinterpret_cast<const float*>(b)[i])
+                                               : double(reinterpret_cast<const unsigned char*>(b)[i]);
+        payload = host_tile.data();
+      }
+      if (!paths[t]) throw UsageError("lithogpu_write_aimg: null path");
+      FILE* f = std::fopen(paths[t], "wb");
+      if (!f) throw std::runtime_error(std::string("cannot write ") + paths[t]);
+      const uint32_t w = uint32_t(grid->nx), h = uint32_t(grid->ny);
+      bool ok = std::fwrite("AIMG", 1, 4, f) == 4 && std::fwrite(&w, 4, 1, f) == 1 && std::fwrite(&h, 4, 1, f) == 1 &&
+                std::fwrite(&grid->pitch_nm, 8, 1, f) == 1 && std::fwrite(payload, 8, n, f) == n;
+      ok = (std::fclose(f) == 0) && ok;
+      if (!ok) throw std::runtime_error(std::string("cannot write ") + paths[t]);
+    }
+  });
+}
+
+lithogpu_status lithogpu_read_aimg(lithogpu_ctx* ctx, const char* path, int* nx, int* ny, double* pitch_nm,
+                                   double* values) {
+  if (!ctx || !path || !nx || !ny || !pitch_nm) {
+    g_last_error = "lithogpu_read_aimg: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    FILE* f = std::fopen(path, "rb");
+    if (!f) throw std::runtime_error(std::string("cannot open ") + path);
+    struct Closer {
+      FILE* f;
+      ~Closer() { std::fclose(f); }
+    } closer{f};
+    char magic[4];
+    if (std::fread(magic, 1, 4, f) != 4 || std::memcmp(magic, "AIMG", 4) != 0)
+      throw std::runtime_error(std::string(path) + ": not an AIMG file");
+    uint32_t w = 0, h = 0;
+    double p = 0;
+    if (std::fread(&w, 4, 1, f) != 1 || std::fread(&h, 4, 1, f) != 1 || std::fread(&p, 8, 1, f) != 1 || w == 0 ||
+        h == 0 || !(p > 0))
+      throw std::runtime_error(std::string(path) + ": bad AIMG header");
+    *nx = int(w);
+    *ny = int(h);
+    *pitch_nm = p;
+    if (!values) return;
+    const size_t n = size_t(w) * h;
+    if (is_device_ptr(values)) {
+      ctx->activate();
+      ctx->pinned_ensure(n * sizeof(double));
+      if (std::fread(ctx->pinned[0], 8, n, f) != n) throw std::runtime_error(std::string(path) + ": truncated AIMG payload");
+      LG_CUDA(cudaMemcpyAsync(values, ctx->pinned[0], n * 8, cudaMemcpyHostToDevice, ctx->stream));
+      LG_CUDA(cudaStreamSynchronize(ctx->stream));
+    } else if (std::fread(values, 8, n, f) != n) {
+      throw std::runtime_error(std::string(path) + ": truncated AIMG payload");
+    }
+  });
+}
