@@ -151,8 +151,7 @@ def kernel_model(geo, F, K, tiles=1):
     m = {
         "mask_cols": ((Pm + 1) * fN, (Pm + 1) * N * c + B * B * c),
         "socs_cols": (F * K * B * fn, F * K * (B * B * c + n * B * c)),
-        "socs_rows": (F * K * n * fn, F * K * (n * B * c + n * n * 4 + (n * n * c if se else 0))),
-        "isub_rows": (F * (n // 2) * fn, F * (2 * n * n * 4 + (P + 1) * n * c)),
+        "socs_rows": (F * (K + 1) * n * fn, F * K * (n * B * c + (n * n * c if se else 0)) + F * (P + 1) * n * c),
         "isub_cols": (F * (P + 1) * (fn + fN), F * ((P + 1) * n * c + N * (P + 1) * c)),
         "resist_rows": (F * (N // 2) * 2 * fN, F * (2 * N * (P + 1) * c + N * N * 4)),
         "wlp_cols": (F * (P + 1) * (fN + fn), F * ((P + 1) * N * c + n * (P + 1) * c)),

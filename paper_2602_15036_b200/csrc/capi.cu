@@ -461,8 +461,8 @@ struct Plan : PlanBase {
   // fp32 fast path (power-of-two tiles, register FFT kernels of socs_fast.cuh)
   bool fast = false;
   lg::FGeo fg{};
-  DevBuf ftNx, ftNy, ftnx, ftny, Wsub, Ih, Rh, Wh, Ip, Eb, Ht;
-  long long s_Wsub = 0, s_band = 0, s_Ip = 0, s_E = 0;
+  DevBuf ftNx, ftNy, ftnx, ftny, Wsub, Ih, Rh, Wh, Eb, Ht;
+  long long s_Wsub = 0, s_band = 0, s_E = 0;
   // ILT: keep the coherent fields E_fk from the forward rows for the adjoint
   // rows (saves one n-point IFFT per (row, kernel)) while they stay
   // L2-sized; beyond that recomputing them is cheaper than the HBM round trip
@@ -568,7 +568,6 @@ struct Plan : PlanBase {
         fg.twny = table(ay.n, ftny);
         s_Wsub = (long long)F * ay.n * ax.n;
         s_band = (long long)F * ay.nb2 * (ax.P + 1);
-        s_Ip = (long long)F * K * ay.n * ax.n;
         s_E = (long long)F * K * ay.n * ax.n;
         const long long npairs = (Ny + 1) / 2;
         const long long wpg = std::max(1, lg::fast_tpr(Nx) / 32);
@@ -672,7 +671,6 @@ struct Plan : PlanBase {
       if (store_E) Eb.ensure(c * s_E);
       Rh.ensure(c * s_band);
       Ih.ensure(c * s_band);
-      Ip.ensure(sizeof(T) * size_t(cap) * s_Ip);
       Wsub.ensure(sizeof(T) * size_t(cap) * s_Wsub);  // W_lp (adjoint) / I_sub (forward) scratch
       if (adjoint) Wh.ensure(c * s_band);
     }
@@ -850,9 +848,8 @@ struct Plan : PlanBase {
         fl("mask_cols", [&] { lg::fl_mask_cols(fg, s, tiles, Mr.as<C>(), s_Mr, Mhat.as<C>(), s_Mhat); });
         fl("socs_cols", [&] { lg::fl_socs_cols(fg, s, tiles, Mhat.as<C>(), s_Mhat, Ht.as<C>(), Tb.as<C>(), s_T); });
         fl("socs_rows", [&] {
-          lg::fl_socs_rows(fg, s, tiles, Tb.as<C>(), s_T, wk.as<T>(), dose, Ip.as<T>(), s_Ip, nullptr, 0);
+          lg::fl_socs_rows(fg, s, tiles, Tb.as<C>(), s_T, wk.as<T>(), dose, Ir.as<C>(), s_Ir, nullptr, 0);
         });
-        fl("isub_rows", [&] { lg::fl_isub_rows(fg, s, tiles, Ip.as<T>(), s_Ip, K, Ir.as<C>(), s_Ir); });
         isub_cols_fast(tiles, want_i, want_r);
         return;
       }
@@ -997,10 +994,9 @@ static void ilt_run_impl(lithogpu_ilt* ilt, int iters, double* cost_user, double
         P.fl("socs_cols", [&] { lg::fl_socs_cols(fg, s, tiles, P.Mhat.template as<C>(), P.s_Mhat, P.Ht.template as<C>(), P.Tb.template as<C>(), P.s_T); });
         C* Ef = P.store_E ? P.Eb.template as<C>() : nullptr;
         P.fl("socs_rows", [&] {
-          lg::fl_socs_rows(fg, s, tiles, P.Tb.template as<C>(), P.s_T, P.wk.template as<T>(), dose, P.Ip.template as<T>(),
-                           P.s_Ip, Ef, P.s_E);
+          lg::fl_socs_rows(fg, s, tiles, P.Tb.template as<C>(), P.s_T, P.wk.template as<T>(), dose, P.Ir.template as<C>(),
+                           P.s_Ir, Ef, P.s_E);
         });
-        P.fl("isub_rows", [&] { lg::fl_isub_rows(fg, s, tiles, P.Ip.template as<T>(), P.s_Ip, P.K, P.Ir.template as<C>(), P.s_Ir); });
         P.isub_cols_fast(tiles, false, true);
         P.fl("resist_rows", [&] {
           lg::fl_resist_rows(fg, s, tiles, P.Rc.template as<C>(), P.s_C, ilt->target.as<T>(), NN, ilt->cfd.as<T>(), beta, thr,

@@ -44,23 +44,12 @@ void fl_real_rows_fwd(const FGeo& g, cudaStream_t s, int tiles, int mode, const 
 }
 
 void fl_socs_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* T, long long t_ts,
-                  const float* wk, float dose, float* Ip, long long ip_ts, C32* Eo, long long e_ts) {
+                  const float* wk, float dose, C32* Ir, long long ir_ts, C32* Eo, long long e_ts) {
   with_len(g.ax.n, [&](auto c) {
     constexpr int L = decltype(c)::value;
-    const int kg = kgroups<L>(g.K);
-    flaunch<L>(fk_socs_rows<L>, dim3(g.ay.n, g.F * g.K / kg, tiles), kg, s, g, T, t_ts, wk, dose, Ip, ip_ts,
-               Eo, e_ts);
-  });
-}
-
-void fl_isub_rows(const FGeo& g, cudaStream_t s, int tiles, const float* Ip, long long ip_ts, int nsum,
-                  C32* Ir, long long ir_ts) {
-  with_len(g.ax.n, [&](auto c) {
-    constexpr int L = decltype(c)::value;
-    const int gr = spread_groups<L>((long long)tiles * g.F * ((g.ay.n + 1) / 2));
-    const size_t extra = size_t(g.ax.P + 1) * 2 * gr * sizeof(C32) + 16;
-    flaunch_x<L>(fk_isub_rows<L>, dim3(cdivi((g.ay.n + 1) / 2, gr), g.F, tiles), gr, extra, s, g, Ip, ip_ts,
-               nsum / kgroups<L>(g.K), Ir, ir_ts);
+    int gr = fgroups<L>(256);
+    if (gr > g.K) gr = g.K;
+    flaunch<L>(fk_socs_rows<L>, dim3(g.ay.n, g.F, tiles), gr, s, g, T, t_ts, wk, dose, Ir, ir_ts, Eo, e_ts);
   });
 }
 

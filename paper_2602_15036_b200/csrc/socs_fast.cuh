@@ -230,99 +230,70 @@ __global__ void __launch_bounds__(256) fk_real_rows_fwd(FGeo g, const float* __r
 }
 
 // ===========================================================================
-// per-kernel rows: CTA = one subgrid row sy x KG consecutive kernels (one per
-// row group), each group  E = IFFT_nx(T_fk[sy]),  then the KG intensity rows
-// dose w_fk |E|^2 are summed in shared memory in fixed group order:
-//   Ip[f][kg][sy][sx] = sum_{k in group kg} dose w_fk |E_fk|^2
-// (fk_isub_rows sums the K/KG partials, again in fixed order).
+// SOCS rows, CTA = one subgrid row sy of focus f: the groups take the K
+// kernels in turn (k = gid, gid + groups, ...), each  E = IFFT_nx(T_fk[sy])
+// and accumulates dose w_fk |E|^2 in registers; the group rows are summed in
+// shared memory in fixed group order (deterministic), and group 0 transforms
+// the intensity row: Ir[f][px][sy] = FFT_nx(I_sub[sy])(px), px in [0, P].
 // Eo (nullable) keeps E_fk[sy][x] for the adjoint rows.
-// grid (ny, F*K/KG, tiles), KG = blockDim / TPR divides K
+// grid (ny, F, tiles)
 // ===========================================================================
 template <int L>
 __global__ void __launch_bounds__(256) fk_socs_rows(FGeo g, const C32* __restrict__ T,
                                                     long long t_ts, const float* __restrict__ wk,
-                                                    float dose, float* __restrict__ Ip,
-                                                    long long ip_ts, C32* __restrict__ Eo,
-                                                    long long e_ts) {
+                                                    float dose, C32* __restrict__ Ir, long long ir_ts,
+                                                    C32* __restrict__ Eo, long long e_ts) {
   FGroup<L> G;
   TraceScope trace_(g);
   constexpr int E = RPlan<L>::E;
-  const int Bx = g.ax.B, ny = g.ay.n, lo = g.ax.lo, hi = g.ax.hi;
-  const int sy = blockIdx.x, fk = blockIdx.y * G.groups + G.gid;
-  const C32* src = T + blockIdx.z * t_ts + size_t(fk) * ny * Bx + size_t(sy) * Bx;
-  C32 v[E];
+  const int Bx = g.ax.B, ny = g.ay.n, lo = g.ax.lo, hi = g.ax.hi, K = g.K;
+  const int sy = blockIdx.x, f = blockIdx.y;
+  float acc[E];
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int sl = kslot(G.idx(e), lo, hi, L);
-    v[e] = sl >= 0 ? src[sl] : mk(0.f, 0.f);
-  }
-  fftr<float, L, +1>(v, G.sm, g.twnx, G.t, G.sync);
-  if (Eo) {  // keep the coherent field for the adjoint (fk_adj_rows<.., FROM_E>)
-    C32* eo = Eo + blockIdx.z * e_ts + (size_t(fk) * ny + sy) * L;
+  for (int e = 0; e < E; ++e) acc[e] = 0.f;
+  for (int k = G.gid; k < K; k += G.groups) {
+    const int fk = f * K + k;
+    const C32* src = T + blockIdx.z * t_ts + size_t(fk) * ny * Bx + size_t(sy) * Bx;
+    C32 v[E];
 #pragma unroll
-    for (int e = 0; e < E; ++e) eo[G.idx(e)] = v[e];
+    for (int e = 0; e < E; ++e) {
+      const int sl = kslot(G.idx(e), lo, hi, L);
+      v[e] = sl >= 0 ? src[sl] : mk(0.f, 0.f);
+    }
+    fftr<float, L, +1>(v, G.sm, g.twnx, G.t, G.sync);
+    if (Eo) {  // keep the coherent field for the adjoint (fk_adj_rows<.., FROM_E>)
+      C32* eo = Eo + blockIdx.z * e_ts + (size_t(fk) * ny + sy) * L;
+#pragma unroll
+      for (int e = 0; e < E; ++e) eo[G.idx(e)] = v[e];
+    }
+    const float w = wk[fk] * dose;
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] += w * (v[e].x * v[e].x + v[e].y * v[e].y);
   }
-  const float w = wk[fk] * dose;
-  G.sync();  // group done with its exchange buffer: reuse it for the row
+  G.sync();  // exchange buffer free: publish the group's partial row
   float* red = reinterpret_cast<float*>(G.sm);
 #pragma unroll
-  for (int e = 0; e < E; ++e) red[G.idx(e)] = w * (v[e].x * v[e].x + v[e].y * v[e].y);
+  for (int e = 0; e < E; ++e) red[G.idx(e)] = acc[e];
   __syncthreads();
+  if (G.gid != 0) return;
   extern __shared__ __align__(16) unsigned char fsm_raw[];
   const float* base = reinterpret_cast<const float*>(fsm_raw);
   constexpr int stride = 2 * rsm_len<L>();
-  float* o = Ip + blockIdx.z * ip_ts + (size_t(blockIdx.y) * ny + sy) * L;
-  for (int x = threadIdx.x; x < L; x += blockDim.x) {
-    float acc = base[x];
-    for (int gg = 1; gg < G.groups; ++gg) acc += base[gg * stride + x];
-    o[x] = acc;
-  }
-}
-
-// ===========================================================================
-// intensity rows (pair sy0, sy0+1 of focus f): I_sub = sum_k Ip (fixed order),
-// one packed FFT of the two real rows -> Ir[f][px][sy], px in [0, P].
-// grid (ceil(ny/2/groups), F, tiles)
-// ===========================================================================
-template <int L>
-__global__ void __launch_bounds__(256) fk_isub_rows(FGeo g, const float* __restrict__ Ip,
-                                                    long long ip_ts, int nsum, C32* __restrict__ Ir,
-                                                    long long ir_ts) {
-  FGroup<L> G;
-  TraceScope trace_(g);
-  constexpr int E = RPlan<L>::E;
-  const int f = blockIdx.y, ny = g.ay.n, npairs = (ny + 1) / 2;
-  const int pair0 = blockIdx.x * G.groups + G.gid;
-  const bool act = pair0 < npairs;
-  const int pair = act ? pair0 : npairs - 1;
-  const int sy0 = 2 * pair;
-  const bool has1 = sy0 + 1 < ny;
-  // Isub rows sy0, sy0+1 = sum over the nsum per-kernel partials Ip[f][k]
-  // (fixed order k = 0, 1, ..: deterministic, same bits as a separate pass)
-  const size_t plane = size_t(ny) * L;
-  const float* is = Ip + blockIdx.z * ip_ts + size_t(f) * nsum * plane;
-  const int sy1 = has1 ? sy0 + 1 : sy0;
   C32 v[E];
 #pragma unroll
-  for (int e = 0; e < E; ++e) v[e] = mk(0.f, 0.f);
-  for (int k = 0; k < nsum; ++k) {
-    const float* a = is + k * plane;
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      v[e].x += __ldg(a + size_t(sy0) * L + G.idx(e));
-      v[e].y += __ldg(a + size_t(sy1) * L + G.idx(e));
-    }
+  for (int e = 0; e < E; ++e) {
+    float s = base[G.idx(e)];
+    for (int gg = 1; gg < G.groups; ++gg) s += base[gg * stride + G.idx(e)];
+    v[e] = mk(s, 0.f);
   }
-  if (!has1) {
-#pragma unroll
-    for (int e = 0; e < E; ++e) v[e].y = 0.f;
-  }
+  G.sync();  // every partial read before group 0 reuses its buffer
   fftr<float, L, -1>(v, G.sm, g.twnx, G.t, G.sync);
-  G.sync();
-  to_smem<float, L>(v, G.sm, G.t);
-  G.sync();
-  store_pair_cols<L>(G, groups_bytes<L>(G.groups), Ir + blockIdx.z * ir_ts + size_t(f) * (g.ax.P + 1) * ny,
-                     ny, 2 * blockIdx.x * G.groups, ny, g.ax.P);
+  C32* o = Ir + blockIdx.z * ir_ts + size_t(f) * (g.ax.P + 1) * ny + sy;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int px = G.idx(e);
+    if (px <= g.ax.P) o[size_t(px) * ny] = v[e];
+  }
 }
 
 // ===========================================================================

@@ -41,13 +41,11 @@ void fast_fill_twiddles(int len, C32* host_out);  // fftr per-stage layout
 // ---- row kernels (fast_rows.cu) ----
 void fl_real_rows_fwd(const FGeo& g, cudaStream_t s, int tiles, int mode, const float* src,
                       long long src_ts, float steep, int Pout, C32* out, long long out_ts);
-// Eo (nullable): keep the coherent fields E_fk[sy][x] for fl_adj_rows(from_e)
+// SOCS rows with the fixed-order sum over the K kernels and the intensity row
+// transform: T -> Ir[F][P+1][n].  Eo (nullable): keep E_fk[sy][x] for
+// fl_adj_rows(from_e)
 void fl_socs_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* T, long long t_ts,
-                  const float* wk, float dose, float* Ip, long long ip_ts, C32* Eo, long long e_ts);
-// sums the per-kernel-group partials of Ip written by fl_socs_rows (fixed
-// order) before the row transform; nsum = K (the launcher divides by the groups)
-void fl_isub_rows(const FGeo& g, cudaStream_t s, int tiles, const float* Ip, long long ip_ts, int nsum,
-                  C32* Ir, long long ir_ts);
+                  const float* wk, float dose, C32* Ir, long long ir_ts, C32* Eo, long long e_ts);
 void fl_resist_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* Rc, long long c_ts,
                     const float* target, long long tg_ts, const float* cf, float beta, float thr,
                     C32* Dr, long long d_ts, double* costp, long long cp_ts);

@@ -14,7 +14,7 @@ import os
 import subprocess
 import sys
 
-NAMES = ["mask_cols", "socs_cols", "socs_rows", "isub_rows", "isub_cols", "resist_rows", "wlp_cols",
+NAMES = ["mask_cols", "socs_cols", "socs_rows", "isub_cols", "resist_rows", "wlp_cols",
          "wlp_rows", "adj_rows", "adj_cols", "grad_cols", "grad_rows"]
 
 CHILD = r'''
