@@ -95,6 +95,10 @@ void lithogpu_kernels_destroy(lithogpu_kernels* ks);
 /* geometry chosen for the tile: decimated grid and kernel band */
 lithogpu_status lithogpu_kernels_info(const lithogpu_kernels* ks, int* nx_sub, int* ny_sub,
                                       int* band_x, int* band_y);
+/* transforms per focus stack on the fp32 fast path: K, or ceil(K/2) when the
+ * kernels are Hermitian-symmetric and run as pairs; 0 when the
+ * stack runs on the generic path */
+lithogpu_status lithogpu_kernels_fast_order(const lithogpu_kernels* ks, int* order);
 
 /* ---- imaging ------------------------------------------------------------
  * image_socs (imaging.cpp:218-241): I = dose * sum_k w_k |IFFT(FFT(mask)/N^2 H_k)|^2

@@ -325,7 +325,10 @@ class DeviceKernels:
     def info(self):
         a, b, c, d = C.c_int(), C.c_int(), C.c_int(), C.c_int()
         check(lib().lithogpu_kernels_info(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(d)))
-        return {"nx_sub": a.value, "ny_sub": b.value, "band_x": c.value, "band_y": d.value}
+        k = C.c_int()
+        check(lib().lithogpu_kernels_fast_order(self._h, C.byref(k)))
+        return {"nx_sub": a.value, "ny_sub": b.value, "band_x": c.value, "band_y": d.value,
+                "fast_order": k.value}
 
     def close(self):
         if getattr(self, "_h", None):

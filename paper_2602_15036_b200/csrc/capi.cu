@@ -566,9 +566,10 @@ struct Plan : PlanBase {
         fg.twNy = table(Ny, ftNy);
         fg.twnx = table(ax.n, ftnx);
         fg.twny = table(ay.n, ftny);
+        make_pairs(weights, S, kx, ky, values);
         s_Wsub = (long long)F * ay.n * ax.n;
         s_band = (long long)F * ay.nb2 * (ax.P + 1);
-        s_E = (long long)F * K * ay.n * ax.n;
+        s_E = (long long)F * fg.K * ay.n * ax.n;
         const long long npairs = (Ny + 1) / 2;
         const long long wpg = std::max(1, lg::fast_tpr(Nx) / 32);
         s_cr = std::max(s_cr, F * npairs * wpg);
@@ -576,6 +577,94 @@ struct Plan : PlanBase {
       }
     }
   }
+
+  // ---- kernel pairing (fast path) ----------------------------
+  // A kernel whose band is Hermitian-symmetric, H(-q) = conj(H(q)), gives a
+  // REAL coherent field E = IFFT(M^ H) for a real mask (M^ is Hermitian); an
+  // anti-Hermitian one becomes Hermitian after a -i rotation (|E|^2 and the
+  // adjoint are unchanged).  When every kernel qualifies (in-focus stacks of a
+  // point-symmetric source: real TCC), kernels a, b are packed into one
+  // complex kernel H_a + i H_b: one transform per PAIR yields E_a + i E_b,
+  // |E_a|^2 w_a + |E_b|^2 w_b = w_a Re^2 + w_b Im^2, and the adjoint of the
+  // pair is exact with the band weight conj(w_a H_a + i w_b H_b) because only
+  // the Hermitian part of the accumulated spectrum reaches the real gradient.
+  bool paired = false;
+  DevBuf Hadj, wRe, wIm, wOne;
+  void make_pairs(const double* weights, int S, const std::vector<int>& kx, const std::vector<int>& ky,
+                  const double* values) {
+    const int Bx = g.ax.B, By = g.ay.B, lox = g.ax.lo, loy = g.ay.lo;
+    if (std::getenv("LITHOGPU_NO_PAIRS") || K < 2 || g.ax.lo != -g.ax.hi || g.ay.lo != -g.ay.hi) return;
+    std::vector<int> at(size_t(Bx) * By, -1);  // band slot -> support index
+    for (int s2 = 0; s2 < S; ++s2) at[size_t(ky[s2] - loy) * Bx + (kx[s2] - lox)] = s2;
+    std::vector<int> mir(S);
+    for (int s2 = 0; s2 < S; ++s2) {
+      mir[s2] = at[size_t(-ky[s2] - loy) * Bx + (-kx[s2] - lox)];
+      if (mir[s2] < 0) return;  // support not point-symmetric
+    }
+    std::vector<int> rot(size_t(F) * K, 0);  // 0: Hermitian, 1: anti-Hermitian (rotate by -i)
+    for (int fk = 0; fk < F * K; ++fk) {
+      const double* v = values + 2 * size_t(fk) * S;
+      double hmax = 0, eh = 0, ea = 0;
+      for (int s2 = 0; s2 < S; ++s2) {
+        const double re = v[2 * s2], im = v[2 * s2 + 1], mr = v[2 * mir[s2]], mi = v[2 * mir[s2] + 1];
+        hmax = std::max(hmax, std::hypot(re, im));
+        eh = std::max(eh, std::hypot(mr - re, mi + im));  // H(-q) - conj(H(q))
+        ea = std::max(ea, std::hypot(mr + re, mi - im));  // H(-q) + conj(H(q))
+      }
+      if (eh <= 1e-9 * hmax)
+        rot[fk] = 0;
+      else if (ea <= 1e-9 * hmax)
+        rot[fk] = 1;
+      else
+        return;
+    }
+    const int Kp = (K + 1) / 2;
+    std::vector<lg::C32> hc(size_t(F) * Kp * Bx * By, lg::C32{0.f, 0.f}), ha(hc.size(), lg::C32{0.f, 0.f});
+    std::vector<float> wr(size_t(F) * Kp, 0.f), wi(wr.size(), 0.f), one(wr.size(), 1.f);
+    for (int f = 0; f < F; ++f)
+      for (int pi = 0; pi < Kp; ++pi) {
+        const int a = 2 * pi, b = 2 * pi + 1;
+        const double wa = weights[size_t(f) * K + a], wb = b < K ? weights[size_t(f) * K + b] : 0.0;
+        wr[size_t(f) * Kp + pi] = float(wa);
+        wi[size_t(f) * Kp + pi] = float(wb);
+        for (int s2 = 0; s2 < S; ++s2) {
+          auto hk = [&](int k, double& re, double& im) {  // rotated kernel value
+            re = im = 0.0;
+            if (k >= K) return;
+            const double* v = values + 2 * (size_t(f * K + k) * S + s2);
+            if (rot[size_t(f) * K + k]) {  // -i (x + i y) = y - i x
+              re = v[1];
+              im = -v[0];
+            } else {
+              re = v[0];
+              im = v[1];
+            }
+          };
+          double ar, ai, br, bi;
+          hk(a, ar, ai);
+          hk(b, br, bi);
+          const size_t o = (size_t(f * Kp + pi) * Bx + (kx[s2] - lox)) * By + (ky[s2] - loy);
+          hc[o] = lg::C32{float(ar - bi), float(ai + br)};                      // H_a + i H_b
+          ha[o] = lg::C32{float(wa * ar - wb * bi), float(wa * ai + wb * br)};  // w_a H_a + i w_b H_b
+        }
+      }
+    auto up = [](DevBuf& d, const void* h, size_t bytes) {
+      d.ensure(bytes);
+      LG_CUDA(cudaMemcpy(d.p, h, bytes, cudaMemcpyHostToDevice));
+    };
+    up(Ht, hc.data(), hc.size() * sizeof(lg::C32));
+    up(Hadj, ha.data(), ha.size() * sizeof(lg::C32));
+    up(wRe, wr.data(), wr.size() * sizeof(float));
+    up(wIm, wi.data(), wi.size() * sizeof(float));
+    up(wOne, one.data(), one.size() * sizeof(float));
+    fg.K = Kp;
+    paired = true;
+  }
+  // weights / adjoint band of the fast kernels (paired or per kernel)
+  const float* fw1() const { return paired ? wRe.as<float>() : reinterpret_cast<const float*>(wk.p); }
+  const float* fw2() const { return paired ? wIm.as<float>() : nullptr; }
+  const lg::C32* fadjH() const { return paired ? Hadj.as<lg::C32>() : Ht.as<lg::C32>(); }
+  const float* fadjW() const { return paired ? wOne.as<float>() : reinterpret_cast<const float*>(wk.p); }
 
   // ---- launch trace (LITHOGPU_TRACE=<path>, diagnostic) ----
   DevBuf trace_buf;
@@ -848,7 +937,7 @@ struct Plan : PlanBase {
         fl("mask_cols", [&] { lg::fl_mask_cols(fg, s, tiles, Mr.as<C>(), s_Mr, Mhat.as<C>(), s_Mhat); });
         fl("socs_cols", [&] { lg::fl_socs_cols(fg, s, tiles, Mhat.as<C>(), s_Mhat, Ht.as<C>(), Tb.as<C>(), s_T); });
         fl("socs_rows", [&] {
-          lg::fl_socs_rows(fg, s, tiles, Tb.as<C>(), s_T, wk.as<T>(), dose, Ir.as<C>(), s_Ir, nullptr, 0);
+          lg::fl_socs_rows(fg, s, tiles, Tb.as<C>(), s_T, fw1(), fw2(), dose, Ir.as<C>(), s_Ir, nullptr, 0);
         });
         isub_cols_fast(tiles, want_i, want_r);
         return;
@@ -879,7 +968,7 @@ struct Plan : PlanBase {
           lg::fl_adj_rows(fg, s, 1, 1, W == nullptr, false, Tb.as<C>(), s_T, Wsub.as<T>(), s_Wsub, U.as<C>(),
                           s_U);
         });
-        fl("adj_cols", [&] { lg::fl_adj_cols(fg, s, 1, U.as<C>(), s_U, Ht.as<C>(), wk.as<T>(), dose, Acc.as<C>(), s_Acc); });
+        fl("adj_cols", [&] { lg::fl_adj_cols(fg, s, 1, U.as<C>(), s_U, fadjH(), fadjW(), dose, Acc.as<C>(), s_Acc); });
         fl("grad_cols", [&] {
           lg::fl_grad_cols(fg, s, 1, Acc.as<C>(), s_Acc, fg.F * fg.K, Gc.as<C>(), s_Gc, nullptr, 0, 0, nullptr, 0);
         });
@@ -994,7 +1083,7 @@ static void ilt_run_impl(lithogpu_ilt* ilt, int iters, double* cost_user, double
         P.fl("socs_cols", [&] { lg::fl_socs_cols(fg, s, tiles, P.Mhat.template as<C>(), P.s_Mhat, P.Ht.template as<C>(), P.Tb.template as<C>(), P.s_T); });
         C* Ef = P.store_E ? P.Eb.template as<C>() : nullptr;
         P.fl("socs_rows", [&] {
-          lg::fl_socs_rows(fg, s, tiles, P.Tb.template as<C>(), P.s_T, P.wk.template as<T>(), dose, P.Ir.template as<C>(),
+          lg::fl_socs_rows(fg, s, tiles, P.Tb.template as<C>(), P.s_T, P.fw1(), P.fw2(), dose, P.Ir.template as<C>(),
                            P.s_Ir, Ef, P.s_E);
         });
         P.isub_cols_fast(tiles, false, true);
@@ -1012,11 +1101,11 @@ static void ilt_run_impl(lithogpu_ilt* ilt, int iters, double* cost_user, double
         const int ncost = int(std::min<long long>(P.s_cr, F * npairs * std::max(1, lg::fast_tpr(P.g.ax.N) / 32)));
         double* cost_it = ilt->cost.as<double>() + size_t(it) * tiles;
         P.fl("adj_cols", [&] {
-          lg::fl_adj_cols(fg, s, tiles, P.U.template as<C>(), P.s_U, P.Ht.template as<C>(), P.wk.template as<T>(), dose,
+          lg::fl_adj_cols(fg, s, tiles, P.U.template as<C>(), P.s_U, P.fadjH(), P.fadjW(), dose,
                           P.Acc.template as<C>(), P.s_Acc);
         });
         P.fl("grad_cols", [&] {
-          lg::fl_grad_cols(fg, s, tiles, P.Acc.template as<C>(), P.s_Acc, F * P.K, P.Gc.template as<C>(), P.s_Gc,
+          lg::fl_grad_cols(fg, s, tiles, P.Acc.template as<C>(), P.s_Acc, F * fg.K, P.Gc.template as<C>(), P.s_Gc,
                            P.costrow.template as<double>(), P.s_cr, ncost, cost_it, 1);
         });
         P.fl("grad_rows", [&] {
@@ -1356,6 +1445,19 @@ void lithogpu_kernels_destroy(lithogpu_kernels* ks) {
   delete ks;
 }
 
+lithogpu_status lithogpu_kernels_fast_order(const lithogpu_kernels* ks, int* order) {
+  if (!ks || !order) {
+    g_last_error = "lithogpu_kernels_fast_order: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    *order = 0;
+    if (ks->precision != LITHOGPU_F32) return;
+    auto& p = const_cast<lithogpu_kernels*>(ks)->p<float>();
+    if (p.fast) *order = p.fg.K;
+  });
+}
+
 lithogpu_status lithogpu_kernels_info(const lithogpu_kernels* ks, int* nx_sub, int* ny_sub,
                                       int* band_x, int* band_y) {
   if (!ks) {
@@ -1491,11 +1593,19 @@ lithogpu_status lithogpu_intensity_gradient(lithogpu_kernels* ks, int focus, con
       LG_CUDA(cudaMemcpyAsync(Hf.p, P.H.template as<char>() + hsz * focus, hsz, cudaMemcpyDeviceToDevice, ctx->stream));
       LG_CUDA(cudaMemcpyAsync(wf.p, P.wk.template as<T>() + size_t(P.K) * focus, sizeof(T) * P.K, cudaMemcpyDeviceToDevice, ctx->stream));
       DevBuf& Htf = ctx->slot(11);
-      if (P.fast) {  // column-major fast-path copy of the same stack
-        Htf.ensure(hsz);
-        LG_CUDA(cudaMemcpyAsync(Htf.p, P.Ht.template as<char>() + hsz * focus, hsz, cudaMemcpyDeviceToDevice,
+      DevBuf& Haf = ctx->slot(12);
+      if (P.fast) {  // column-major fast-path copy of the same stack (kernel pairs when paired)
+        const size_t fsz = size_t(P.fg.K) * P.g.ay.B * P.g.ax.B * sizeof(lg::C32);
+        Htf.ensure(fsz);
+        LG_CUDA(cudaMemcpyAsync(Htf.p, P.Ht.template as<char>() + fsz * focus, fsz, cudaMemcpyDeviceToDevice,
                                 ctx->stream));
         std::swap(P.Ht.p, Htf.p);
+        if (P.paired) {
+          Haf.ensure(fsz);
+          LG_CUDA(cudaMemcpyAsync(Haf.p, P.Hadj.template as<char>() + fsz * focus, fsz, cudaMemcpyDeviceToDevice,
+                                  ctx->stream));
+          std::swap(P.Hadj.p, Haf.p);
+        }
       }
       std::swap(P.H.p, Hf.p);
       std::swap(P.wk.p, wf.p);
@@ -1507,6 +1617,7 @@ lithogpu_status lithogpu_intensity_gradient(lithogpu_kernels* ks, int focus, con
         P.gradient(m, w, T(dose), og.work);
       } catch (...) {
         if (P.fast) std::swap(P.Ht.p, Htf.p);
+        if (P.fast && P.paired) std::swap(P.Hadj.p, Haf.p);
         std::swap(P.H.p, Hf.p);
         std::swap(P.wk.p, wf.p);
         P.F = F0;
@@ -1515,6 +1626,7 @@ lithogpu_status lithogpu_intensity_gradient(lithogpu_kernels* ks, int focus, con
         throw;
       }
       if (P.fast) std::swap(P.Ht.p, Htf.p);
+      if (P.fast && P.paired) std::swap(P.Hadj.p, Haf.p);
       std::swap(P.H.p, Hf.p);
       std::swap(P.wk.p, wf.p);
       P.F = F0;

@@ -44,12 +44,13 @@ void fl_real_rows_fwd(const FGeo& g, cudaStream_t s, int tiles, int mode, const 
 }
 
 void fl_socs_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* T, long long t_ts,
-                  const float* wk, float dose, C32* Ir, long long ir_ts, C32* Eo, long long e_ts) {
+                  const float* wk, const float* wk2, float dose, C32* Ir, long long ir_ts, C32* Eo,
+                  long long e_ts) {
   with_len(g.ax.n, [&](auto c) {
     constexpr int L = decltype(c)::value;
     int gr = fgroups<L>(256);
     if (gr > g.K) gr = g.K;
-    flaunch<L>(fk_socs_rows<L>, dim3(g.ay.n, g.F, tiles), gr, s, g, T, t_ts, wk, dose, Ir, ir_ts, Eo, e_ts);
+    flaunch<L>(fk_socs_rows<L>, dim3(g.ay.n, g.F, tiles), gr, s, g, T, t_ts, wk, wk2, dose, Ir, ir_ts, Eo, e_ts);
   });
 }
 

@@ -232,7 +232,8 @@ __global__ void __launch_bounds__(256) fk_real_rows_fwd(FGeo g, const float* __r
 // ===========================================================================
 // SOCS rows, CTA = one subgrid row sy of focus f: the groups take the K
 // kernels in turn (k = gid, gid + groups, ...), each  E = IFFT_nx(T_fk[sy])
-// and accumulates dose w_fk |E|^2 in registers; the group rows are summed in
+// and accumulates dose w_fk |E|^2 in registers (wk2 != null: K kernel PAIRS,
+// dose (w_a Re(E)^2 + w_b Im(E)^2), Plan::make_pairs); the group rows are summed in
 // shared memory in fixed group order (deterministic), and group 0 transforms
 // the intensity row: Ir[f][px][sy] = FFT_nx(I_sub[sy])(px), px in [0, P].
 // Eo (nullable) keeps E_fk[sy][x] for the adjoint rows.
@@ -241,7 +242,8 @@ __global__ void __launch_bounds__(256) fk_real_rows_fwd(FGeo g, const float* __r
 template <int L>
 __global__ void __launch_bounds__(256) fk_socs_rows(FGeo g, const C32* __restrict__ T,
                                                     long long t_ts, const float* __restrict__ wk,
-                                                    float dose, C32* __restrict__ Ir, long long ir_ts,
+                                                    const float* __restrict__ wk2, float dose,
+                                                    C32* __restrict__ Ir, long long ir_ts,
                                                     C32* __restrict__ Eo, long long e_ts) {
   FGroup<L> G;
   TraceScope trace_(g);
@@ -267,8 +269,14 @@ __global__ void __launch_bounds__(256) fk_socs_rows(FGeo g, const C32* __restric
       for (int e = 0; e < E; ++e) eo[G.idx(e)] = v[e];
     }
     const float w = wk[fk] * dose;
+    if (wk2) {  // kernel pair: E = E_a + i E_b with real E_a, E_b
+      const float w2 = wk2[fk] * dose;
 #pragma unroll
-    for (int e = 0; e < E; ++e) acc[e] += w * (v[e].x * v[e].x + v[e].y * v[e].y);
+      for (int e = 0; e < E; ++e) acc[e] += w * (v[e].x * v[e].x) + w2 * (v[e].y * v[e].y);
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[e] += w * (v[e].x * v[e].x + v[e].y * v[e].y);
+    }
   }
   G.sync();  // exchange buffer free: publish the group's partial row
   float* red = reinterpret_cast<float*>(G.sm);

@@ -44,8 +44,10 @@ void fl_real_rows_fwd(const FGeo& g, cudaStream_t s, int tiles, int mode, const 
 // SOCS rows with the fixed-order sum over the K kernels and the intensity row
 // transform: T -> Ir[F][P+1][n].  Eo (nullable): keep E_fk[sy][x] for
 // fl_adj_rows(from_e)
+// wk2 != nullptr: g.K kernel pairs with weights wk (real part) / wk2 (imaginary part)
 void fl_socs_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* T, long long t_ts,
-                  const float* wk, float dose, C32* Ir, long long ir_ts, C32* Eo, long long e_ts);
+                  const float* wk, const float* wk2, float dose, C32* Ir, long long ir_ts, C32* Eo,
+                  long long e_ts);
 void fl_resist_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* Rc, long long c_ts,
                     const float* target, long long tg_ts, const float* cf, float beta, float thr,
                     C32* Dr, long long d_ts, double* costp, long long cp_ts);

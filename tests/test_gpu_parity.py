@@ -270,3 +270,37 @@ def test_gpu_kernel_generation_vs_host(ctx, n, K, foci):
             a = O.image_socs(mask, host.weights[f], host.support, host.values[f])
             b = O.image_socs(mask, gpu.weights[f], gpu.support, gpu.values[f])
             assert rel_linf(b, a) < 1e-6
+
+
+def test_kernel_pairs_engage_and_match(ctx, monkeypatch):
+    """in-focus kernels of the symmetric annular source are Hermitian-symmetric:
+    the fast path runs them as pairs (half the kernel transforms) with the
+    same images / gradients / ILT steps as the per-kernel path and the oracle."""
+    n = 512
+    ks = kernels_for(n, 1.0, (0.0,), k=16, grid_n=21)
+    defocus = kernels_for(n, 1.0, (40.0,), k=16, grid_n=21)
+    rng = np.random.default_rng(31)
+    mask = (rng.random((n, n)) > 0.5).astype(np.float64)
+    W = rng.standard_normal((n, n))
+    dk = L.DeviceKernels(ks, "f32", ctx)
+    assert dk.info()["fast_order"] == 8
+    assert L.DeviceKernels(defocus, "f32", ctx).info()["fast_order"] == 16
+    monkeypatch.setenv("LITHOGPU_NO_PAIRS", "1")
+    dk1 = L.DeviceKernels(ks, "f32", ctx)
+    assert dk1.info()["fast_order"] == 16
+    want = O.image_socs(mask, ks.weights[0], ks.support, ks.values[0])
+    a = dk.image(mask)["intensity"]
+    b = dk1.image(mask)["intensity"]
+    assert rel_linf(a, want) < 1e-4 and rel_linf(b, want) < 1e-4
+    gw = O.weighted_gradient(mask, ks.weights[0], ks.support, ks.values[0], W, dose=1.0)
+    assert rel_linf(dk.gradient(mask, 1.0, weight=W), gw) < 1e-4
+    prm = L.IltParams(step=0.05, focus_weights=[1.0])
+    th0 = rng.standard_normal((n, n)) * 0.5
+    out = []
+    for d in (dk, dk1):
+        s = L.IltSolver(d, prm, 1, "f32", ctx)
+        s.set_tiles(mask[None], th0[None])
+        c = s.run(2)
+        out.append((c, s.get_tiles()[0]))
+    assert np.abs(out[0][0] - out[1][0]).max() <= 1e-4 * np.abs(out[1][0]).max()
+    assert rel_linf(out[0][1] - th0, out[1][1] - th0) < 1e-3
