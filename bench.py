@@ -252,7 +252,8 @@ def run_ours(args, world, rank, local):
     peak_fp32 = ctx.fp32_peak_tflops()
     geo = {"N": N, "n": info["nx_sub"], "B": info["band_x"]}
     Kt = info.get("fast_order") or K  # transforms per stack (kernel pairs: ceil(K/2))
-    model = kernel_model(geo, F, Kt)
+    Ft = info.get("fast_stacks") or F  # computed focus stacks (mirror stacks merged)
+    model = kernel_model(geo, Ft, Kt)
     kernel_ms = {k: v[1] / v[0] for k, v in prof.items()}
     top = max(prof, key=lambda k: prof[k][1])
     top_flops, top_bytes = model.get(top, (0.0, 0.0))
@@ -330,7 +331,7 @@ def run_ours(args, world, rank, local):
             "data": "synthetic (seeded line/space+contact layout, GPU-rasterized; Abbe-SVD SOCS kernels)",
             "config": {"workload": desc, "tile": N, "K": K, "F": F, "iterations_per_step": iters,
                        "tiles_per_gpu": 1, "decimated_grid": info["nx_sub"], "kernel_band": info["band_x"],
-                       "kernel_transforms_per_stack": Kt,
+                       "kernel_transforms_per_stack": Kt, "computed_focus_stacks": Ft,
                        "ilt": ILT, "l2": "flushed between steps (256 MiB write, untimed)",
                        "parallelism": f"tiles sharded over {world} rank(s); NCCL all-reduce of the per-iteration "
                                       f"global cost vector once per step (no tile data crosses GPUs)"},

@@ -99,6 +99,10 @@ lithogpu_status lithogpu_kernels_info(const lithogpu_kernels* ks, int* nx_sub, i
  * kernels are Hermitian-symmetric and run as pairs; 0 when the
  * stack runs on the generic path */
 lithogpu_status lithogpu_kernels_fast_order(const lithogpu_kernels* ks, int* order);
+/* focus stacks the fast path computes: F, fewer when a stack is the conjugate
+ * mirror of another (paraxial -F / +F under a point-symmetric source; both
+ * print the same image) */
+lithogpu_status lithogpu_kernels_fast_stacks(const lithogpu_kernels* ks, int* stacks);
 
 /* ---- imaging ------------------------------------------------------------
  * image_socs (imaging.cpp:218-241): I = dose * sum_k w_k |IFFT(FFT(mask)/N^2 H_k)|^2

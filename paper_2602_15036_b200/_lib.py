@@ -58,6 +58,7 @@ _SIGS = {
     "lithogpu_kernels_info": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                         C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "lithogpu_kernels_fast_order": (C.c_int, [_vp, C.POINTER(C.c_int)]),
+    "lithogpu_kernels_fast_stacks": (C.c_int, [_vp, C.POINTER(C.c_int)]),
     "lithogpu_image_socs": (C.c_int, [_vp, C.c_int, _vp, C.c_int, C.c_double, _vp, C.c_int]),
     "lithogpu_image_resist": (C.c_int, [_vp, C.c_int, _vp, C.c_int, C.c_double, C.c_double,
                                         C.c_double, _vp, _vp, C.c_int, _vp]),

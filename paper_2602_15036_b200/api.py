@@ -325,10 +325,11 @@ class DeviceKernels:
     def info(self):
         a, b, c, d = C.c_int(), C.c_int(), C.c_int(), C.c_int()
         check(lib().lithogpu_kernels_info(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(d)))
-        k = C.c_int()
+        k, fs = C.c_int(), C.c_int()
         check(lib().lithogpu_kernels_fast_order(self._h, C.byref(k)))
+        check(lib().lithogpu_kernels_fast_stacks(self._h, C.byref(fs)))
         return {"nx_sub": a.value, "ny_sub": b.value, "band_x": c.value, "band_y": d.value,
-                "fast_order": k.value}
+                "fast_order": k.value, "fast_stacks": fs.value}
 
     def close(self):
         if getattr(self, "_h", None):

@@ -550,23 +550,40 @@ struct Plan : PlanBase {
           LG_CUDA(cudaMemcpy(b.p, h.data(), h.size() * sizeof(lg::C32), cudaMemcpyHostToDevice));
           return b.as<lg::C32>();
         };
+        // focus stacks computed on the fast path (mirror stacks merged)
+        merge_foci(weights, S, kx, ky, values);
+        const int Fc = fg.F;
         // column-major copy of the kernel band for the fast column kernels
         {
-          std::vector<lg::C32> ht(h.size());
-          for (int fk = 0; fk < F * K; ++fk)
-            for (int jy = 0; jy < By; ++jy)
-              for (int jx = 0; jx < Bx; ++jx) {
-                const C& src = h[(size_t(fk) * By + jy) * Bx + jx];
-                ht[(size_t(fk) * Bx + jx) * By + jy] = lg::C32{float(src.x), float(src.y)};
-              }
+          std::vector<lg::C32> ht(size_t(Fc) * K * Bx * By);
+          for (int r = 0; r < Fc; ++r)
+            for (int k = 0; k < K; ++k)
+              for (int jy = 0; jy < By; ++jy)
+                for (int jx = 0; jx < Bx; ++jx) {
+                  const C& src = h[((size_t(rep_src[r]) * K + k) * By + jy) * Bx + jx];
+                  ht[((size_t(r) * K + k) * Bx + jx) * By + jy] = lg::C32{float(src.x), float(src.y)};
+                }
           Ht.ensure(ht.size() * sizeof(lg::C32));
           LG_CUDA(cudaMemcpy(Ht.p, ht.data(), ht.size() * sizeof(lg::C32), cudaMemcpyHostToDevice));
+          std::vector<float> wf(size_t(Fc) * K);
+          for (int r = 0; r < Fc; ++r)
+            for (int k = 0; k < K; ++k) wf[size_t(r) * K + k] = float(weights[size_t(rep_src[r]) * K + k]);
+          wkf.ensure(wf.size() * sizeof(float));
+          LG_CUDA(cudaMemcpy(wkf.p, wf.data(), wf.size() * sizeof(float), cudaMemcpyHostToDevice));
         }
         fg.twNx = table(Nx, ftNx);
         fg.twNy = table(Ny, ftNy);
         fg.twnx = table(ax.n, ftnx);
         fg.twny = table(ay.n, ftny);
-        make_pairs(weights, S, kx, ky, values);
+        {
+          std::vector<double> cw(size_t(Fc) * K), cv(size_t(Fc) * K * S * 2);
+          for (int r = 0; r < Fc; ++r) {
+            std::copy(weights + size_t(rep_src[r]) * K, weights + size_t(rep_src[r] + 1) * K, cw.begin() + size_t(r) * K);
+            std::copy(values + size_t(rep_src[r]) * K * S * 2, values + size_t(rep_src[r] + 1) * K * S * 2,
+                      cv.begin() + size_t(r) * K * S * 2);
+          }
+          make_pairs(cw.data(), S, kx, ky, cv.data());
+        }
         s_Wsub = (long long)F * ay.n * ax.n;
         s_band = (long long)F * ay.nb2 * (ax.P + 1);
         s_E = (long long)F * fg.K * ay.n * ax.n;
@@ -592,7 +609,7 @@ struct Plan : PlanBase {
   DevBuf Hadj, wRe, wIm, wOne;
   void make_pairs(const double* weights, int S, const std::vector<int>& kx, const std::vector<int>& ky,
                   const double* values) {
-    const int Bx = g.ax.B, By = g.ay.B, lox = g.ax.lo, loy = g.ay.lo;
+    const int Bx = g.ax.B, By = g.ay.B, lox = g.ax.lo, loy = g.ay.lo, F = fg.F;
     if (std::getenv("LITHOGPU_NO_PAIRS") || K < 2 || g.ax.lo != -g.ax.hi || g.ay.lo != -g.ay.hi) return;
     std::vector<int> at(size_t(Bx) * By, -1);  // band slot -> support index
     for (int s2 = 0; s2 < S; ++s2) at[size_t(ky[s2] - loy) * Bx + (kx[s2] - lox)] = s2;
@@ -661,10 +678,101 @@ struct Plan : PlanBase {
     paired = true;
   }
   // weights / adjoint band of the fast kernels (paired or per kernel)
-  const float* fw1() const { return paired ? wRe.as<float>() : reinterpret_cast<const float*>(wk.p); }
+  const float* fw1() const { return paired ? wRe.as<float>() : wkf.as<float>(); }
   const float* fw2() const { return paired ? wIm.as<float>() : nullptr; }
   const lg::C32* fadjH() const { return paired ? Hadj.as<lg::C32>() : Ht.as<lg::C32>(); }
-  const float* fadjW() const { return paired ? wOne.as<float>() : reinterpret_cast<const float*>(wk.p); }
+  const float* fadjW() const { return paired ? wOne.as<float>() : wkf.as<float>(); }
+
+  // ---- mirror focus stacks (fast path) ----------------------
+  // Paraxial defocus flips the pupil phase, P(f; -F) = conj(P(f; F)); with a
+  // point-symmetric source the -F stack is the conjugate of the +F stack and
+  // both print the same aerial image of a real mask, so a
+  // stack that is the conjugate mirror of an earlier one is not recomputed:
+  // it is imaged / weighted through its representative.  The test is on the
+  // kernel values themselves (any source / generator): equal weights and
+  // H_f'(q) = c conj(H_f(-q)) with |c| = 1 per kernel, or H_f'(q) = c conj(H_f(q))
+  // with H_f of definite parity.
+  std::vector<int> rep;      // focus stack -> computed stack index
+  std::vector<int> rep_src;  // computed stack -> its source focus stack
+  DevBuf wkf;                // weights of the computed stacks [Fc][K]
+  void merge_foci(const double* weights, int S, const std::vector<int>& kx, const std::vector<int>& ky,
+                  const double* values) {
+    rep.assign(F, 0);
+    rep_src.clear();
+    const bool off = std::getenv("LITHOGPU_NO_FOCUS_MERGE") != nullptr;
+    const int Bx = g.ax.B, lox = g.ax.lo, loy = g.ay.lo;
+    std::vector<int> mir(S, -1);
+    if (g.ax.lo == -g.ax.hi && g.ay.lo == -g.ay.hi) {
+      std::vector<int> at(size_t(Bx) * g.ay.B, -1);
+      for (int s2 = 0; s2 < S; ++s2) at[size_t(ky[s2] - loy) * Bx + (kx[s2] - lox)] = s2;
+      for (int s2 = 0; s2 < S; ++s2) mir[s2] = at[size_t(-ky[s2] - loy) * Bx + (-kx[s2] - lox)];
+    }
+    const bool sym_support = std::find(mir.begin(), mir.end(), -1) == mir.end();
+    auto kv = [&](int f, int k, int s2, int comp) { return values[2 * ((size_t(f) * K + k) * S + s2) + comp]; };
+    auto mirror_of = [&](int f, int f2) {  // is stack f2 the conjugate mirror of stack f?
+      if (!sym_support) return false;
+      for (int k = 0; k < K; ++k) {
+        const double wa = weights[size_t(f) * K + k], wb = weights[size_t(f2) * K + k];
+        if (std::abs(wa - wb) > 1e-12 * std::max(std::abs(wa), 1e-300)) return false;
+        double hmax = 0;
+        int im = 0;
+        for (int s2 = 0; s2 < S; ++s2) {
+          const double a = std::hypot(kv(f, k, s2, 0), kv(f, k, s2, 1));
+          if (a > hmax) {
+            hmax = a;
+            im = s2;
+          }
+        }
+        if (hmax == 0) continue;
+        // parity of H_f (needed for the sigma = +1 form)
+        double ep = 0, eo = 0;
+        for (int s2 = 0; s2 < S; ++s2) {
+          ep = std::max(ep, std::hypot(kv(f, k, mir[s2], 0) - kv(f, k, s2, 0), kv(f, k, mir[s2], 1) - kv(f, k, s2, 1)));
+          eo = std::max(eo, std::hypot(kv(f, k, mir[s2], 0) + kv(f, k, s2, 0), kv(f, k, mir[s2], 1) + kv(f, k, s2, 1)));
+        }
+        const bool parity = std::min(ep, eo) <= 1e-9 * hmax;
+        bool ok = false;
+        for (int sigma : {-1, 1}) {
+          if (sigma == 1 && !parity) continue;
+          // c = H_f2(q_m) / conj(H_f(sigma q_m)), |c| = 1
+          const int sm = sigma == 1 ? im : mir[im];
+          const double xr = kv(f, k, sm, 0), xi = -kv(f, k, sm, 1);  // conj(H_f(sigma q_m))
+          const double yr = kv(f2, k, im, 0), yi = kv(f2, k, im, 1);
+          const double d = xr * xr + xi * xi;
+          if (d == 0) continue;
+          double cr = (yr * xr + yi * xi) / d, ci = (yi * xr - yr * xi) / d;
+          const double cn = std::hypot(cr, ci);
+          if (std::abs(cn - 1.0) > 1e-9) continue;
+          double err = 0;
+          for (int s2 = 0; s2 < S && err <= 1e-9 * hmax; ++s2) {
+            const int ss = sigma == 1 ? s2 : mir[s2];
+            const double ar = kv(f, k, ss, 0), ai = -kv(f, k, ss, 1);
+            const double pr = cr * ar - ci * ai, pi = cr * ai + ci * ar;
+            err = std::max(err, std::hypot(kv(f2, k, s2, 0) - pr, kv(f2, k, s2, 1) - pi));
+          }
+          if (err <= 1e-9 * hmax) {
+            ok = true;
+            break;
+          }
+        }
+        if (!ok) return false;
+      }
+      return true;
+    };
+    for (int f = 0; f < F; ++f) {
+      int r = -1;
+      if (!off)
+        for (int c = 0; c < int(rep_src.size()) && r < 0; ++c)
+          if (mirror_of(rep_src[c], f)) r = c;
+      if (r < 0) {
+        r = int(rep_src.size());
+        rep_src.push_back(f);
+      }
+      rep[f] = r;
+    }
+    fg.F = int(rep_src.size());
+  }
+  int frep(int focus) const { return fast ? rep[focus] : focus; }
 
   // ---- launch trace (LITHOGPU_TRACE=<path>, diagnostic) ----
   DevBuf trace_buf;
@@ -895,18 +1003,18 @@ struct Plan : PlanBase {
     bool fused = false;
     if (!unfused())
       fl("isub_cols", [&] {
-      fused = lg::fl_band_col2(fg, s, tiles, F, true, Ir.as<C>(), s_Ir, gxh.as<T>(), gyb.as<T>(),
+      fused = lg::fl_band_col2(fg, s, tiles, fg.F, true, Ir.as<C>(), s_Ir, gxh.as<T>(), gyb.as<T>(),
                                want_r ? Rc.as<C>() : nullptr, want_i ? Ic.as<C>() : nullptr, s_C);
     });
     if (fused) return;
     fl("isub_colfwd", [&] {
-      lg::fl_band_colfwd(fg, s, tiles, F, true, Ir.as<C>(), s_Ir, gxh.as<T>(), gyb.as<T>(),
+      lg::fl_band_colfwd(fg, s, tiles, fg.F, true, Ir.as<C>(), s_Ir, gxh.as<T>(), gyb.as<T>(),
                          want_r ? Rh.as<C>() : nullptr, want_i ? Ih.as<C>() : nullptr, s_band);
     });
     if (want_i)
-      fl("isub_colinv", [&] { lg::fl_band_colinv(fg, s, tiles, F, false, Ih.as<C>(), s_band, Ic.as<C>(), s_C); });
+      fl("isub_colinv", [&] { lg::fl_band_colinv(fg, s, tiles, fg.F, false, Ih.as<C>(), s_band, Ic.as<C>(), s_C); });
     if (want_r)
-      fl("isub_colinv", [&] { lg::fl_band_colinv(fg, s, tiles, F, false, Rh.as<C>(), s_band, Rc.as<C>(), s_C); });
+      fl("isub_colinv", [&] { lg::fl_band_colinv(fg, s, tiles, fg.F, false, Rh.as<C>(), s_band, Rc.as<C>(), s_C); });
   }
   void wlp_cols_fast(int tiles, int nf, bool gauss) {
     cudaStream_t s = ctx->stream;
@@ -1075,7 +1183,7 @@ static void ilt_run_impl(lithogpu_ilt* ilt, int iters, double* cost_user, double
         return e && e[0] == '1';
       }();
       lg::fast_set_pdl(ilt_pdl);
-      const int F = P.F;
+      const int F = P.fg.F;  // computed focus stacks (mirrors merged)
       if (need_prime)
         P.fl("real_rows_fwd", [&] { lg::fl_real_rows_fwd(fg, s, tiles, 1, theta, NN, a, P.g.ax.Pm, P.Mr.template as<C>(), P.s_Mr); });
       for (int it = 0; it < iters; ++it) {
@@ -1458,6 +1566,19 @@ lithogpu_status lithogpu_kernels_fast_order(const lithogpu_kernels* ks, int* ord
   });
 }
 
+lithogpu_status lithogpu_kernels_fast_stacks(const lithogpu_kernels* ks, int* stacks) {
+  if (!ks || !stacks) {
+    g_last_error = "lithogpu_kernels_fast_stacks: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    *stacks = ks->F;
+    if (ks->precision != LITHOGPU_F32) return;
+    auto& p = const_cast<lithogpu_kernels*>(ks)->p<float>();
+    if (p.fast) *stacks = p.fg.F;
+  });
+}
+
 lithogpu_status lithogpu_kernels_info(const lithogpu_kernels* ks, int* nx_sub, int* ny_sub,
                                       int* band_x, int* band_y) {
   if (!ks) {
@@ -1510,15 +1631,15 @@ void image_impl(lithogpu_kernels* ks, int focus, const void* mask, lithogpu_dtyp
                          want_r ? fullR.as<T>() : nullptr, pr ? fullP.as<unsigned char>() : nullptr,
                          0, T(thr), 1);
   if (I)
-    LG_CUDA(cudaMemcpyAsync(oi.work, fullI.as<T>() + size_t(focus) * n, sizeof(T) * n,
+    LG_CUDA(cudaMemcpyAsync(oi.work, fullI.as<T>() + size_t(P.frep(focus)) * n, sizeof(T) * n,
                             cudaMemcpyDeviceToDevice, ctx->stream));
   if (R)
-    LG_CUDA(cudaMemcpyAsync(orr.work, fullR.as<T>() + size_t(focus) * n, sizeof(T) * n,
+    LG_CUDA(cudaMemcpyAsync(orr.work, fullR.as<T>() + size_t(P.frep(focus)) * n, sizeof(T) * n,
                             cudaMemcpyDeviceToDevice, ctx->stream));
   bool host = oi.finish();
   host |= orr.finish();
   if (pr) {
-    LG_CUDA(cudaMemcpyAsync(pr, fullP.as<unsigned char>() + size_t(focus) * n, n, cudaMemcpyDefault,
+    LG_CUDA(cudaMemcpyAsync(pr, fullP.as<unsigned char>() + size_t(P.frep(focus)) * n, n, cudaMemcpyDefault,
                             ctx->stream));
     host |= !is_device_ptr(pr);
   }
@@ -1594,17 +1715,24 @@ lithogpu_status lithogpu_intensity_gradient(lithogpu_kernels* ks, int focus, con
       LG_CUDA(cudaMemcpyAsync(wf.p, P.wk.template as<T>() + size_t(P.K) * focus, sizeof(T) * P.K, cudaMemcpyDeviceToDevice, ctx->stream));
       DevBuf& Htf = ctx->slot(11);
       DevBuf& Haf = ctx->slot(12);
-      if (P.fast) {  // column-major fast-path copy of the same stack (kernel pairs when paired)
+      DevBuf& Wff = ctx->slot(13);
+      if (P.fast) {  // fast-path copies of the computed stack of `focus` (kernel pairs when paired)
+        const int fr = P.frep(focus);
         const size_t fsz = size_t(P.fg.K) * P.g.ay.B * P.g.ax.B * sizeof(lg::C32);
         Htf.ensure(fsz);
-        LG_CUDA(cudaMemcpyAsync(Htf.p, P.Ht.template as<char>() + fsz * focus, fsz, cudaMemcpyDeviceToDevice,
+        LG_CUDA(cudaMemcpyAsync(Htf.p, P.Ht.template as<char>() + fsz * fr, fsz, cudaMemcpyDeviceToDevice,
                                 ctx->stream));
         std::swap(P.Ht.p, Htf.p);
         if (P.paired) {
           Haf.ensure(fsz);
-          LG_CUDA(cudaMemcpyAsync(Haf.p, P.Hadj.template as<char>() + fsz * focus, fsz, cudaMemcpyDeviceToDevice,
+          LG_CUDA(cudaMemcpyAsync(Haf.p, P.Hadj.template as<char>() + fsz * fr, fsz, cudaMemcpyDeviceToDevice,
                                   ctx->stream));
           std::swap(P.Hadj.p, Haf.p);
+        } else {
+          Wff.ensure(sizeof(float) * P.K);
+          LG_CUDA(cudaMemcpyAsync(Wff.p, P.wkf.template as<float>() + size_t(P.K) * fr, sizeof(float) * P.K,
+                                  cudaMemcpyDeviceToDevice, ctx->stream));
+          std::swap(P.wkf.p, Wff.p);
         }
       }
       std::swap(P.H.p, Hf.p);
@@ -1618,6 +1746,7 @@ lithogpu_status lithogpu_intensity_gradient(lithogpu_kernels* ks, int focus, con
       } catch (...) {
         if (P.fast) std::swap(P.Ht.p, Htf.p);
         if (P.fast && P.paired) std::swap(P.Hadj.p, Haf.p);
+        if (P.fast && !P.paired) std::swap(P.wkf.p, Wff.p);
         std::swap(P.H.p, Hf.p);
         std::swap(P.wk.p, wf.p);
         P.F = F0;
@@ -1627,6 +1756,7 @@ lithogpu_status lithogpu_intensity_gradient(lithogpu_kernels* ks, int focus, con
       }
       if (P.fast) std::swap(P.Ht.p, Htf.p);
       if (P.fast && P.paired) std::swap(P.Hadj.p, Haf.p);
+      if (P.fast && !P.paired) std::swap(P.wkf.p, Wff.p);
       std::swap(P.H.p, Hf.p);
       std::swap(P.wk.p, wf.p);
       P.F = F0;
@@ -1795,7 +1925,16 @@ lithogpu_status lithogpu_ilt_create(lithogpu_kernels* ks, const lithogpu_ilt_par
       ilt->target.ensure(es * n);
       ilt->cfd.ensure(es * ks->F);
       if (es == 4) {
+        // fp32 fast path: weights of the computed stacks (mirror stacks add to
+        // their representative, Plan::merge_foci)
+        auto& P = ks->p<float>();
         std::vector<float> c(ilt->cf.begin(), ilt->cf.end());
+        if (P.fast) {
+          std::vector<double> m(size_t(P.fg.F), 0.0);
+          for (int f = 0; f < ks->F; ++f) m[size_t(P.rep[f])] += ilt->cf[f];
+          c.assign(m.begin(), m.end());
+          c.resize(size_t(ks->F), 0.f);
+        }
         LG_CUDA(cudaMemcpy(ilt->cfd.p, c.data(), 4 * c.size(), cudaMemcpyHostToDevice));
       } else {
         LG_CUDA(cudaMemcpy(ilt->cfd.p, ilt->cf.data(), 8 * ilt->cf.size(), cudaMemcpyHostToDevice));
@@ -2304,7 +2443,7 @@ void evaluate_epe_impl(lithogpu_kernels* ks, int focus, int nm, const void* mask
   r64.ensure(sizeof(double) * NN, ctx->stream);
   const lithogpu_grid grid = ks->grid;
   for (int t = 0; t < nm; ++t) {
-    const T* rt = fullR.as<T>() + (size_t(t) * P.F + focus) * NN;
+    const T* rt = fullR.as<T>() + (size_t(t) * P.F + P.frep(focus)) * NN;
     const double* f64;
     if constexpr (std::is_same<T, double>::value) {
       f64 = rt;

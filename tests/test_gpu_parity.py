@@ -304,3 +304,39 @@ def test_kernel_pairs_engage_and_match(ctx, monkeypatch):
         out.append((c, s.get_tiles()[0]))
     assert np.abs(out[0][0] - out[1][0]).max() <= 1e-4 * np.abs(out[1][0]).max()
     assert rel_linf(out[0][1] - th0, out[1][1] - th0) < 1e-3
+
+
+def test_mirror_focus_stacks_merge(ctx, monkeypatch):
+    """paraxial -F / +F stacks of the symmetric source are conjugate mirrors:
+    the fast path computes one of them (fast_stacks), with images, gradients
+    and ILT cost equal to the oracle on every stack's own kernels."""
+    n = 256
+    foci = (-40.0, 0.0, 40.0)
+    ks = kernels_for(n, 1.0, foci, k=8, grid_n=21)
+    dk = L.DeviceKernels(ks, "f32", ctx)
+    assert dk.info()["fast_stacks"] == 2
+    rng = np.random.default_rng(37)
+    mask = (rng.random((n, n)) > 0.5).astype(np.float64)
+    W = rng.standard_normal((n, n))
+    for f in range(3):
+        want = O.image_socs(mask, ks.weights[f], ks.support, ks.values[f])
+        assert rel_linf(dk.image(mask, focus=f)["intensity"], want) < 1e-4
+        gw = O.weighted_gradient(mask, ks.weights[f], ks.support, ks.values[f], W, dose=1.0)
+        assert rel_linf(dk.gradient(mask, 1.0, weight=W, focus=f), gw) < 1e-4
+    prm = L.IltParams(step=0.05, focus_weights=[0.2, 0.5, 0.3])
+    th0 = rng.standard_normal((n, n)) * 0.5
+    out = []
+    for merge in ("", "1"):
+        if merge:
+            monkeypatch.setenv("LITHOGPU_NO_FOCUS_MERGE", "1")
+        d = L.DeviceKernels(ks, "f32", ctx)
+        assert d.info()["fast_stacks"] == (3 if merge else 2)
+        s = L.IltSolver(d, prm, 1, "f32", ctx)
+        s.set_tiles(mask[None], th0[None])
+        out.append((s.run(2), s.get_tiles()[0]))
+    th = th0.copy()
+    c_ref, _ = O.ilt_iteration(th, mask, ks.weights, ks.support, ks.values, [0.2, 0.5, 0.3],
+                               [4.0, 30.0, 0.25, 2.0, 1.0, 0.05], 1.0)
+    assert abs(out[0][0][0, 0] - c_ref) <= 1e-4 * abs(c_ref)
+    assert np.abs(out[0][0] - out[1][0]).max() <= 1e-4 * np.abs(out[1][0]).max()
+    assert rel_linf(out[0][1] - th0, out[1][1] - th0) < 1e-3
