@@ -239,8 +239,13 @@ __global__ void __launch_bounds__(256) fk_real_rows_fwd(FGeo g, const float* __r
 // Eo (nullable) keeps E_fk[sy][x] for the adjoint rows.
 // grid (ny, F, tiles)
 // ===========================================================================
+// 3 CTAs / SM (80 registers, small spills) keeps all n rows resident: -2 % per
+// ILT iteration at C2 against the unbounded 128-register build
+#ifndef LG_SOCSROWS_MINB
+#define LG_SOCSROWS_MINB 3
+#endif
 template <int L>
-__global__ void __launch_bounds__(256) fk_socs_rows(FGeo g, const C32* __restrict__ T,
+__global__ void __launch_bounds__(256, LG_SOCSROWS_MINB) fk_socs_rows(FGeo g, const C32* __restrict__ T,
                                                     long long t_ts, const float* __restrict__ wk,
                                                     const float* __restrict__ wk2, float dose,
                                                     C32* __restrict__ Ir, long long ir_ts,
@@ -433,8 +438,11 @@ __global__ void __launch_bounds__(256) fk_wlp_rows(FGeo g, const C32* __restrict
 //   U_fk[qx][sy] = FFT_nx(W_lp(sy,.) . IFFT_nx(T_fk[sy]))(qx), qx in band
 // grid (ceil(ny/groups), F*K, tiles)
 // ===========================================================================
+#ifndef LG_ADJROWS_MINB
+#define LG_ADJROWS_MINB 2
+#endif
 template <int L, bool UNIFORM, bool FROM_E>
-__global__ void __launch_bounds__(256, 2) fk_adj_rows(FGeo g, const C32* __restrict__ T,
+__global__ void __launch_bounds__(256, LG_ADJROWS_MINB) fk_adj_rows(FGeo g, const C32* __restrict__ T,
                                                       long long t_ts, const float* __restrict__ Wsub,
                                                       long long ws_ts, C32* __restrict__ U,
                                                       long long u_ts) {
