@@ -546,9 +546,33 @@ def _contours_c1(ctx, stream, dk, m32, grid, n_gauges=4096, radius=20.0):
            "loops": len(cs.loop_start) - 1, "points": int(len(cs.xs)), "gauges": n_gauges,
            "gpu_ms_contours": (t1 - t0) / reps * 1e3, "gpu_ms_epe": (t2 - t1) / reps * 1e3,
            "timer": "host perf_counter around the synchronous API call (device field, host result)"}
+    # evaluate_epe (opc.cpp:140-151) over a batch of 8 MEEF-style probe masks, fused on the device
+    m64 = m32.double()
+    probes = torch.stack([torch.roll(m64, shifts=k % 3, dims=k % 2) for k in range(8)])
+    probes[:, :16, :] = 0.0
+    probes[:, -16:, :] = 0.0
+    probes[:, :, :16] = 0.0
+    probes[:, :, -16:] = 0.0
+    ph = probes.cpu().numpy()
+    L.evaluate_epe(ph, dk, gauges, 1.0, 2.0, ILT["threshold"], radius)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    L.evaluate_epe(ph, dk, gauges, 1.0, 2.0, ILT["threshold"], radius)
+    out["gpu_ms_evaluate_epe_per_mask"] = (time.perf_counter() - t0) / len(ph) * 1e3
+    out["evaluate_epe_batch"] = len(ph)
     try:
         from oracle import refpy as R
         if R.available():
+            # the reference pipeline on one probe (image_socs -> gaussian_blur -> contours -> EPE)
+            ks = dk.kernels if hasattr(dk, "kernels") else None
+            R.set_threads(1)
+            if ks is not None:
+                t0 = time.perf_counter()
+                I = R.image_socs(ph[0], ks.weights[0], ks.support, ks.values[0])
+                rr = R.gaussian_blur(I, 2.0, 1.0)
+                R.marching_squares(rr, ILT["threshold"])
+                R.measure_epe(gauges, radius)
+                out["ref_cpu_ms_evaluate_epe_per_mask"] = (time.perf_counter() - t0) * 1e3
             f = res.cpu().numpy()
             t0 = time.perf_counter()
             R.marching_squares(f, ILT["threshold"], grid.pitch_nm, grid.origin_x_nm, grid.origin_y_nm)

@@ -46,6 +46,21 @@ def test_status_mapping_without_gpu():
         lib.lithogpu_ctx_destroy(h)
     assert lib.lithogpu_kernels_create(None, None, 0, 1, 1, None, 1, None, None, None) == _lib.ERR_USAGE
     assert lib.lithogpu_ilt_run(None, 1, None, None) == _lib.ERR_USAGE
+    # contour / EPE / evaluate_epe / AIMG / GPU kernel generation entry points
+    assert lib.lithogpu_marching_squares(None, None, None, 0.5, None) == _lib.ERR_USAGE
+    assert lib.lithogpu_contours_size(None, None, None) == _lib.ERR_USAGE
+    assert lib.lithogpu_contours_get(None, None, None, None) == _lib.ERR_USAGE
+    assert lib.lithogpu_measure_epe(None, None, 1, 1.0, None, None) == _lib.ERR_USAGE
+    assert lib.lithogpu_measure_epe_loops(None, None, 0, None, None, None, 1, 1.0, None, None) == _lib.ERR_USAGE
+    assert lib.lithogpu_evaluate_epe(None, 0, 1, None, 1, 1.0, 2.0, 0.25, None, 0, 1.0, None, None,
+                                     None) == _lib.ERR_USAGE
+    assert lib.lithogpu_write_aimg(None, None, 1, None, None, 1) == _lib.ERR_USAGE
+    assert lib.lithogpu_read_aimg(None, b"x", None, None, None, None) == _lib.ERR_USAGE
+    assert lib.lithogpu_socs_kernels_gpu(None, 8, 8, 1.0, 13.5, 0.33, 0, None, 0, 1, None, 0, None, 0, 1.0, 1,
+                                         None, None, None, None) == _lib.ERR_USAGE
+    assert lib.lithogpu_kernels_fast_order(None, None) == _lib.ERR_USAGE
+    assert lib.lithogpu_kernels_fast_stacks(None, None) == _lib.ERR_USAGE
+    lib.lithogpu_contours_destroy(None)  # null-safe
     with pytest.raises(_lib.LithoUsageError):
         _lib.check(_lib.ERR_USAGE)
 
