@@ -107,6 +107,47 @@ struct DevBuf {
   }
 };
 
+// Stream-ordered pool allocation (cudaMallocAsync) for per-call scratch of the
+// non-graph entry points (rasterization, contours, EPE, evaluate_epe): no
+// cudaMalloc / cudaFree (tens of microseconds to milliseconds) on every call.
+struct PoolBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaStream_t s = nullptr;
+  PoolBuf() = default;
+  PoolBuf(const PoolBuf&) = delete;
+  PoolBuf& operator=(const PoolBuf&) = delete;
+  ~PoolBuf() { release(); }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    bytes = 0;
+  }
+  void ensure(size_t b, cudaStream_t st) {
+    if (b <= bytes && st == s) return;
+    release();
+    s = st;
+    if (b == 0) return;
+    static const bool pool_init = [] {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        unsigned long long keep = ~0ull;  // keep freed blocks for reuse
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      return true;
+    }();
+    (void)pool_init;
+    LG_CUDA(cudaMallocAsync(&p, b, s));
+    bytes = b;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
 bool is_device_ptr(const void* p) {
   if (!p) return false;
   cudaPointerAttributes a;
@@ -1462,14 +1503,14 @@ lithogpu_status lithogpu_rasterize(lithogpu_ctx* ctx, const lithogpu_grid* grid,
     const int nby = (ny + lg::kRasterBin - 1) / lg::kRasterBin;
     const int nbins = nbx * nby;
     // device scratch
-    DevBuf dxy, dst, vx, vy, bb, cnt, off, tmp;
-    dxy.ensure(sizeof(int64_t) * 2 * std::max<int64_t>(nv, 1));
-    dst.ensure(sizeof(int64_t) * (n_poly + 1));
-    vx.ensure(sizeof(double) * std::max<int64_t>(nv, 1));
-    vy.ensure(sizeof(double) * std::max<int64_t>(nv, 1));
-    bb.ensure(sizeof(int4) * std::max(n_poly, 1));
-    cnt.ensure(sizeof(int) * (nbins + 1));
-    off.ensure(sizeof(int) * (nbins + 1));
+    PoolBuf dxy, dst, vx, vy, bb, cnt, off, tmp;
+    dxy.ensure(sizeof(int64_t) * 2 * std::max<int64_t>(nv, 1), ctx->stream);
+    dst.ensure(sizeof(int64_t) * (n_poly + 1), ctx->stream);
+    vx.ensure(sizeof(double) * std::max<int64_t>(nv, 1), ctx->stream);
+    vy.ensure(sizeof(double) * std::max<int64_t>(nv, 1), ctx->stream);
+    bb.ensure(sizeof(int4) * std::max(n_poly, 1), ctx->stream);
+    cnt.ensure(sizeof(int) * (nbins + 1), ctx->stream);
+    off.ensure(sizeof(int) * (nbins + 1), ctx->stream);
     if (nv > 0) LG_CUDA(cudaMemcpyAsync(dxy.p, xy, sizeof(int64_t) * 2 * nv, cudaMemcpyDefault, ctx->stream));
     LG_CUDA(cudaMemcpyAsync(dst.p, st.data(), sizeof(int64_t) * (n_poly + 1), cudaMemcpyHostToDevice, ctx->stream));
     if (n_poly > 0) {
@@ -1483,20 +1524,20 @@ lithogpu_status lithogpu_rasterize(lithogpu_ctx* ctx, const lithogpu_grid* grid,
     ctx->check_launch();
     size_t tbytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tbytes, cnt.as<int>(), off.as<int>(), nbins + 1, ctx->stream);
-    tmp.ensure(std::max<size_t>(tbytes, 16));
+    tmp.ensure(std::max<size_t>(tbytes, 16), ctx->stream);
     cub::DeviceScan::ExclusiveSum(tmp.p, tbytes, cnt.as<int>(), off.as<int>(), nbins + 1, ctx->stream);
     int total = 0;
     LG_CUDA(cudaMemcpyAsync(&total, off.as<int>() + nbins, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     LG_CUDA(cudaStreamSynchronize(ctx->stream));
-    DevBuf lists;
-    lists.ensure(sizeof(int) * std::max(total, 1));
+    PoolBuf lists;
+    lists.ensure(sizeof(int) * std::max(total, 1), ctx->stream);
     lg::k_raster_bin<true><<<nbins, 256, 0, ctx->stream>>>(bb.as<int4>(), n_poly, nbx, cnt.as<int>(), off.as<int>(), lists.as<int>());
     ctx->check_launch();
     const bool dev_out = is_device_ptr(out);
-    DevBuf obuf;
+    PoolBuf obuf;
     double* dout = out;
     if (!dev_out) {
-      obuf.ensure(sizeof(double) * npix);
+      obuf.ensure(sizeof(double) * npix, ctx->stream);
       dout = obuf.as<double>();
     }
     dim3 blk(32, 8), grd(cdiv(nx, 32), cdiv(ny, 8));
@@ -2096,47 +2137,6 @@ lithogpu_status lithogpu_ilt_get_tiles(lithogpu_ilt* ilt, void* theta, void* mas
 // ===========================================================================
 // contours + EPE: contour_kernels.cuh
 // ===========================================================================
-// Stream-ordered pool allocation (cudaMallocAsync): the contour path runs
-// once per resist image, so its grid-sized scratch must not pay cudaMalloc /
-// cudaFree (milliseconds) on every call.
-struct PoolBuf {
-  void* p = nullptr;
-  size_t bytes = 0;
-  cudaStream_t s = nullptr;
-  PoolBuf() = default;
-  PoolBuf(const PoolBuf&) = delete;
-  PoolBuf& operator=(const PoolBuf&) = delete;
-  ~PoolBuf() { release(); }
-  void release() {
-    if (p) cudaFreeAsync(p, s);
-    p = nullptr;
-    bytes = 0;
-  }
-  void ensure(size_t b, cudaStream_t st) {
-    if (b <= bytes && st == s) return;
-    release();
-    s = st;
-    if (b == 0) return;
-    static const bool pool_init = [] {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaMemPool_t pool;
-      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        unsigned long long keep = ~0ull;  // keep freed blocks for reuse
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-      }
-      return true;
-    }();
-    (void)pool_init;
-    LG_CUDA(cudaMallocAsync(&p, b, s));
-    bytes = b;
-  }
-  template <typename T>
-  T* as() const {
-    return static_cast<T*>(p);
-  }
-};
-
 struct lithogpu_contours {
   lithogpu_ctx* ctx = nullptr;
   lg::CGeo g{};
