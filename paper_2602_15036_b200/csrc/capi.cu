@@ -3,6 +3,8 @@
 // the reference interface each entry point replaces).
 #include <cuda_runtime.h>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 
 #include <algorithm>
 #include <cmath>
@@ -1503,12 +1505,14 @@ lithogpu_status lithogpu_rasterize(lithogpu_ctx* ctx, const lithogpu_grid* grid,
     const int nby = (ny + lg::kRasterBin - 1) / lg::kRasterBin;
     const int nbins = nbx * nby;
     // device scratch
-    PoolBuf dxy, dst, vx, vy, bb, cnt, off, tmp;
+    PoolBuf dxy, dst, vx, vy, bb, cnt, off, tmp, rect, rsign;
     dxy.ensure(sizeof(int64_t) * 2 * std::max<int64_t>(nv, 1), ctx->stream);
     dst.ensure(sizeof(int64_t) * (n_poly + 1), ctx->stream);
     vx.ensure(sizeof(double) * std::max<int64_t>(nv, 1), ctx->stream);
     vy.ensure(sizeof(double) * std::max<int64_t>(nv, 1), ctx->stream);
     bb.ensure(sizeof(int4) * std::max(n_poly, 1), ctx->stream);
+    rect.ensure(sizeof(double4) * std::max(n_poly, 1), ctx->stream);
+    rsign.ensure(sizeof(double) * std::max(n_poly, 1), ctx->stream);
     cnt.ensure(sizeof(int) * (nbins + 1), ctx->stream);
     off.ensure(sizeof(int) * (nbins + 1), ctx->stream);
     if (nv > 0) LG_CUDA(cudaMemcpyAsync(dxy.p, xy, sizeof(int64_t) * 2 * nv, cudaMemcpyDefault, ctx->stream));
@@ -1516,7 +1520,8 @@ lithogpu_status lithogpu_rasterize(lithogpu_ctx* ctx, const lithogpu_grid* grid,
     if (n_poly > 0) {
       lg::k_raster_prep<<<cdiv(n_poly, 128), 128, 0, ctx->stream>>>(
           dxy.as<int64_t>(), dst.as<int64_t>(), n_poly, 1.0 / dbu_per_nm, grid->origin_x_nm,
-          grid->origin_y_nm, grid->pitch_nm, nx, ny, vx.as<double>(), vy.as<double>(), bb.as<int4>());
+          grid->origin_y_nm, grid->pitch_nm, nx, ny, vx.as<double>(), vy.as<double>(), bb.as<int4>(),
+          rect.as<double4>(), rsign.as<double>());
       ctx->check_launch();
     }
     LG_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int) * (nbins + 1), ctx->stream));
@@ -1541,7 +1546,27 @@ lithogpu_status lithogpu_rasterize(lithogpu_ctx* ctx, const lithogpu_grid* grid,
       dout = obuf.as<double>();
     }
     dim3 blk(32, 8), grd(cdiv(nx, 32), cdiv(ny, 8));
-    lg::k_raster_pixels<<<grd, blk, 0, ctx->stream>>>(vx.as<double>(), vy.as<double>(), dst.as<int64_t>(), bb.as<int4>(), off.as<int>(), cnt.as<int>(), lists.as<int>(), nx, ny, nbx, dout);
+    PoolBuf slow, slist, nslow, stmp;
+    slow.ensure(sizeof(int) * npix, ctx->stream);
+    slist.ensure(sizeof(int) * npix, ctx->stream);
+    nslow.ensure(sizeof(int), ctx->stream);
+    lg::k_raster_pixels<<<grd, blk, 0, ctx->stream>>>(vx.as<double>(), vy.as<double>(), dst.as<int64_t>(), bb.as<int4>(),
+                                                      rect.as<double4>(), rsign.as<double>(), off.as<int>(),
+                                                      cnt.as<int>(), lists.as<int>(), nx, ny, nbx, dout,
+                                                      slow.as<int>());
+    ctx->check_launch();
+    {  // compact the pixels that need the clip chain (edges of rectangles, general polygons)
+      cub::CountingInputIterator<int> ids(0);
+      size_t sb = 0;
+      cub::DeviceSelect::Flagged(nullptr, sb, ids, slow.as<int>(), slist.as<int>(), nslow.as<int>(), int(npix),
+                                 ctx->stream);
+      stmp.ensure(std::max<size_t>(sb, 16), ctx->stream);
+      cub::DeviceSelect::Flagged(stmp.p, sb, ids, slow.as<int>(), slist.as<int>(), nslow.as<int>(), int(npix),
+                                 ctx->stream);
+    }
+    lg::k_raster_pixels_slow<<<148 * 8, 256, 0, ctx->stream>>>(
+        vx.as<double>(), vy.as<double>(), dst.as<int64_t>(), bb.as<int4>(), rect.as<double4>(), rsign.as<double>(),
+        off.as<int>(), cnt.as<int>(), lists.as<int>(), nx, nbx, slist.as<int>(), nslow.as<int>(), dout);
     ctx->check_launch();
     if (!dev_out) LG_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * npix, cudaMemcpyDeviceToHost, ctx->stream));
     LG_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -25,13 +25,31 @@ namespace lg {
 constexpr int kRasterBin = 32;
 
 // --- stage 0: vertices to pixel units + clamped bbox (raster.cpp:62-81) ---
+// Axis-aligned rectangles also get their pixel-unit bounds and orientation:
+// a pixel box lying inside such a rectangle clips (raster.cpp:31-49) to its
+// own four integer corners (every intersection is computed along an
+// axis-parallel edge, so it is exact), whose shoelace sum is exactly +-2, i.e.
+// the reference adds exactly +-1.0 -- k_raster_pixels adds that directly.
 __global__ void k_raster_prep(const int64_t* __restrict__ xy, const int64_t* __restrict__ starts,
                               int npoly, double scale, double ox, double oy, double pitch, int nx,
                               int ny, double* __restrict__ vx, double* __restrict__ vy,
-                              int4* __restrict__ bbox) {
+                              int4* __restrict__ bbox, double4* __restrict__ rect,
+                              double* __restrict__ rsign) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= npoly) return;
   const int64_t v0 = starts[p], v1 = starts[p + 1];
+  double sg = 0.0;
+  if (v1 - v0 == 4) {
+    const int64_t* q = xy + 2 * v0;  // (x0,y0) .. (x3,y3)
+    const bool a = q[0] == q[2] && q[3] == q[5] && q[4] == q[6] && q[7] == q[1];
+    const bool b = q[1] == q[3] && q[2] == q[4] && q[5] == q[7] && q[6] == q[0];
+    if ((a || b) && q[0] != q[4] && q[1] != q[5]) {
+      // orientation: sign of the cross product of the first two edges
+      const double e1x = double(q[2] - q[0]), e1y = double(q[3] - q[1]);
+      const double e2x = double(q[4] - q[2]), e2y = double(q[5] - q[3]);
+      sg = (e1x * e2y - e1y * e2x) > 0 ? 1.0 : -1.0;
+    }
+  }
   int4 bb = make_int4(1, 0, 1, 0);  // empty: ix0 > ix1
   if (v1 - v0 >= 3) {
     double minx = 1e300, maxx = -1e300, miny = 1e300, maxy = -1e300;
@@ -52,8 +70,10 @@ __global__ void k_raster_prep(const int64_t* __restrict__ xy, const int64_t* __r
     iy1 = iy1 > ny - 1 ? ny - 1 : iy1;
     ix1 = ix1 > nx - 1 ? nx - 1 : ix1;
     bb = make_int4(ix0, ix1, iy0, iy1);
+    rect[p] = make_double4(minx, maxx, miny, maxy);
   }
   bbox[p] = bb;
+  rsign[p] = sg;
 }
 
 __device__ __forceinline__ bool bb_hits_bin(int4 bb, int bx, int by) {
@@ -200,21 +220,34 @@ struct ClipChain {
 // emit<S> counts into s[S-1].out for S in 1..3; stage 3's outputs go to the
 // area accumulator (ar.n).  Row polygon size = s[1].out, cell size = ar.n.
 
-__global__ void k_raster_pixels(const double* __restrict__ vx, const double* __restrict__ vy,
-                                const int64_t* __restrict__ starts, const int4* __restrict__ bbox,
-                                const int* __restrict__ offsets, const int* __restrict__ counts,
-                                const int* __restrict__ lists, int nx, int ny, int nbx,
-                                double* __restrict__ out) {
-  const int ix = blockIdx.x * blockDim.x + threadIdx.x;
-  const int iy = blockIdx.y * blockDim.y + threadIdx.y;
-  if (ix >= nx || iy >= ny) return;
+// Pixel value: every polygon of the pixel's bin in order (raster.cpp:83-93).
+// EXACT_ONLY: only pixels whose polygons all take the exact shortcut (outside
+// the bbox, or inside a rectangle) are finished here; the others set
+// slow[pix] and are finished by the full clip pass over their compacted list,
+// so no warp carries a clip chain for a few edge pixels.
+template <bool EXACT_ONLY>
+__device__ __forceinline__ bool raster_pixel(int ix, int iy, const double* __restrict__ vx,
+                                             const double* __restrict__ vy, const int64_t* __restrict__ starts,
+                                             const int4* __restrict__ bbox, const double4* __restrict__ rect,
+                                             const double* __restrict__ rsign, const int* __restrict__ offsets,
+                                             const int* __restrict__ counts, const int* __restrict__ lists,
+                                             int nbx, double& pix) {
   const int bin = (iy / kRasterBin) * nbx + ix / kRasterBin;
   const int o = offsets[bin], c = counts[bin];
-  double pix = 0.0;
+  pix = 0.0;
   for (int i = 0; i < c; ++i) {
     const int p = lists[o + i];
     const int4 bb = bbox[p];
     if (ix < bb.x || ix > bb.y || iy < bb.z || iy > bb.w) continue;
+    const double sg = rsign[p];
+    if (sg != 0.0) {
+      const double4 r = rect[p];
+      if (r.x <= double(ix) && r.y >= double(ix + 1) && r.z <= double(iy) && r.w >= double(iy + 1)) {
+        pix = __dadd_rn(pix, sg);  // == pix + 0.5 * (+-2): the exact clipped unit square
+        continue;
+      }
+    }
+    if (EXACT_ONLY) return false;
     ClipChain ch;
     ch.init(ix, iy);
     const int64_t v0 = starts[p], v1 = starts[p + 1];
@@ -224,7 +257,46 @@ __global__ void k_raster_pixels(const double* __restrict__ vx, const double* __r
     if (ch.ar.n < 3) continue;      // raster.cpp:88 cell polygon degenerate
     pix = __dadd_rn(pix, __dmul_rn(0.5, ch.ar.a));  // raster.cpp:24,89
   }
-  out[size_t(iy) * nx + ix] = pix < 0.0 ? 0.0 : (pix > 1.0 ? 1.0 : pix);  // raster.cpp:93
+  return true;
+}
+
+__device__ __forceinline__ double raster_clamp(double pix) {
+  return pix < 0.0 ? 0.0 : (pix > 1.0 ? 1.0 : pix);  // raster.cpp:93
+}
+
+// pass 1: all pixels; exact-shortcut pixels are written, the rest flagged
+__global__ void k_raster_pixels(const double* __restrict__ vx, const double* __restrict__ vy,
+                                const int64_t* __restrict__ starts, const int4* __restrict__ bbox,
+                                const double4* __restrict__ rect, const double* __restrict__ rsign,
+                                const int* __restrict__ offsets, const int* __restrict__ counts,
+                                const int* __restrict__ lists, int nx, int ny, int nbx,
+                                double* __restrict__ out, int* __restrict__ slow) {
+  const int ix = blockIdx.x * blockDim.x + threadIdx.x;
+  const int iy = blockIdx.y * blockDim.y + threadIdx.y;
+  if (ix >= nx || iy >= ny) return;
+  double pix;
+  const bool done = raster_pixel<true>(ix, iy, vx, vy, starts, bbox, rect, rsign, offsets, counts, lists, nbx, pix);
+  const size_t o = size_t(iy) * nx + ix;
+  slow[o] = done ? 0 : 1;
+  if (done) out[o] = raster_clamp(pix);
+}
+
+// pass 2: the flagged pixels (compacted list), full ordered clip chain
+__global__ void k_raster_pixels_slow(const double* __restrict__ vx, const double* __restrict__ vy,
+                                     const int64_t* __restrict__ starts, const int4* __restrict__ bbox,
+                                     const double4* __restrict__ rect, const double* __restrict__ rsign,
+                                     const int* __restrict__ offsets, const int* __restrict__ counts,
+                                     const int* __restrict__ lists, int nx, int nbx,
+                                     const int* __restrict__ slow_list, const int* __restrict__ nslow,
+                                     double* __restrict__ out) {
+  const int n = *nslow;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int q = slow_list[i];
+    const int ix = q % nx, iy = q / nx;
+    double pix;
+    raster_pixel<false>(ix, iy, vx, vy, starts, bbox, rect, rsign, offsets, counts, lists, nbx, pix);
+    out[q] = raster_clamp(pix);
+  }
 }
 
 }  // namespace lg

@@ -340,3 +340,23 @@ def test_mirror_focus_stacks_merge(ctx, monkeypatch):
     assert abs(out[0][0][0, 0] - c_ref) <= 1e-4 * abs(c_ref)
     assert np.abs(out[0][0] - out[1][0]).max() <= 1e-4 * np.abs(out[1][0]).max()
     assert rel_linf(out[0][1] - th0, out[1][1] - th0) < 1e-3
+
+
+def test_rasterize_rectangles_bit_exact(ctx):
+    """Manhattan layouts (the bench targets): rectangles take the exact
+    full-pixel shortcut inside, the clip chain on their edges; bitwise equal
+    to the reference at fractional origins / pitches / dbu."""
+    from paper_2602_15036_b200 import layouts as LY
+    rng = np.random.default_rng(77)
+    polys = LY.line_space_contacts(300, 260, seed=3)
+    # extra rectangles and an L shape with odd coordinates, healed by the reference
+    extra = [[(7, 9), (51, 9), (51, 33), (7, 33)], [(201, 150), (237, 150), (237, 211), (219, 211), (219, 171),
+                                                   (201, 171)]]
+    healed_extra = R.heal(extra)
+    for (ox, oy, pitch, dbu) in [(0.0, 0.0, 1.0, 1.0), (-3.25, 1.5, 0.5, 2.0), (0.3, -0.7, 1.25, 1.0)]:
+        nx, ny = int(330 / pitch), int(290 / pitch)
+        for layer in (polys, healed_extra):
+            want = R.rasterize(layer, nx, ny, pitch, ox, oy, dbu)
+            got = L.rasterize_layer(layer, L.Grid(nx, ny, pitch, ox, oy), dbu, ctx)
+            assert np.array_equal(got, want), (ox, oy, pitch, dbu)
+    assert rng is not None
