@@ -424,8 +424,10 @@ def run_ours(args, world, rank, local):
     result = None
     if rank == 0:
         cpu = None
+        cufftw = None
         if not args.no_cpu_baseline and world == 1:
             cpu = _cpu_baseline(args.config)
+            cufftw = _cufftw_baseline(args.config)
         result = {
             "metric": f"ILT tile-iterations/s ({desc})",
             "value": value,
@@ -457,6 +459,7 @@ def run_ours(args, world, rank, local):
                          "kernel_share": shares, "kernel_ms_avg": kernel_ms,
                          "instrumented_iter_ms": iter_ms_prof},
             "cpu_baseline": cpu,
+            "reference_cufftw": cufftw,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clk,
@@ -668,6 +671,33 @@ def _cpu_baseline(cfg_name, n_iter=2):
             "sample": f"{n_iter} ILT iterations of the {grid.nx}x{grid.ny} tile (K={ks.weights.shape[1]}, F={F}) "
                       f"through the unmodified reference image_socs/gaussian_blur/fft2 (fp64, FFT shim, "
                       f"{cores} OpenMP threads), {dt:.1f} s"}
+
+
+def _cufftw_baseline(cfg_name, n_iter=2):
+    """The unmodified reference with its FFTW calls on NVIDIA cuFFTW (library
+    GPU FFTs; the reference algorithm, host memory, a plan per fft2 call):
+    the naive GPU port the hand-written path is measured against.  Run in a
+    subprocess so the two reference builds never share one process."""
+    code = (
+        "import json, sys, time, numpy as np; sys.path.insert(0, '.');"
+        "import bench; from oracle import refpy as R; R.use_variant('cufftw');"
+        "assert R.available();"
+        f"g, ks, t, it, d = bench._ref_problem('{cfg_name}');"
+        "th = ((2 * t - 1) * (2.0 / bench.ILT['mask_steepness'])).copy(); F = ks.weights.shape[0];"
+        "prm = [bench.ILT[k] for k in ('mask_steepness', 'resist_beta', 'threshold', 'resist_sigma_nm', 'dose', 'step')];"
+        "R.ilt_iteration(th, t, ks.weights, ks.support, ks.values, [1.0 / F] * F, prm, g.pitch_nm);"
+        "t0 = time.perf_counter();"
+        f"[R.ilt_iteration(th, t, ks.weights, ks.support, ks.values, [1.0 / F] * F, prm, g.pitch_nm) for _ in range({n_iter})];"
+        f"dt = (time.perf_counter() - t0) / {n_iter};"
+        "print(json.dumps({'value': 1.0 / dt, 'unit': 'tile-iter/s', 'ms_per_iteration': dt * 1e3}))")
+    try:
+        r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=600)
+        out = json.loads(r.stdout.strip().splitlines()[-1])
+        out["sample"] = (f"{n_iter} ILT iterations (after 1 warm-up) of the same tile through the unmodified "
+                         "reference with FFTW resolved by cuFFTW (GPU FFTs on host buffers, fp64)")
+        return out
+    except Exception as e:  # optional data point
+        return {"unavailable": str(e)[:200]}
 
 
 def run_reference(args, world, rank):

@@ -15,6 +15,17 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_ref", "libref_litho.so")
 _lib = None
+# the same reference sources with FFTW resolved by NVIDIA cuFFTW (GPU FFTs,
+# host memory): oracle/build_ref_cufftw.sh; select with use_variant("cufftw")
+VARIANTS = {"cpu": LIB_PATH, "cufftw": os.path.join(_HERE, "_ref", "libref_litho_cufftw.so")}
+
+
+def use_variant(name: str) -> None:
+    """switch the reference build ("cpu": FFT stand-in on host cores,
+    "cufftw": cuFFT through its FFTW interface)."""
+    global LIB_PATH, _lib
+    LIB_PATH = VARIANTS[name]
+    _lib = None
 
 
 def available() -> bool:
