@@ -360,3 +360,55 @@ def test_rasterize_rectangles_bit_exact(ctx):
             got = L.rasterize_layer(layer, L.Grid(nx, ny, pitch, ox, oy), dbu, ctx)
             assert np.array_equal(got, want), (ox, oy, pitch, dbu)
     assert rng is not None
+
+
+@pytest.mark.parametrize("K,foci", [(5, (0.0,)), (6, (-30.0, 30.0))])
+def test_odd_pairs_and_two_mirror_stacks(ctx, K, foci):
+    """odd K (the last kernel pair has one member) and a lone -F/+F pair of
+    stacks: images and one ILT step against the oracle."""
+    n = 128
+    ks = kernels_for(n, 1.0, foci, k=K, grid_n=21)
+    dk = L.DeviceKernels(ks, "f32", ctx)
+    info = dk.info()
+    F = len(foci)
+    if F == 1:
+        assert info["fast_order"] == (K + 1) // 2
+    else:
+        assert info["fast_stacks"] == 1
+    rng = np.random.default_rng(K)
+    mask = rng.random((n, n))
+    for f in range(F):
+        want = O.image_socs(mask, ks.weights[f], ks.support, ks.values[f])
+        assert rel_linf(dk.image(mask, focus=f)["intensity"], want) < 1e-4
+    target = (mask > 0.5).astype(np.float64)
+    th0 = rng.standard_normal((n, n)) * 0.5
+    prm = L.IltParams(step=0.05, focus_weights=[1.0 / F] * F)
+    s = L.IltSolver(dk, prm, 1, "f32", ctx)
+    s.set_tiles(target[None], th0[None])
+    c = s.run(1)
+    th = th0.copy()
+    c_ref, _ = O.ilt_iteration(th, target, ks.weights, ks.support, ks.values, [1.0 / F] * F,
+                               [4.0, 30.0, 0.25, 2.0, 1.0, 0.05], 1.0)
+    assert abs(c[0, 0] - c_ref) <= 1e-4 * abs(c_ref)
+    assert rel_linf(s.get_tiles()[0][0] - th0, th - th0) < 1e-3
+
+
+def test_evaluate_epe_f32_kernels(ctx):
+    """evaluate_epe on the fp32 fast path (resist widened to f64 on the device)
+    against the fp64 path: same open flags, EPE within the fp32 image tolerance."""
+    from paper_2602_15036_b200 import layouts as LY
+    n = 256
+    grid = L.Grid(n, n, 1.0)
+    m = L.rasterize_layer(LY.line_space_contacts(n, n, seed=4), grid, 1.0, ctx)
+    m[:16, :] = m[-16:, :] = 0.0
+    m[:, :16] = m[:, -16:] = 0.0
+    ks = kernels_for(n, 1.0, (0.0,), k=8, grid_n=21)
+    rng = np.random.default_rng(5)
+    k = 300
+    ang = rng.choice([0.0, np.pi / 2, np.pi, 1.5 * np.pi], k)
+    g = np.column_stack([rng.uniform(20, n - 20, k), rng.uniform(20, n - 20, k), np.cos(ang), np.sin(ang)])
+    e32, o32 = L.evaluate_epe(m, L.DeviceKernels(ks, "f32", ctx), g, 1.0, 2.0, 0.25, 10.0)
+    e64, o64 = L.evaluate_epe(m, L.DeviceKernels(ks, "f64", ctx), g, 1.0, 2.0, 0.25, 10.0)
+    both = ~o32 & ~o64
+    assert (o32 != o64).sum() <= 2  # a gauge exactly at the search radius may flip
+    assert np.abs(e32[both] - e64[both]).max() < 0.05  # nm; fp32 intensity 1e-4 rel near the threshold
