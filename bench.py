@@ -460,6 +460,7 @@ def run_ours(args, world, rank, local):
                          "instrumented_iter_ms": iter_ms_prof},
             "cpu_baseline": cpu,
             "reference_cufftw": cufftw,
+            "in_graph": _in_graph_timeline(args.config, top, top_flops, peak_fp32) if world == 1 else None,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clk,
@@ -671,6 +672,27 @@ def _cpu_baseline(cfg_name, n_iter=2):
             "sample": f"{n_iter} ILT iterations of the {grid.nx}x{grid.ny} tile (K={ks.weights.shape[1]}, F={F}) "
                       f"through the unmodified reference image_socs/gaussian_blur/fft2 (fp64, FFT shim, "
                       f"{cores} OpenMP threads), {dt:.1f} s"}
+
+
+def _in_graph_timeline(cfg_name, top, top_flops, peak):
+    """Per-kernel durations inside the replayed CUDA graph (tools/trace.py:
+    first-CTA start to last-warp end from %globaltimer stamps, no per-launch
+    events breaking the graph), and the dominant kernel's roofline fraction on
+    that duration beside the event-timed one."""
+    try:
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "trace.py"), "--config", cfg_name],
+                           cwd=ROOT, capture_output=True, text=True, timeout=300)
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+        per = d["per_kernel"]
+        us = per.get(top, {}).get("dur_us")
+        out = {"per_iter_us": d["per_iter_us"], "kernel_us": {k: v["dur_us"] for k, v in per.items()},
+               "gap_us": {k: v["gap_before_us"] for k, v in per.items()}}
+        if us:
+            out.update({"top_kernel": top, "achieved_tflops": top_flops / (us * 1e-6) / 1e12,
+                        "frac": top_flops / (us * 1e-6) / 1e12 / peak if peak else None})
+        return out
+    except Exception as e:
+        return {"unavailable": str(e)[:200]}
 
 
 def _cufftw_baseline(cfg_name, n_iter=2):
