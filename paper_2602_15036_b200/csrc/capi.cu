@@ -661,7 +661,9 @@ struct Plan : PlanBase {
       mir[s2] = at[size_t(-ky[s2] - loy) * Bx + (-kx[s2] - lox)];
       if (mir[s2] < 0) return;  // support not point-symmetric
     }
-    std::vector<int> rot(size_t(F) * K, 0);  // 0: Hermitian, 1: anti-Hermitian (rotate by -i)
+    // per kernel: 0 Hermitian, 1 anti-Hermitian (rotate by -i), -1 neither
+    std::vector<int> rot(size_t(F) * K, 0);
+    std::vector<char> stack_ok(F, 1);
     for (int fk = 0; fk < F * K; ++fk) {
       const double* v = values + 2 * size_t(fk) * S;
       double hmax = 0, eh = 0, ea = 0;
@@ -671,43 +673,59 @@ struct Plan : PlanBase {
         eh = std::max(eh, std::hypot(mr - re, mi + im));  // H(-q) - conj(H(q))
         ea = std::max(ea, std::hypot(mr + re, mi - im));  // H(-q) + conj(H(q))
       }
-      if (eh <= 1e-9 * hmax)
-        rot[fk] = 0;
-      else if (ea <= 1e-9 * hmax)
-        rot[fk] = 1;
-      else
-        return;
+      rot[fk] = eh <= 1e-9 * hmax ? 0 : (ea <= 1e-9 * hmax ? 1 : -1);
+      if (rot[fk] < 0) stack_ok[fk / K] = 0;
     }
-    const int Kp = (K + 1) / 2;
-    std::vector<lg::C32> hc(size_t(F) * Kp * Bx * By, lg::C32{0.f, 0.f}), ha(hc.size(), lg::C32{0.f, 0.f});
-    std::vector<float> wr(size_t(F) * Kp, 0.f), wi(wr.size(), 0.f), one(wr.size(), 1.f);
-    for (int f = 0; f < F; ++f)
-      for (int pi = 0; pi < Kp; ++pi) {
-        const int a = 2 * pi, b = 2 * pi + 1;
-        const double wa = weights[size_t(f) * K + a], wb = b < K ? weights[size_t(f) * K + b] : 0.0;
-        wr[size_t(f) * Kp + pi] = float(wa);
-        wi[size_t(f) * Kp + pi] = float(wb);
+    const int npair = int(std::count(stack_ok.begin(), stack_ok.end(), 1));
+    if (npair == 0) return;
+    // all stacks pair: Kp slots per stack.  Mixed (e.g. the in-focus stack of a
+    // through-focus set): K slots per stack; a pairing stack uses its first
+    // Kp slots and leaves the rest empty (skipped by every kernel via
+    // FGeo::slot_on), the others keep one kernel per slot with w_a = w_b = w
+    // (w Re^2 + w Im^2 = w |E|^2, adjoint band w H: the per-kernel path).
+    const bool mixed = npair < F;
+    const int Kp = (K + 1) / 2, KS = mixed ? K : Kp;
+    std::vector<lg::C32> hc(size_t(F) * KS * Bx * By, lg::C32{0.f, 0.f}), ha(hc.size(), lg::C32{0.f, 0.f});
+    std::vector<float> wr(size_t(F) * KS, 0.f), wi(wr.size(), 0.f), one(wr.size(), 1.f);
+    std::vector<int> on(wr.size(), 0);
+    for (int f = 0; f < F; ++f) {
+      auto kval = [&](int k, int s2, bool rotate, double& re, double& im) {
+        re = im = 0.0;
+        if (k >= K) return;
+        const double* v = values + 2 * (size_t(f * K + k) * S + s2);
+        if (rotate && rot[size_t(f) * K + k] == 1) {  // -i (x + i y) = y - i x
+          re = v[1];
+          im = -v[0];
+        } else {
+          re = v[0];
+          im = v[1];
+        }
+      };
+      const int nslot = stack_ok[f] ? Kp : K;
+      for (int sl = 0; sl < nslot; ++sl) {
+        const int a = stack_ok[f] ? 2 * sl : sl, b = stack_ok[f] ? 2 * sl + 1 : -1;
+        const double wa = weights[size_t(f) * K + a];
+        const double wb = b >= 0 ? (b < K ? weights[size_t(f) * K + b] : 0.0) : wa;
+        const size_t si = size_t(f) * KS + sl;
+        wr[si] = float(wa);
+        wi[si] = float(wb);
+        on[si] = (wa != 0.0 || (b >= 0 && wb != 0.0)) ? 1 : 0;
         for (int s2 = 0; s2 < S; ++s2) {
-          auto hk = [&](int k, double& re, double& im) {  // rotated kernel value
-            re = im = 0.0;
-            if (k >= K) return;
-            const double* v = values + 2 * (size_t(f * K + k) * S + s2);
-            if (rot[size_t(f) * K + k]) {  // -i (x + i y) = y - i x
-              re = v[1];
-              im = -v[0];
-            } else {
-              re = v[0];
-              im = v[1];
-            }
-          };
-          double ar, ai, br, bi;
-          hk(a, ar, ai);
-          hk(b, br, bi);
-          const size_t o = (size_t(f * Kp + pi) * Bx + (kx[s2] - lox)) * By + (ky[s2] - loy);
-          hc[o] = lg::C32{float(ar - bi), float(ai + br)};                      // H_a + i H_b
-          ha[o] = lg::C32{float(wa * ar - wb * bi), float(wa * ai + wb * br)};  // w_a H_a + i w_b H_b
+          const size_t o = ((size_t(f) * KS + sl) * Bx + (kx[s2] - lox)) * By + (ky[s2] - loy);
+          double ar, ai;
+          kval(a, s2, stack_ok[f] != 0, ar, ai);
+          if (b >= 0) {  // pair: H_a + i H_b, adjoint w_a H_a + i w_b H_b
+            double br, bi;
+            kval(b, s2, true, br, bi);
+            hc[o] = lg::C32{float(ar - bi), float(ai + br)};
+            ha[o] = lg::C32{float(wa * ar - wb * bi), float(wa * ai + wb * br)};
+          } else {  // single kernel in its own slot
+            hc[o] = lg::C32{float(ar), float(ai)};
+            ha[o] = lg::C32{float(wa * ar), float(wa * ai)};
+          }
         }
       }
+    }
     auto up = [](DevBuf& d, const void* h, size_t bytes) {
       d.ensure(bytes);
       LG_CUDA(cudaMemcpy(d.p, h, bytes, cudaMemcpyHostToDevice));
@@ -717,9 +735,15 @@ struct Plan : PlanBase {
     up(wRe, wr.data(), wr.size() * sizeof(float));
     up(wIm, wi.data(), wi.size() * sizeof(float));
     up(wOne, one.data(), one.size() * sizeof(float));
-    fg.K = Kp;
+    if (mixed) {
+      up(slotOn, on.data(), on.size() * sizeof(int));
+      fg.slot_on = slotOn.as<int>();
+    }
+    fg.K = KS;
     paired = true;
   }
+  DevBuf slotOn;
+
   // weights / adjoint band of the fast kernels (paired or per kernel)
   const float* fw1() const { return paired ? wRe.as<float>() : wkf.as<float>(); }
   const float* fw2() const { return paired ? wIm.as<float>() : nullptr; }
@@ -1804,6 +1828,8 @@ lithogpu_status lithogpu_intensity_gradient(lithogpu_kernels* ks, int focus, con
       std::swap(P.H.p, Hf.p);
       std::swap(P.wk.p, wf.p);
       const int fgF0 = P.fg.F;
+      const int* slot0 = P.fg.slot_on;
+      if (P.fast && slot0) P.fg.slot_on = slot0 + size_t(P.frep(focus)) * P.fg.K;  // mixed pairs: this stack's slots
       P.F = 1;
       P.g.F = 1;
       P.fg.F = 1;
@@ -1818,6 +1844,7 @@ lithogpu_status lithogpu_intensity_gradient(lithogpu_kernels* ks, int focus, con
         P.F = F0;
         P.g = g0;
         P.fg.F = fgF0;
+        P.fg.slot_on = slot0;
         throw;
       }
       if (P.fast) std::swap(P.Ht.p, Htf.p);
@@ -1828,6 +1855,7 @@ lithogpu_status lithogpu_intensity_gradient(lithogpu_kernels* ks, int focus, con
       P.F = F0;
       P.g = g0;
       P.fg.F = fgF0;
+      P.fg.slot_on = slot0;
       const bool host = og.finish();
       if (host || !is_device_ptr(mask)) LG_CUDA(cudaStreamSynchronize(ctx->stream));
     };

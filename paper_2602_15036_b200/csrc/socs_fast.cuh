@@ -260,6 +260,7 @@ __global__ void __launch_bounds__(256, LG_SOCSROWS_MINB) fk_socs_rows(FGeo g, co
   for (int e = 0; e < E; ++e) acc[e] = 0.f;
   for (int k = G.gid; k < K; k += G.groups) {
     const int fk = f * K + k;
+    if (g.slot_on && !g.slot_on[fk]) continue;  // empty slot (mixed kernel pairs)
     const C32* src = T + blockIdx.z * t_ts + size_t(fk) * ny * Bx + size_t(sy) * Bx;
     C32 v[E];
 #pragma unroll
@@ -451,6 +452,7 @@ __global__ void __launch_bounds__(256, LG_ADJROWS_MINB) fk_adj_rows(FGeo g, cons
   constexpr int E = RPlan<L>::E;
   const int ny = g.ay.n, Bx = g.ax.B, K = g.K, lo = g.ax.lo, hi = g.ax.hi;
   const int fk = blockIdx.y, f = fk / K;
+  if (g.slot_on && !g.slot_on[fk]) return;  // empty slot: U never read
   const int r0 = blockIdx.x * G.groups;
   const int sy0 = r0 + G.gid;
   const bool act = sy0 < ny;
@@ -632,6 +634,7 @@ __global__ void __launch_bounds__(512) fk_socs_cols(FGeo g, const C32* __restric
   TraceScope trace_(g);
   constexpr int E = RPlan<L>::E;
   const int Bx = g.ax.B, By = g.ay.B, fk = blockIdx.y;
+  if (g.slot_on && !g.slot_on[fk]) return;  // empty slot: T never read
   const int c0 = blockIdx.x * G.groups;
   const int cx0 = c0 + G.gid;
   const bool act = cx0 < Bx;
@@ -827,12 +830,13 @@ __global__ void __launch_bounds__(256) fk_adj_cols(FGeo g, const C32* __restrict
   constexpr int E = RPlan<L>::E;
   const int Bx = g.ax.B, By = g.ay.B, cx = blockIdx.x, fk = blockIdx.y * G.groups + G.gid;
   const float sc = float(2.0 / (double(g.ax.n) * double(g.ay.n)));  // 2 (N/n)^2 / N^2
+  const bool on = !g.slot_on || g.slot_on[fk];  // empty slot contributes 0
   const C32* src = U + blockIdx.z * u_ts + (size_t(fk) * Bx + cx) * L;
   C32 v[E];
 #pragma unroll
-  for (int e = 0; e < E; ++e) v[e] = src[G.idx(e)];
-  fftr<float, L, -1>(v, G.sm, g.twny, G.t, G.sync);
-  const float w = wk[fk] * dose * sc;
+  for (int e = 0; e < E; ++e) v[e] = on ? src[G.idx(e)] : mk(0.f, 0.f);
+  if (on) fftr<float, L, -1>(v, G.sm, g.twny, G.t, G.sync);
+  const float w = on ? wk[fk] * dose * sc : 0.f;
   const C32* h = H + (size_t(fk) * Bx + cx) * By;  // column-major [fk][cx][jy]
   G.sync();
 #pragma unroll

@@ -23,6 +23,9 @@ struct FGeo {
   // launch `trace_slot`, kTraceCtas CTAs per slot; null = off
   unsigned long long* trace = nullptr;
   int trace_slot = 0;
+  // mixed kernel pairs (Plan::make_pairs): 0 marks an empty kernel slot that
+  // every kernel skips; null = all slots active
+  const int* slot_on = nullptr;
 };
 constexpr int kTraceCtas = 4096;
 

@@ -412,3 +412,40 @@ def test_evaluate_epe_f32_kernels(ctx):
     both = ~o32 & ~o64
     assert (o32 != o64).sum() <= 2  # a gauge exactly at the search radius may flip
     assert np.abs(e32[both] - e64[both]).max() < 0.05  # nm; fp32 intensity 1e-4 rel near the threshold
+
+
+def test_mixed_kernel_pairs_through_focus(ctx, monkeypatch):
+    """through-focus set (-40, 0, 40): the in-focus stack runs as kernel pairs
+    inside the same launches as the defocused (unpaired, mirror-merged)
+    stack; images, gradients and ILT cost against the oracle and against the
+    unpaired path."""
+    n = 256
+    foci = (-40.0, 0.0, 40.0)
+    ks = kernels_for(n, 1.0, foci, k=8, grid_n=21)
+    dk = L.DeviceKernels(ks, "f32", ctx)
+    info = dk.info()
+    assert info["fast_stacks"] == 2 and info["fast_order"] == 8
+    rng = np.random.default_rng(53)
+    mask = (rng.random((n, n)) > 0.5).astype(np.float64)
+    W = rng.standard_normal((n, n))
+    for f in range(3):
+        want = O.image_socs(mask, ks.weights[f], ks.support, ks.values[f])
+        assert rel_linf(dk.image(mask, focus=f)["intensity"], want) < 1e-4
+        gw = O.weighted_gradient(mask, ks.weights[f], ks.support, ks.values[f], W, dose=1.0)
+        assert rel_linf(dk.gradient(mask, 1.0, weight=W, focus=f), gw) < 1e-4
+    prm = L.IltParams(step=0.05, focus_weights=[0.25, 0.5, 0.25])
+    th0 = rng.standard_normal((n, n)) * 0.5
+    out = []
+    for nopair in ("", "1"):
+        if nopair:
+            monkeypatch.setenv("LITHOGPU_NO_PAIRS", "1")
+        d = L.DeviceKernels(ks, "f32", ctx)
+        s = L.IltSolver(d, prm, 1, "f32", ctx)
+        s.set_tiles(mask[None], th0[None])
+        out.append((s.run(2), s.get_tiles()[0]))
+    th = th0.copy()
+    c_ref, _ = O.ilt_iteration(th, mask, ks.weights, ks.support, ks.values, [0.25, 0.5, 0.25],
+                               [4.0, 30.0, 0.25, 2.0, 1.0, 0.05], 1.0)
+    assert abs(out[0][0][0, 0] - c_ref) <= 1e-4 * abs(c_ref)
+    assert np.abs(out[0][0] - out[1][0]).max() <= 1e-4 * np.abs(out[1][0]).max()
+    assert rel_linf(out[0][1] - th0, out[1][1] - th0) < 1e-3
