@@ -135,11 +135,11 @@ def fft_flops(L):
 
 def store_e(geo, F, K, tiles=1):
     """Mirror of Plan::reserve: the ILT keeps E_fk for the adjoint rows while
-    F*K*n^2 complex64 per launch stays <= 96 MiB (LITHOGPU_STORE_E overrides)."""
+    F*K*n^2 complex64 per launch stays <= 8 GiB (LITHOGPU_STORE_E overrides)."""
     env = os.environ.get("LITHOGPU_STORE_E")
     if env is not None:
         return env.startswith("1")
-    return 8 * F * K * geo["n"] ** 2 * tiles <= (96 << 20)
+    return 8 * F * K * geo["n"] ** 2 * tiles <= (8 << 30)
 
 
 def kernel_model(geo, F, K, tiles=1):
