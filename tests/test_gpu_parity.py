@@ -449,3 +449,52 @@ def test_mixed_kernel_pairs_through_focus(ctx, monkeypatch):
     assert abs(out[0][0][0, 0] - c_ref) <= 1e-4 * abs(c_ref)
     assert np.abs(out[0][0] - out[1][0]).max() <= 1e-4 * np.abs(out[1][0]).max()
     assert rel_linf(out[0][1] - th0, out[1][1] - th0) < 1e-3
+
+
+def test_batched_tiles_match_single_tile_runs(ctx):
+    """tiles batched on blockIdx.z (the chip-scale launches) compute each tile
+    exactly as a one-tile run: costs and theta bitwise equal."""
+    n, T = 256, 3
+    ks = kernels_for(n, 1.0, (-40.0, 0.0, 40.0), k=8, grid_n=21)
+    dk = L.DeviceKernels(ks, "f32", ctx)
+    rng = np.random.default_rng(61)
+    targets = (rng.random((T, n, n)) > 0.5).astype(np.float64)
+    th0 = rng.standard_normal((T, n, n)) * 0.5
+    prm = L.IltParams(step=0.05, focus_weights=[0.25, 0.5, 0.25])
+    sb = L.IltSolver(dk, prm, T, "f32", ctx)
+    sb.set_tiles(targets, th0)
+    cb = sb.run(3)
+    thb = sb.get_tiles()[0]
+    for t in range(T):
+        s1 = L.IltSolver(dk, prm, 1, "f32", ctx)
+        s1.set_tiles(targets[t:t + 1], th0[t:t + 1])
+        c1 = s1.run(3)
+        assert np.array_equal(c1[:, 0], cb[:, t])
+        assert np.array_equal(s1.get_tiles()[0][0], thb[t])
+        s1.close()
+
+
+def test_chip_ilt_tiles_and_costs(ctx):
+    """chip.ChipIlt on a 2x2-tile window (world 1): the global per-iteration
+    cost is the sum of the per-tile costs of independent one-tile runs."""
+    from paper_2602_15036_b200 import chip, layouts as LY
+    core, halo = 96, 16
+    n = core + 2 * halo
+    chipg = L.Grid(2 * core, 2 * core, 1.0, 0.0, 0.0)
+    tiling = LY.Tiling(chipg, core, halo)
+    polys = LY.line_space_contacts(2 * core, 2 * core, seed=12)
+    ks = kernels_for(n, 1.0, (0.0,), k=8, grid_n=21)
+    prm = L.IltParams(step=0.05, focus_weights=[1.0])
+    ci = chip.ChipIlt(tiling, polys, ks, prm, ctx)
+    res = ci.run(4, sync_every=2)
+    assert len(res.cost) == 4 and list(res.tiles) == [0, 1, 2, 3]
+    tot = np.zeros(4)
+    from paper_2602_15036_b200 import layouts
+    for t in range(4):
+        g = tiling.tile_grid(t)
+        raster = L.rasterize_layer(tiling.tile_polygons(polys, t), g, 1.0, ctx)
+        s = L.IltSolver(ks, prm, 1, "f32", ctx)
+        s.set_tiles(raster[None].astype(np.float32))
+        tot += s.run(4)[:, 0]
+    assert np.abs(res.cost - tot).max() <= 1e-6 * np.abs(tot).max()
+    assert np.all(res.gmax > 0)
