@@ -95,9 +95,30 @@ __host__ __device__ constexpr int swz_len(int L) {
   return (SW == 0) ? L + (L >> 4) + 1 : (SW == 4) ? L + (L >> 5) + 1 : L;
 }
 
+// swz<SW>(i + C) == swz<SW>(i) + lin_delta<SW>(C) for every i >= 0 when
+// lin_ok<SW>(C): the exchange addresses of a stage are then one swizzle per
+// thread plus compile-time offsets.
+template <int SW>
+__host__ __device__ constexpr bool lin_ok(int C) {
+  return SW == 0 ? C % 16 == 0 : (SW == 1 ? C % 128 == 0 : (SW == 4 ? C % 32 == 0 : false));
+}
+template <int SW>
+__host__ __device__ constexpr int lin_delta(int C) {
+  return SW == 0 ? C + C / 16 : (SW == 4 ? C + C / 32 : C);
+}
+
 template <int SW>
 struct Xch2 {  // float2 cells
   static constexpr bool soa = false;
+  static constexpr int sw = SW;
+  template <typename T>
+  static __device__ __forceinline__ void st_raw(void* sm, int p, cx<T> v) {
+    reinterpret_cast<cx<T>*>(sm)[p] = v;
+  }
+  template <typename T>
+  static __device__ __forceinline__ cx<T> ld_raw(const void* sm, int p) {
+    return reinterpret_cast<const cx<T>*>(sm)[p];
+  }
   template <int L>
   __host__ __device__ static constexpr int bytes() { return swz_len<SW>(L) * 8; }
   template <typename T>
@@ -112,6 +133,7 @@ struct Xch2 {  // float2 cells
 template <int SW>
 struct XchS {  // split re / im
   static constexpr bool soa = true;
+  static constexpr int sw = -1;  // no linear fast path
   template <int L>
   __host__ __device__ static constexpr int bytes() { return 2 * swz_len<SW>(L) * 4; }
   template <typename T>
@@ -194,11 +216,21 @@ __device__ __forceinline__ void fftr_stage(cx<T> (&v)[RPlan<L>::E], cx<T>* sm,
       for (int r = 1; r < R; ++r) w[b][r] = ldg_cx(tw + G::tw_off + (r - 1) * Ns + k);
     }
   }
+  constexpr int SW = X::sw;
   if constexpr (FIRST) {
 #pragma unroll
     for (int b = 0; b < NB; ++b)
 #pragma unroll
       for (int r = 0; r < R; ++r) x[b][r] = v[b + r * NB];
+  } else if constexpr (SW >= 0 && lin_ok<(SW < 0 ? 0 : SW)>(TPR) && lin_ok<(SW < 0 ? 0 : SW)>(L / R)) {
+    // one swizzle per thread, compile-time offsets
+    constexpr int SWc = SW < 0 ? 0 : SW;
+    const int p0 = swz<SWc>(t);
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        x[b][r] = X::template ld_raw<T>(sm, p0 + b * lin_delta<SWc>(TPR) + r * lin_delta<SWc>(L / R));
   } else {
 #pragma unroll
     for (int b = 0; b < NB; ++b)
@@ -224,13 +256,25 @@ __device__ __forceinline__ void fftr_stage(cx<T> (&v)[RPlan<L>::E], cx<T>* sm,
       for (int r = 0; r < R; ++r) v[b + r * NB] = x[b][r];
   } else {
     sync();  // every thread finished reading sm (previous stage / previous use)
+    constexpr int SWc = SW < 0 ? 0 : SW;
+    if constexpr (SW >= 0 && TPR % Ns == 0 && lin_ok<SWc>(Ns) && lin_ok<SWc>(TPR * R)) {
+      // k = j mod Ns is the same for every butterfly of the thread
+      const int k = t % Ns;
+      const int p0 = swz<SWc>((t - k) * R + k);
 #pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      const int j = t + b * TPR;
-      const int k = j % Ns;
-      const int base = (j - k) * R + k;
+      for (int b = 0; b < NB; ++b)
 #pragma unroll
-      for (int r = 0; r < R; ++r) X::template st<T>(sm, L, base + r * Ns, x[b][r]);
+        for (int r = 0; r < R; ++r)
+          X::template st_raw<T>(sm, p0 + b * lin_delta<SWc>(TPR * R) + r * lin_delta<SWc>(Ns), x[b][r]);
+    } else {
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int j = t + b * TPR;
+        const int k = j % Ns;
+        const int base = (j - k) * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) X::template st<T>(sm, L, base + r * Ns, x[b][r]);
+      }
     }
     sync();
     fftr_stage<T, L, SIGN, S + 1, X>(v, sm, tw, t, sync);
