@@ -40,13 +40,9 @@ LG_RPLAN(128, 16, 16, 8)
 LG_RPLAN(256, 16, 16, 16)
 LG_RPLAN(512, 8, 8, 8, 8)
 LG_RPLAN(1024, 16, 16, 8, 8)
-// 2048: 8*8*8*4 on 256 threads measured ahead of 16*16*8 on 128 inside the
-// full-resolution row kernels (more, shorter warps per row pair)
-#ifdef LG_PLAN2048_E16
-LG_RPLAN(2048, 16, 16, 16, 8)
-#else
-LG_RPLAN(2048, 8, 8, 8, 8, 4)
-#endif
+// 2048 = 8*4*8*8 on 256 threads: in-graph A/B at C2 against 8*8*8*4 (-1.0 %),
+// 4*8*8*8, 8*8*4*8 and the E = 16 plans 16*16*8, 16*8*16, 8*16*16 (+3-6 %)
+LG_RPLAN(2048, 8, 8, 4, 8, 8)
 LG_RPLAN(4096, 16, 16, 16, 16)
 LG_RPLAN(8192, 16, 16, 16, 16, 2)
 LG_RPLAN(192, 12, 12, 4, 4)
