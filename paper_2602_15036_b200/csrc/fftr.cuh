@@ -49,7 +49,9 @@ LG_RPLAN(192, 12, 12, 4, 4)
 // 384 = 4*6*4*4: in-graph A/B at C2 against 12*4*4*2 (-1.5 %), 4*4*4*6,
 // 4*4*6*4, 6*4*4*4, 4*4*2*12 and the E = 24 plans 8*6*8 / 6*8*8 (+16-26 %)
 LG_RPLAN(384, 12, 4, 6, 4, 4)
-LG_RPLAN(768, 12, 12, 4, 4, 4)
+// 768 = 4*4*4*12: C4 A/B against 12*4*4*4 (+5 % tile-iter/s), 4*12*4*4 (+3 %),
+// 8*6*4*4 (E = 24, -1 %)
+LG_RPLAN(768, 12, 4, 4, 4, 12)
 LG_RPLAN(1536, 12, 12, 4, 4, 4, 2)
 LG_RPLAN(3072, 12, 12, 4, 4, 4, 4)
 #undef LG_RPLAN

@@ -498,3 +498,19 @@ def test_chip_ilt_tiles_and_costs(ctx):
         tot += s.run(4)[:, 0]
     assert np.abs(res.cost - tot).max() <= 1e-6 * np.abs(tot).max()
     assert np.all(res.gmax > 0)
+
+
+def test_c4_scale_image_and_gradient(ctx):
+    """4096^2 tiles (C4: N = 4096 plans, decimated n = 768 plans) against the
+    oracle: aerial image and weighted gradient, fp32 1e-4."""
+    n = 4096
+    ks = kernels_for(n, 1.0, (40.0,), k=4, grid_n=21)
+    rng = np.random.default_rng(97)
+    mask = (rng.random((n, n)) > 0.5).astype(np.float64)
+    dk = L.DeviceKernels(ks, "f32", ctx)
+    assert dk.info()["nx_sub"] == 768
+    want = O.image_socs(mask, ks.weights[0], ks.support, ks.values[0])
+    assert rel_linf(dk.image(mask)["intensity"], want) < 1e-4
+    W = rng.standard_normal((n, n))
+    gw = O.weighted_gradient(mask, ks.weights[0], ks.support, ks.values[0], W, dose=1.0)
+    assert rel_linf(dk.gradient(mask, 1.0, weight=W), gw) < 1e-4
