@@ -15,31 +15,31 @@ using namespace lg;
 template <int LG, typename X>
 __global__ void sweep_kernel(const cx<float>* __restrict__ in, cx<float>* __restrict__ out,
                              const cx<float>* __restrict__ tw, int rows, int reps) {
-  constexpr int E = RPlan<LG>::E, TPR = RPlan<LG>::TPR, L = 1 << LG;
+  constexpr int E = RPlan<(1 << LG)>::E, TPR = RPlan<(1 << LG)>::TPR, L = 1 << LG;
   extern __shared__ __align__(16) unsigned char raw[];
   const int groups = blockDim.x / TPR, gid = threadIdx.x / TPR, t = threadIdx.x % TPR;
   const int row = blockIdx.x * groups + gid;
-  const int bytes = (X::template bytes<LG>() + 15) / 16 * 16;
+  const int bytes = (X::template bytes<(1 << LG)>() + 15) / 16 * 16;
   cx<float>* sm = reinterpret_cast<cx<float>*>(raw + size_t(gid) * bytes);
-  const GSync sync = make_gsync<LG>(gid, groups);
+  const GSync sync = make_gsync<(1 << LG)>(gid, groups);
   const int r = row < rows ? row : rows - 1;
   cx<float> v[E];
   for (int e = 0; e < E; ++e) v[e] = in[size_t(r) * L + t + e * TPR];
-  for (int k = 0; k < reps; ++k) fftr<float, LG, -1, X>(v, sm, tw, t, sync);
+  for (int k = 0; k < reps; ++k) fftr<float, (1 << LG), -1, X>(v, sm, tw, t, sync);
   if (row < rows)
     for (int e = 0; e < E; ++e) out[size_t(row) * L + t + e * TPR] = v[e];
 }
 
 template <int LG, typename X>
 void run(const char* name, int rows) {
-  constexpr int L = 1 << LG, TPR = RPlan<LG>::TPR;
+  constexpr int L = 1 << LG, TPR = RPlan<(1 << LG)>::TPR;
   std::vector<cx<float>> h(size_t(rows) * L), o(size_t(rows) * L);
   for (size_t i = 0; i < h.size(); ++i) {
     h[i].x = float(std::sin(0.37 * double(i)) + 0.1 * double(i % 7));
     h[i].y = float(std::cos(0.11 * double(i)));
   }
-  std::vector<cx<float>> tw(TwLen<LG>::value + 1);
-  fill_rtwiddles<LG>([&](int idx, int rk, int NsR) {
+  std::vector<cx<float>> tw(TwLen<(1 << LG)>::value + 1);
+  fill_rtwiddles<(1 << LG)>([&](int idx, int rk, int NsR) {
     const double a = 2.0 * M_PI * double(rk) / double(NsR);
     tw[idx].x = float(std::cos(a));
     tw[idx].y = float(-std::sin(a));
@@ -51,7 +51,7 @@ void run(const char* name, int rows) {
   cudaMemcpy(din, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
   cudaMemcpy(dtw, tw.data(), tw.size() * 8, cudaMemcpyHostToDevice);
   const int groups = TPR >= 256 ? 1 : 256 / TPR;
-  const int bytes = (X::template bytes<LG>() + 15) / 16 * 16;
+  const int bytes = (X::template bytes<(1 << LG)>() + 15) / 16 * 16;
   const size_t smem = size_t(groups) * bytes;
   cudaFuncSetAttribute(sweep_kernel<LG, X>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   const int grid = (rows + groups - 1) / groups;
