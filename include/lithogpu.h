@@ -178,6 +178,13 @@ lithogpu_status lithogpu_ilt_set_tiles(lithogpu_ilt* ilt, const void* target,
  * max |dcost/dtheta| per iteration and tile, same layout. */
 lithogpu_status lithogpu_ilt_run(lithogpu_ilt* ilt, int iterations, double* cost,
                                  double* gmax);
+/* Cost and exact gradient dcost/dtheta at the CURRENT theta of every tile,
+ * without updating theta (one iteration of the same kernels with step 0).
+ * cost (nullable): n_tiles f64; grad: n_tiles*nx*ny of `dtype` (F32/F64),
+ * host or device.  The oracle twin is orc_ilt_iteration's grad_out
+ * (oracle/litho_oracle.c); W = 1 reduces it to intensity_gradient
+ * (ai.cpp:11-42) chained through the resist and mask sigmoids. */
+lithogpu_status lithogpu_ilt_gradient(lithogpu_ilt* ilt, double* cost, void* grad, lithogpu_dtype dtype);
 /* theta and/or mask = sigmoid(steepness*theta) of one tile (nullable outs) */
 lithogpu_status lithogpu_ilt_get_tile(lithogpu_ilt* ilt, int tile, void* theta, void* mask,
                                       lithogpu_dtype dtype);

@@ -549,17 +549,25 @@ def evaluate_epe(masks, kernels, gauges, dose: float, sigma_nm: float, t_eff: fl
     measure_epe, imaged in one batched launch sequence.
     Returns (epe [m, n], open [m, n] bool[, resist [m, ny, nx]])."""
     dk = _kernels_on_device(kernels, precision, ctx)
-    single = np.ndim(masks) == 2
-    m = np.ascontiguousarray(masks, np.float64)
-    if single:
-        m = m[None]
+    single = len(tuple(masks.shape) if hasattr(masks, "shape") else np.shape(masks)) == 2
+    if _is_torch(masks):  # device-resident masks stay on the device
+        m = masks[None] if single else masks
+        finite = bool(torch.isfinite(m).all())
+    else:
+        m = np.ascontiguousarray(masks, np.float64)
+        if single:
+            m = m[None]
+        finite = bool(np.isfinite(m).all())
+    if not finite:  # the resist field would be non-finite (reference contour.cpp:62-63)
+        raise ValueError("evaluate_epe: non-finite mask")
+    mp, mdt, keep = _buf(m)
     nm = m.shape[0]
     g = np.ascontiguousarray(gauges, np.float64).reshape(-1, 4)
     n = g.shape[0]
     epe = np.zeros((nm, max(n, 1)), np.float64)
     op = np.zeros((nm, max(n, 1)), np.uint8)
-    res = np.zeros(m.shape, np.float64) if want_resist else None
-    check(lib().lithogpu_evaluate_epe(dk.handle, focus, nm, m.ctypes.data, F64, dose, sigma_nm, t_eff,
+    res = np.zeros(tuple(m.shape), np.float64) if want_resist else None
+    check(lib().lithogpu_evaluate_epe(dk.handle, focus, nm, mp, mdt, dose, sigma_nm, t_eff,
                                       g.ctypes.data if n else None, n, search_radius_nm, epe.ctypes.data,
                                       op.ctypes.data, res.ctypes.data if want_resist else None))
     out = (epe[:, :n], op[:, :n].astype(bool))
@@ -619,6 +627,10 @@ class IltSolver:
         self.dk = _kernels_on_device(kernels, precision, ctx)
         F = self.dk.F
         fw = params.focus_weights if params.focus_weights is not None else [1.0 / F] * F
+        if len(fw) != F:
+            raise ValueError(f"IltParams.focus_weights: {len(fw)} weights for {F} focus stacks")
+        if not all(math.isfinite(float(c)) and float(c) >= 0 for c in fw):
+            raise ValueError("IltParams.focus_weights: weights must be finite and >= 0")
         self._fw = (C.c_double * F)(*fw)
         self.params = params
         p = _lib.IltParams(params.mask_steepness, params.resist_beta, params.threshold,
@@ -646,6 +658,18 @@ class IltSolver:
         check(lib().lithogpu_ilt_run(self._h, iterations, cost.ctypes.data,
                                      gmax.ctypes.data if with_gmax else None))
         return (cost, gmax) if with_gmax else cost
+
+    def gradient(self, like=None, dtype=None):
+        """(cost [n_tiles], dcost/dtheta [n_tiles, ny, nx]) at the current
+        theta, theta unchanged (lithogpu_ilt_gradient).  `like`: a CUDA tensor
+        to allocate the gradient next to (device-resident result)."""
+        dt = dtype if dtype is not None else (F32 if self.dk.precision == "f32" else F64)
+        shape = (self.n_tiles, self.grid.ny, self.grid.nx)
+        g = _empty_like(like if like is not None else np.empty(0), shape, dt)
+        cost = np.zeros(self.n_tiles)
+        gp = g.data_ptr() if _is_torch(g) else g.ctypes.data
+        check(lib().lithogpu_ilt_gradient(self._h, cost.ctypes.data, gp, dt))
+        return cost, g
 
     def run_device(self, iterations: int, cost_dev=None, gmax_dev=None):
         """Enqueue without host sync of results (cost_dev / gmax_dev: device

@@ -52,7 +52,7 @@ class ChipIlt:
         import torch
 
         from . import api
-        from .layouts import polygon_arrays
+        from .layouts import polygon_arrays, polygon_bboxes
         self.tiling = tiling
         self.rank, self.world = rank, world
         self.mine = shard(len(tiling), world, rank)
@@ -60,24 +60,34 @@ class ChipIlt:
         n = tiling.n
         dev = torch.device("cuda", ctx.device)
         self.target = torch.empty((len(self.mine), n, n), dtype=torch.float64, device=dev)
+        bb = polygon_bboxes(polys)
         for j, t in enumerate(self.mine):
             g = tiling.tile_grid(t)
-            tp = tiling.tile_polygons(polys, t, dbu_per_nm)
+            tp = tiling.tile_polygons(polys, t, dbu_per_nm, bboxes=bb)
             xy, st = polygon_arrays(tp)
             _raster(ctx, g, xy, st, self.target[j], dbu_per_nm)
-        self.solver = api.IltSolver(kernels, params, max(1, len(self.mine)), "f32", ctx)
+        # a rank with an empty shard (world > tiles) runs no solver and
+        # contributes zero cost / gmax to the all-reduce
+        self.solver = api.IltSolver(kernels, params, len(self.mine), "f32", ctx) if len(self.mine) else None
         self.target32 = self.target.float().contiguous()
-        self.solver.set_tiles(self.target32)
+        if self.solver is not None:
+            self.solver.set_tiles(self.target32)
 
     def run(self, iters: int, want_mask: bool = False, sync_every: Optional[int] = None,
             tol: Optional[float] = None) -> ChipResult:
         """`iters` ILT iterations of this rank's tiles (see segmented_ilt)."""
-        gl_cost, gl_gmax = segmented_ilt(self.solver.run_device, iters, self.solver.n_tiles, sync_every, tol,
-                                         self.target.device)
+        if self.solver is None:
+            def run_segment(k, cost, gmax):  # empty shard: zero partials
+                cost.zero_()
+                gmax.zero_()
+            n_tiles = 1
+        else:
+            run_segment, n_tiles = self.solver.run_device, self.solver.n_tiles
+        gl_cost, gl_gmax = segmented_ilt(run_segment, iters, n_tiles, sync_every, tol, self.target.device)
         res = ChipResult(gl_cost, gl_gmax, self.mine)
         if want_mask:
-            _, m = self.solver.get_tiles()
-            res.mask = m
+            n = self.tiling.n
+            res.mask = self.solver.get_tiles()[1] if self.solver is not None else np.zeros((0, n, n))
         return res
 
 

@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -107,6 +108,28 @@ struct DevBuf {
   T* as() const {
     return static_cast<T*>(p);
   }
+};
+
+// Host -> device upload of a freshly built table that returns only when the
+// bytes are in device memory.  A plain cudaMemcpy from pageable memory may
+// return once the data is staged, before the DMA lands; the tables are then
+// read by kernels on the context's (non-blocking) stream, which does not
+// order against the legacy stream — so wait for the legacy stream here.
+inline void h2d_blocking(void* dst, const void* src, size_t bytes) {
+  LG_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+  LG_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
+}
+
+// Non-owning view of a device table (Plan::set_sigma's per-sigma tables).
+struct TabView {
+  void* p = nullptr;
+  template <typename U>
+  U* as() const {
+    return static_cast<U*>(p);
+  }
+};
+struct GTab {
+  DevBuf x, y;
 };
 
 // Stream-ordered pool allocation (cudaMallocAsync) for per-call scratch of the
@@ -432,7 +455,7 @@ void make_twiddles(int L, DevBuf& buf) {
     h[m].y = T(-std::sin(a));
   }
   buf.ensure(sizeof(lg::cx<T>) * L);
-  LG_CUDA(cudaMemcpy(buf.p, h.data(), sizeof(lg::cx<T>) * L, cudaMemcpyHostToDevice));
+  h2d_blocking(buf.p, h.data(), sizeof(lg::cx<T>) * L);
 }
 
 // 1-D DFT of the reference's truncated unit-sum Gaussian on an N-grid
@@ -491,8 +514,12 @@ struct Plan : PlanBase {
   int F = 0, K = 0;
   DevBuf twNx, twNy, twnx, twny, H, wk;
   // Gaussian transfer cache
+  // Gaussian band tables, one immutable device table per resist sigma: a
+  // solver or image() call with another sigma never overwrites a table that
+  // queued work (or a captured ILT graph) still reads.
+  std::map<double, std::unique_ptr<GTab>> gtabs;
   double gsig = -1.0;
-  DevBuf gxh, gyb;
+  TabView gxh, gyb;
   // work buffers (sized for `cap` tiles)
   int cap = 0;
   DevBuf Mr, Mhat, Tb, Ir, Ic, Rc, Dr, Wc, U, Acc, Gc, costrow, gmaxrow;
@@ -559,11 +586,11 @@ struct Plan : PlanBase {
         dst.y = T(values[2 * (size_t(fk) * S + s) + 1]);
       }
     H.ensure(h.size() * sizeof(C));
-    LG_CUDA(cudaMemcpy(H.p, h.data(), h.size() * sizeof(C), cudaMemcpyHostToDevice));
+    h2d_blocking(H.p, h.data(), h.size() * sizeof(C));
     std::vector<T> w(size_t(F) * K);
     for (size_t i = 0; i < w.size(); ++i) w[i] = T(weights[i]);
     wk.ensure(w.size() * sizeof(T));
-    LG_CUDA(cudaMemcpy(wk.p, w.data(), w.size() * sizeof(T), cudaMemcpyHostToDevice));
+    h2d_blocking(wk.p, w.data(), w.size() * sizeof(T));
     // strides (elements)
     const auto& ax = g.ax;
     const auto& ay = g.ay;
@@ -591,7 +618,7 @@ struct Plan : PlanBase {
           std::vector<lg::C32> h(std::max(1, lg::fast_tw_len(len)));
           lg::fast_fill_twiddles(len, h.data());
           b.ensure(h.size() * sizeof(lg::C32));
-          LG_CUDA(cudaMemcpy(b.p, h.data(), h.size() * sizeof(lg::C32), cudaMemcpyHostToDevice));
+          h2d_blocking(b.p, h.data(), h.size() * sizeof(lg::C32));
           return b.as<lg::C32>();
         };
         // focus stacks computed on the fast path (mirror stacks merged)
@@ -608,12 +635,12 @@ struct Plan : PlanBase {
                   ht[((size_t(r) * K + k) * Bx + jx) * By + jy] = lg::C32{float(src.x), float(src.y)};
                 }
           Ht.ensure(ht.size() * sizeof(lg::C32));
-          LG_CUDA(cudaMemcpy(Ht.p, ht.data(), ht.size() * sizeof(lg::C32), cudaMemcpyHostToDevice));
+          h2d_blocking(Ht.p, ht.data(), ht.size() * sizeof(lg::C32));
           std::vector<float> wf(size_t(Fc) * K);
           for (int r = 0; r < Fc; ++r)
             for (int k = 0; k < K; ++k) wf[size_t(r) * K + k] = float(weights[size_t(rep_src[r]) * K + k]);
           wkf.ensure(wf.size() * sizeof(float));
-          LG_CUDA(cudaMemcpy(wkf.p, wf.data(), wf.size() * sizeof(float), cudaMemcpyHostToDevice));
+          h2d_blocking(wkf.p, wf.data(), wf.size() * sizeof(float));
         }
         fg.twNx = table(Nx, ftNx);
         fg.twNy = table(Ny, ftNy);
@@ -729,7 +756,7 @@ struct Plan : PlanBase {
     }
     auto up = [](DevBuf& d, const void* h, size_t bytes) {
       d.ensure(bytes);
-      LG_CUDA(cudaMemcpy(d.p, h, bytes, cudaMemcpyHostToDevice));
+      h2d_blocking(d.p, h, bytes);
     };
     up(Ht, hc.data(), hc.size() * sizeof(lg::C32));
     up(Hadj, ha.data(), ha.size() * sizeof(lg::C32));
@@ -899,6 +926,13 @@ struct Plan : PlanBase {
 
   void set_sigma(double sigma_nm) {
     if (sigma_nm == gsig) return;
+    auto hit = gtabs.find(sigma_nm);
+    if (hit != gtabs.end()) {
+      gxh.p = hit->second->x.p;
+      gyb.p = hit->second->y.p;
+      gsig = sigma_nm;
+      return;
+    }
     const auto& ax = g.ax;
     const auto& ay = g.ay;
     std::vector<T> hx(ax.P + 1), hy(ay.nb2);
@@ -913,10 +947,14 @@ struct Plan : PlanBase {
       for (int p = 0; p <= ax.P; ++p) hx[p] = T(gauss_hat(ax.N, tx, rx, p));
       for (int j = 0; j < ay.nb2; ++j) hy[j] = T(gauss_hat(ay.N, ty, ry, lg::band2_p(ay, j)));
     }
-    gxh.ensure(hx.size() * sizeof(T));
-    gyb.ensure(hy.size() * sizeof(T));
-    LG_CUDA(cudaMemcpy(gxh.p, hx.data(), hx.size() * sizeof(T), cudaMemcpyHostToDevice));
-    LG_CUDA(cudaMemcpy(gyb.p, hy.data(), hy.size() * sizeof(T), cudaMemcpyHostToDevice));
+    auto tab = std::make_unique<GTab>();
+    tab->x.ensure(hx.size() * sizeof(T));
+    tab->y.ensure(hy.size() * sizeof(T));
+    h2d_blocking(tab->x.p, hx.data(), hx.size() * sizeof(T));
+    h2d_blocking(tab->y.p, hy.data(), hy.size() * sizeof(T));
+    gxh.p = tab->x.p;
+    gyb.p = tab->y.p;
+    gtabs.emplace(sigma_nm, std::move(tab));
     gsig = sigma_nm;
   }
 
@@ -1220,8 +1258,13 @@ struct lithogpu_ilt {
   }
 };
 
+// grad_dev (device, tiles x N^2, nullable): dL/dtheta of the LAST iteration;
+// step_override >= 0 replaces params.step (0: evaluate without moving theta —
+// theta - 0*g == theta exactly, so the mask spectrum re-derived by grad_rows
+// is unchanged).  Graph capture only for the plain run (grad_dev == nullptr).
 template <typename T>
-static void ilt_run_impl(lithogpu_ilt* ilt, int iters, double* cost_user, double* gmax_user) {
+static void ilt_run_impl(lithogpu_ilt* ilt, int iters, double* cost_user, double* gmax_user,
+                         T* grad_dev = nullptr, double step_override = -1.0) {
   using C = lg::cx<T>;
   Plan<T>& P = ilt->ks->p<T>();
   lithogpu_ctx* ctx = ilt->ks->ctx;
@@ -1233,7 +1276,8 @@ static void ilt_run_impl(lithogpu_ilt* ilt, int iters, double* cost_user, double
   ilt->cost.ensure(sizeof(double) * size_t(std::max(iters, 1)) * tiles);
   ilt->gmax.ensure(sizeof(double) * size_t(std::max(iters, 1)) * tiles);
   T* theta = ilt->theta.as<T>();
-  const T a = T(prm.mask_steepness), step = T(prm.step), beta = T(prm.resist_beta),
+  const T a = T(prm.mask_steepness), step = T(step_override >= 0 ? step_override : prm.step),
+          beta = T(prm.resist_beta),
           thr = T(prm.threshold), dose = T(prm.dose);
   // initial mask row pass (subsequent ones are fused into grad_rows)
   const bool need_prime = !(ilt->primed && P.mr_owner == ilt);
@@ -1285,7 +1329,8 @@ static void ilt_run_impl(lithogpu_ilt* ilt, int iters, double* cost_user, double
                            P.costrow.template as<double>(), P.s_cr, ncost, cost_it, 1);
         });
         P.fl("grad_rows", [&] {
-          lg::fl_grad_rows(fg, s, tiles, true, P.Gc.template as<C>(), P.s_Gc, nullptr, 0, theta, NN, a, step,
+          lg::fl_grad_rows(fg, s, tiles, true, P.Gc.template as<C>(), P.s_Gc, it + 1 == iters ? grad_dev : nullptr,
+                           NN, theta, NN, a, step,
                            P.Mr.template as<C>(), P.s_Mr, P.gmaxrow.template as<double>(), P.s_gm);
         });
         if (gmax_user) {
@@ -1311,7 +1356,7 @@ static void ilt_run_impl(lithogpu_ilt* ilt, int iters, double* cost_user, double
     P.adj_cols(dose, tiles);
     // cost of iteration `it` for each tile -> cost[it*tiles + tile]
     P.grad_cols(tiles, true, ilt->cost.as<double>() + size_t(it) * tiles, 1);
-    P.template grad_rows<true, T>(static_cast<T*>(nullptr), 0, theta, NN, a, step,
+    P.template grad_rows<true, T>(it + 1 == iters ? grad_dev : static_cast<T*>(nullptr), NN, theta, NN, a, step,
                                   P.gmaxrow.template as<double>(), tiles);
     if (gmax_user) {
       lg::k_reduce_max<<<tiles, 32, 0, ctx->stream>>>(
@@ -1326,7 +1371,8 @@ static void ilt_run_impl(lithogpu_ilt* ilt, int iters, double* cost_user, double
   if (trace_path) P.trace_reset();
   // CUDA graph of the whole `iters`-iteration launch sequence: captured on the
   // second call with an identical configuration, replayed afterwards.
-  const bool graphable = ctx->stream != nullptr && !ctx->profiling && iters > 0 &&
+  const bool graphable = ctx->stream != nullptr && !ctx->profiling && iters > 0 && !grad_dev &&
+                         step_override < 0 &&
                          !std::getenv("LITHOGPU_NO_GRAPH");
   if (!graphable) {
     enqueue();
@@ -2030,12 +2076,12 @@ lithogpu_status lithogpu_ilt_create(lithogpu_kernels* ks, const lithogpu_ilt_par
           c.assign(m.begin(), m.end());
           c.resize(size_t(ks->F), 0.f);
         }
-        LG_CUDA(cudaMemcpy(ilt->cfd.p, c.data(), 4 * c.size(), cudaMemcpyHostToDevice));
+        h2d_blocking(ilt->cfd.p, c.data(), 4 * c.size());
       } else {
-        LG_CUDA(cudaMemcpy(ilt->cfd.p, ilt->cf.data(), 8 * ilt->cf.size(), cudaMemcpyHostToDevice));
+        h2d_blocking(ilt->cfd.p, ilt->cf.data(), 8 * ilt->cf.size());
       }
-      LG_CUDA(cudaMemset(ilt->theta.p, 0, es * n));
-      LG_CUDA(cudaMemset(ilt->target.p, 0, es * n));
+      LG_CUDA(cudaMemsetAsync(ilt->theta.p, 0, es * n, ks->ctx->stream));
+      LG_CUDA(cudaMemsetAsync(ilt->target.p, 0, es * n, ks->ctx->stream));
     } catch (...) {
       delete ilt;
       throw;
@@ -2150,6 +2196,30 @@ lithogpu_status lithogpu_ilt_run(lithogpu_ilt* ilt, int iterations, double* cost
       ilt_run_impl<float>(ilt, iterations, cost, gmax);
     else
       ilt_run_impl<double>(ilt, iterations, cost, gmax);
+  });
+}
+
+lithogpu_status lithogpu_ilt_gradient(lithogpu_ilt* ilt, double* cost, void* grad, lithogpu_dtype dtype) {
+  if (!ilt || !grad) {
+    g_last_error = "lithogpu_ilt_gradient: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    dtype_size(dtype);
+    if (dtype == LITHOGPU_U8) throw UsageError("lithogpu_ilt_gradient: gradient dtype must be F32 or F64");
+    ilt->ks->ctx->activate();
+    lithogpu_ctx* ctx = ilt->ks->ctx;
+    const size_t n = size_t(ilt->ks->grid.nx) * ilt->ks->grid.ny * ilt->tiles;
+    auto run = [&](auto tag) {
+      using T = decltype(tag);
+      OutStage<T> o(ctx, grad, dtype, n, 0);
+      ilt_run_impl<T>(ilt, 1, cost, nullptr, o.work, 0.0);
+      if (o.finish()) LG_CUDA(cudaStreamSynchronize(ctx->stream));
+    };
+    if (ilt->ks->precision == LITHOGPU_F32)
+      run(float{});
+    else
+      run(double{});
   });
 }
 

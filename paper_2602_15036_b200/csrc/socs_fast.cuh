@@ -565,9 +565,11 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_grad_rows(FGeo g, con
       const float n1 = t1 - step * g1;
       gm = fmaxf(gm, fabsf(g1));
       if (act) th[size_t(y1) * L + i] = n1;
+      if (grad && act) grad[blockIdx.z * gr_ts + size_t(y1) * L + i] = g1;
       n1v = fsig(steep * n1);
     }
     if (act) th[size_t(y0) * L + i] = n0;
+    if (grad && act) grad[blockIdx.z * gr_ts + size_t(y0) * L + i] = g0;  // dL/dtheta (lithogpu_ilt_gradient)
     v[e] = mk(fsig(steep * n0), n1v);
   }
   gm = warp_max(gm, TPR < 32 ? TPR : 32);

@@ -751,6 +751,7 @@ __global__ void k_grad_rows(Geo<T> g, const cx<T>* __restrict__ Gc, long long g_
       const T g0 = v.x * steep * m0 * (T(1) - m0);
       const T n0 = t0 - step * g0;
       th[size_t(y0) * Nx + x] = n0;
+      if (grad) grad[tile * gr_ts + size_t(y0) * Nx + x] = OutT(g0);  // dL/dtheta (lithogpu_ilt_gradient)
       gm = fmax(gm, fabs(double(g0)));
       T n1v = T(0);
       if (has1) {
@@ -759,6 +760,7 @@ __global__ void k_grad_rows(Geo<T> g, const cx<T>* __restrict__ Gc, long long g_
         const T g1 = v.y * steep * m1 * (T(1) - m1);
         const T n1 = t1 - step * g1;
         th[size_t(y1) * Nx + x] = n1;
+        if (grad) grad[tile * gr_ts + size_t(y1) * Nx + x] = OutT(g1);
         gm = fmax(gm, fabs(double(g1)));
         n1v = sigm(steep * n1);
       }

@@ -27,6 +27,10 @@ def _canon(polys: List[np.ndarray]) -> List[np.ndarray]:
     out = []
     for p in polys:
         p = np.asarray(p, np.int64)
+        if len(p) == 4 and p[0, 0] == p[3, 0] == min(p[0, 0], p[1, 0]) and p[1, 0] == p[2, 0] != p[0, 0] \
+                and p[0, 1] == p[1, 1] < p[2, 1] == p[3, 1]:
+            out.append(p)  # _rect output: CCW, smallest vertex first, already canonical
+            continue
         # drop consecutive duplicates and collinear vertices (normalize_chain)
         changed = True
         while changed and len(p) >= 3:
@@ -118,6 +122,39 @@ def curvilinear(width_nm: int, height_nm: int, seed: int = 0, x0: int = 0, y0: i
     return _canon(polys)
 
 
+def polygon_bboxes(polys: Sequence[np.ndarray]) -> np.ndarray:
+    """[P, 4] int64 (xmin, ymin, xmax, ymax) per polygon."""
+    if not len(polys):
+        return np.zeros((0, 4), np.int64)
+    xy, st = polygon_arrays(polys)
+    idx = st[:-1]
+    return np.stack([np.minimum.reduceat(xy[:, 0], idx), np.minimum.reduceat(xy[:, 1], idx),
+                     np.maximum.reduceat(xy[:, 0], idx), np.maximum.reduceat(xy[:, 1], idx)], 1)
+
+
+def chip_tiling(tile: int, tiles_x: int, tiles_y: int, halo: int, pitch_nm: float = 1.0,
+                origin_nm=(0.0, 0.0)) -> "Tiling":
+    """Tiling of a chip window into tiles_x x tiles_y halo-padded tiles of
+    `tile` px (core = tile - 2 halo)."""
+    core = tile - 2 * halo
+    if core <= 0:
+        raise ValueError("chip_tiling: halo leaves no core")
+    chip = Grid(tiles_x * core, tiles_y * core, pitch_nm, origin_nm[0], origin_nm[1])
+    return Tiling(chip, core, halo)
+
+
+def chip_layout(tiling: "Tiling", seed: int = 0, curvilinear_layout: bool = False) -> List[np.ndarray]:
+    """One seeded synthetic layout over the halo-extended chip window
+    (integer nm; pitch 1 nm), heal-canonical."""
+    ext = tiling.extended_grid()
+    w = int(round(ext.nx * ext.pitch_nm))
+    h = int(round(ext.ny * ext.pitch_nm))
+    x0 = int(math.floor(ext.origin_x_nm))
+    y0 = int(math.floor(ext.origin_y_nm))
+    gen = curvilinear if curvilinear_layout else line_space_contacts
+    return gen(w, h, seed=seed, x0=x0, y0=y0)
+
+
 def polygon_arrays(polys: Sequence[np.ndarray]):
     """Flattened (xy [V,2] int64, starts [P+1] int64) for the C ABI."""
     if len(polys):
@@ -132,6 +169,35 @@ def polygon_arrays(polys: Sequence[np.ndarray]):
 # ---------------------------------------------------------------------------
 # halo-padded tiling
 # ---------------------------------------------------------------------------
+def blur_radius_px(resist_sigma_nm: float, pitch_nm: float) -> int:
+    """Support of the reference resist blur: r = ceil(6 sigma_px) + 1
+    (imaging.cpp:296-297; the min(N/2, .) cap does not bind at tile sizes)."""
+    if resist_sigma_nm <= 0:
+        return 0
+    return int(math.ceil(6.0 * resist_sigma_nm / pitch_nm)) + 1
+
+
+def optical_halo_px(wavelength_nm: float, na: float, pitch_nm: float, resist_sigma_nm: float,
+                    ambit_lambda_over_na: float = 2.0, align: int = 64, minimum: int = 64) -> int:
+    """Guard band of a halo-padded tile, in pixels: the optical ambit
+    (`ambit_lambda_over_na` x lambda/NA, the coherent impulse response's main
+    lobes) plus the resist-blur support (blur_radius_px), rounded up to
+    `align` and at least `minimum` — the reference's window guard is this
+    "pupil impulse-response support + resist sigma" band (SPEC.md:457,
+    make_window opc.cpp:97-112).  EUV defaults (13.5 nm, NA 0.33, sigma 2 nm,
+    1 nm pitch): 82 + 13 = 95 -> 128 px.
+
+    The cores of halo-padded cyclic tiles equal a larger window's image only
+    up to the hard-pupil tail, which decays slowly: measured on the oracle
+    (tests/test_gpu_tiling.py) the core-vs-window aerial difference is a
+    few 1e-2 of max I for halos from 64 to 384 px.  Tiles are therefore
+    closed problems by definition (each cyclic window is imaged exactly, as
+    the reference images each make_window window) and only cores are
+    stitched."""
+    ambit = ambit_lambda_over_na * wavelength_nm / na / pitch_nm
+    h = int(math.ceil(ambit)) + blur_radius_px(resist_sigma_nm, pitch_nm)
+    h = max(h, minimum)
+    return -(-h // align) * align
 @dataclass(frozen=True)
 class Tiling:
     """Chip window `chip` split into tx x ty cores of `core` px; each tile is
@@ -172,16 +238,15 @@ class Tiling:
         return Grid(self.tx * self.core + 2 * self.halo, self.ty * self.core + 2 * self.halo, p,
                     self.chip.origin_x_nm - self.halo * p, self.chip.origin_y_nm - self.halo * p)
 
-    def tile_polygons(self, polys: Sequence[np.ndarray], t: int, dbu_per_nm: float = 1.0):
-        """Polygons whose bbox meets tile t's window, in layer order."""
+    def tile_polygons(self, polys: Sequence[np.ndarray], t: int, dbu_per_nm: float = 1.0, bboxes=None):
+        """Polygons whose bbox meets tile t's window, in layer order
+        (`bboxes`: polygon_bboxes(polys), precomputed for many tiles)."""
         g = self.tile_grid(t)
         x0, y0 = g.origin_x_nm * dbu_per_nm, g.origin_y_nm * dbu_per_nm
         x1, y1 = x0 + g.nx * g.pitch_nm * dbu_per_nm, y0 + g.ny * g.pitch_nm * dbu_per_nm
-        out = []
-        for p in polys:
-            if p[:, 0].max() >= x0 and p[:, 0].min() <= x1 and p[:, 1].max() >= y0 and p[:, 1].min() <= y1:
-                out.append(p)
-        return out
+        bb = polygon_bboxes(polys) if bboxes is None else bboxes
+        hit = (bb[:, 2] >= x0) & (bb[:, 0] <= x1) & (bb[:, 3] >= y0) & (bb[:, 1] <= y1)
+        return [polys[i] for i in np.nonzero(hit)[0]]
 
     def stitch(self, tiles: np.ndarray) -> np.ndarray:
         """Core regions of [T, n, n] tile images -> chip image [ny, nx]."""

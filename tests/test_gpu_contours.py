@@ -159,3 +159,11 @@ def test_evaluate_epe_fused_batch(ctx):
         assert np.array_equal(ro, op[t])
         assert np.abs(re - epe[t]).max() < 1e-6
     assert op.sum() < op.size  # most gauges see an edge
+    # device-resident masks (torch CUDA tensor) give the same records
+    import torch
+    e_d, o_d = L.evaluate_epe(torch.from_numpy(masks).cuda(), dk, gauges, 1.0, 2.0, 0.25, 12.0, focus=1)
+    assert np.array_equal(e_d, epe) and np.array_equal(o_d, op)
+    bad = masks.copy()
+    bad[0, 5, 5] = np.nan
+    with pytest.raises(ValueError):
+        L.evaluate_epe(bad, dk, gauges, 1.0, 2.0, 0.25, 12.0, focus=1)
