@@ -188,6 +188,12 @@ lithogpu_status lithogpu_ilt_gradient(lithogpu_ilt* ilt, double* cost, void* gra
 /* theta and/or mask = sigmoid(steepness*theta) of one tile (nullable outs) */
 lithogpu_status lithogpu_ilt_get_tile(lithogpu_ilt* ilt, int tile, void* theta, void* mask,
                                       lithogpu_dtype dtype);
+/* Mask window of one tile for chip stitching (only tile
+ * cores are kept): out[r*row_stride + c] = sigmoid(steepness*theta) at pixel
+ * (x0 + c, y0 + r) of `tile`, r < h, c < w (dtype F32/F64; host or device;
+ * e.g. the core [halo, halo+core)^2 written straight into the chip image). */
+lithogpu_status lithogpu_ilt_get_window(lithogpu_ilt* ilt, int tile, int x0, int y0, int w, int h, void* mask,
+                                        int64_t row_stride, lithogpu_dtype dtype);
 /* all tiles: n_tiles*nx*ny (nullable outs) */
 lithogpu_status lithogpu_ilt_get_tiles(lithogpu_ilt* ilt, void* theta, void* mask,
                                        lithogpu_dtype dtype);

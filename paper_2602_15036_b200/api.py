@@ -686,6 +686,23 @@ class IltSolver:
         check(lib().lithogpu_ilt_get_tiles(self._h, ptr(theta), ptr(mask), dtype))
         return theta, mask
 
+    def get_window(self, tile: int, x0: int, y0: int, w: int, h: int, out=None, dtype=F32):
+        """Mask window of one tile (lithogpu_ilt_get_window) into `out`
+        (numpy / CUDA tensor view with unit column stride, e.g. a block of
+        the stitched chip mask) or a new (h, w) host array."""
+        if out is None:
+            out = np.empty((h, w), np.float32 if dtype == F32 else np.float64)
+        if _is_torch(out):
+            ptr, stride = out.data_ptr(), out.stride(0)
+            dt = {torch.float32: F32, torch.float64: F64}[out.dtype]
+        else:
+            if out.strides[1] != out.itemsize:
+                raise ValueError("get_window: out needs unit column stride")
+            ptr, stride = out.ctypes.data, out.strides[0] // out.itemsize
+            dt = _NP2DT[out.dtype]
+        check(lib().lithogpu_ilt_get_window(self._h, tile, x0, y0, w, h, ptr, stride, dt))
+        return out
+
     def close(self):
         if getattr(self, "_h", None):
             lib().lithogpu_ilt_destroy(self._h)

@@ -29,9 +29,18 @@ def allreduce_scalars(cost, gmax, group=None):
     |dL/dtheta|) — the only cross-GPU traffic of the tiled ILT."""
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized():
-        dist.all_reduce(cost, op=dist.ReduceOp.SUM, group=group)
+        host = cost.is_cuda and dist.get_backend(group) == "gloo"  # gloo: reduce host copies
+
+        def red(t, op):
+            if host:
+                h = t.cpu()
+                dist.all_reduce(h, op=op, group=group)
+                t.copy_(h)
+            else:
+                dist.all_reduce(t, op=op, group=group)
+        red(cost, dist.ReduceOp.SUM)
         if gmax is not None:
-            dist.all_reduce(gmax, op=dist.ReduceOp.MAX, group=group)
+            red(gmax, dist.ReduceOp.MAX)
     return cost, gmax
 
 

@@ -2223,6 +2223,56 @@ lithogpu_status lithogpu_ilt_gradient(lithogpu_ilt* ilt, double* cost, void* gra
   });
 }
 
+lithogpu_status lithogpu_ilt_get_window(lithogpu_ilt* ilt, int tile, int x0, int y0, int w, int h, void* mask,
+                                        int64_t row_stride, lithogpu_dtype dtype) {
+  if (!ilt || !mask) {
+    g_last_error = "lithogpu_ilt_get_window: null argument";
+    return LITHOGPU_ERR_USAGE;
+  }
+  return guarded([&] {
+    const int nx = ilt->ks->grid.nx, ny = ilt->ks->grid.ny;
+    if (tile < 0 || tile >= ilt->tiles) throw UsageError("lithogpu_ilt_get_window: tile out of range");
+    if (x0 < 0 || y0 < 0 || w <= 0 || h <= 0 || x0 + w > nx || y0 + h > ny || row_stride < w)
+      throw UsageError("lithogpu_ilt_get_window: window outside the tile");
+    if (dtype != LITHOGPU_F32 && dtype != LITHOGPU_F64) throw UsageError("lithogpu_ilt_get_window: dtype");
+    lithogpu_ctx* ctx = ilt->ks->ctx;
+    ctx->activate();
+    const size_t es = dtype_size(dtype);
+    const bool dev = is_device_ptr(mask);
+    void* dst = mask;
+    long long stride = row_stride;
+    if (!dev) {
+      DevBuf& b = ctx->slot(0);
+      b.ensure(es * size_t(w) * h);
+      dst = b.p;
+      stride = w;
+    }
+    const dim3 grd((w + 255) / 256, h);
+    auto launch = [&](auto tag) {
+      using T = decltype(tag);
+      const T* th = ilt->theta.as<T>() + size_t(nx) * ny * tile;
+      if (dtype == LITHOGPU_F32)
+        lg::k_sigmoid_window<T, float><<<grd, 256, 0, ctx->stream>>>(th, nx, x0, y0, w, h,
+                                                                      T(ilt->prm.mask_steepness),
+                                                                      static_cast<float*>(dst), stride);
+      else
+        lg::k_sigmoid_window<T, double><<<grd, 256, 0, ctx->stream>>>(th, nx, x0, y0, w, h,
+                                                                       T(ilt->prm.mask_steepness),
+                                                                       static_cast<double*>(dst), stride);
+      ctx->check_launch();
+    };
+    if (ilt->ks->precision == LITHOGPU_F32)
+      launch(float{});
+    else
+      launch(double{});
+    if (!dev) {
+      LG_CUDA(cudaMemcpy2DAsync(mask, size_t(row_stride) * es, dst, size_t(w) * es, size_t(w) * es, size_t(h),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+      LG_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+  });
+}
+
 lithogpu_status lithogpu_ilt_get_tile(lithogpu_ilt* ilt, int tile, void* theta, void* mask,
                                       lithogpu_dtype dtype) {
   if (!ilt) {

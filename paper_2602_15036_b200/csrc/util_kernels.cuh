@@ -38,6 +38,17 @@ __global__ void k_sigmoid(const T* __restrict__ theta, T* __restrict__ m, size_t
     m[i] = T(1) / (T(1) + exp(-a * theta[i]));
 }
 
+// mask window: out[r * stride + c] = sigmoid(a * theta[(y0 + r) * nx + x0 + c])
+template <typename T, typename OutT>
+__global__ void k_sigmoid_window(const T* __restrict__ theta, int nx, int x0, int y0, int w, int h, T a,
+                                 OutT* __restrict__ out, long long stride) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y;
+  if (c >= w || r >= h) return;
+  const T t = theta[size_t(y0 + r) * nx + x0 + c];
+  out[size_t(r) * stride + c] = OutT(T(1) / (T(1) + exp(-a * t)));
+}
+
 // One separable pass of the cyclic truncated Gaussian (gaussian_blur,
 // imaging.cpp:287-314, is the same cyclic convolution done with 3 FFTs).
 // AXIS 0: along x (contiguous), AXIS 1: along y.  taps[d + r] = g(d)/sum g.

@@ -178,3 +178,42 @@ def test_oracle_vs_reference_live():
     h = R.heal(polys)
     assert np.array_equal(O.rasterize(h, 128, 128, 0.75, -1.0, 2.5, 1.0),
                           R.rasterize(polys, 128, 128, 0.75, -1.0, 2.5, 1.0))
+
+
+@pytest.mark.parametrize("n,pitch,focus,grid_n", [(16, 4.0, 0.0, 7), (24, 4.0, 30.0, 7), (32, 2.0, -20.0, 5)])
+def test_numpy_kernel_source_vs_reference_decompose_tcc(n, pitch, focus, grid_n):
+    """oracle/kernels_np.py (the reference arm's kernel source) against the
+    reference build_tcc + decompose_tcc itself (oracle/_ref): same support
+    order, eigenvalues, and the same full-rank image."""
+    from oracle import kernels_np as KN
+    if not R.available():
+        pytest.skip("oracle/_ref not built")
+    rk = R.RefKernels(n, n, pitch, focus=focus, grid_n=grid_n, energy_floor=1.0)
+    src = KN.annular_source(0.4, 0.8, grid_n)
+    w, sup, v = KN.socs_kernels(n, n, pitch, src, focus, 0, energy_floor=1.0)
+    assert np.array_equal(sup, rk.support)
+    k = min(len(w), rk.K)
+    assert np.abs(w[:k] - rk.weights[:k]).max() <= 1e-10 * rk.weights[0]
+    rng = np.random.default_rng(n)
+    mask = rng.random((n, n))
+    a = O.image_socs(mask, w, sup, v)
+    b = O.image_socs(mask, rk.weights, rk.support, rk.values)
+    assert rel(a, b) < 1e-9
+
+
+def test_numpy_kernel_source_vs_product_generator():
+    """the same numbers as the product's host generator at a BASELINE-like
+    band (256^2, 1 nm, K = 12, through focus)."""
+    import paper_2602_15036_b200 as L
+    from oracle import kernels_np as KN
+    n = 256
+    W, sup, V = KN.socs_kernel_stacks(n, 1.0, [-40.0, 0.0], 12)
+    ks = L.build_socs_kernels(L.OpticalModel(source=L.make_annular_source(0.4, 0.8, 21)), L.Grid(n, n, 1.0),
+                              [-40.0, 0.0], k_fixed=12)
+    assert np.array_equal(sup, ks.support)
+    assert np.abs(W - ks.weights).max() <= 1e-10 * ks.weights.max()
+    mask = np.random.default_rng(1).random((n, n))
+    for f in range(2):
+        a = O.image_socs(mask, W[f], sup, V[f])
+        b = O.image_socs(mask, ks.weights[f], ks.support, ks.values[f])
+        assert rel(a, b) < 1e-8

@@ -5,7 +5,7 @@ Each fast kernel records its first-CTA start and last-warp end
 (%globaltimer) per launch; this prints, for the last replay of `iters`
 iterations, every launch's duration and the gap before it.
 
-  python tools/trace.py [--iters 4] [--lib path]
+  python tools/trace.py [--iters 4] [--config c2|c5 ...] [--tiles T]
 """
 import json
 import os
@@ -20,6 +20,7 @@ import bench
 import paper_2602_15036_b200 as L
 from paper_2602_15036_b200 import layouts as LY
 iters = int(sys.argv[1])
+tiles = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 torch.cuda.set_device(0)
 st = torch.cuda.Stream(); torch.cuda.set_stream(st)
 ctx = L.Context(0); ctx.set_stream(st.cuda_stream)
@@ -29,12 +30,12 @@ xy, starts = LY.polygon_arrays(polys)
 N = grid.nx
 tgt = torch.empty((1, N, N), dtype=torch.float64, device="cuda")
 bench._raster_to(ctx, grid, xy, starts, tgt)
-t32 = tgt.float()
+t32 = tgt.float().expand(tiles, -1, -1).contiguous()
 th = ((2 * t32 - 1) * 0.5).contiguous()
 F = ks.weights.shape[0]
 prm = L.IltParams(focus_weights=[1.0 / F] * F, **bench.ILT)
-sol = L.IltSolver(dk, prm, 1, "f32", ctx)
-cost = torch.zeros((iters, 1), dtype=torch.float64, device="cuda")
+sol = L.IltSolver(dk, prm, tiles, "f32", ctx)
+cost = torch.zeros((iters, tiles), dtype=torch.float64, device="cuda")
 for _ in range(4):
     sol.set_tiles(t32, th); sol.run_device(iters, cost)
 torch.cuda.synchronize()
@@ -44,11 +45,12 @@ torch.cuda.synchronize()
 def main():
     iters = int(sys.argv[sys.argv.index("--iters") + 1]) if "--iters" in sys.argv else 4
     cfg = sys.argv[sys.argv.index("--config") + 1] if "--config" in sys.argv else "c2"
+    tiles = sys.argv[sys.argv.index("--tiles") + 1] if "--tiles" in sys.argv else "1"
     fd, path = tempfile.mkstemp(suffix=".jsonl")
     os.close(fd)
     env = dict(os.environ, LITHOGPU_TRACE=path)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", CHILD, str(iters), cfg], env=env, cwd=root, capture_output=True,
+    r = subprocess.run([sys.executable, "-c", CHILD, str(iters), cfg, tiles], env=env, cwd=root, capture_output=True,
                        text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stderr[-3000:])
