@@ -279,6 +279,22 @@ lithogpu_status lithogpu_write_aimg(lithogpu_ctx* ctx, const lithogpu_grid* grid
 lithogpu_status lithogpu_read_aimg(lithogpu_ctx* ctx, const char* path, int* nx, int* ny, double* pitch_nm,
                                    double* values);
 
+/* ---- layout JSON -> polygon buffers ------------------
+ * Reader of the reference layout format (load_layout, io.cpp:53-116): same
+ * validation and error messages (LITHOGPU_ERR_DOMAIN + lithogpu_last_error).
+ * A layer's polygons come out flattened for lithogpu_rasterize: xy (2 int64
+ * per vertex, dbu) and poly_start (n_poly + 1 offsets), into host OR device
+ * memory.  Polygons are as stored (the reference heals inside
+ * rasterize_layer; the GPU rasterizer takes healed input). */
+typedef struct lithogpu_layout lithogpu_layout;
+lithogpu_status lithogpu_layout_load(const char* path, lithogpu_layout** out);
+void lithogpu_layout_destroy(lithogpu_layout* layout);
+lithogpu_status lithogpu_layout_info(const lithogpu_layout* layout, int* n_layers, int64_t* dbu_num,
+                                     int64_t* dbu_den);
+lithogpu_status lithogpu_layout_layer(const lithogpu_layout* layout, int layer, const char** name,
+                                      int64_t* n_poly, int64_t* n_vert);
+lithogpu_status lithogpu_layout_get(const lithogpu_layout* layout, int layer, int64_t* xy, int64_t* poly_start);
+
 /* GPU kernel generation: lithogpu_socs_kernels for
  * n_focus focus planes in one call (fp64; cuBLAS Gram + cuSOLVER eigensolve
  * + cuBLAS kernel assembly).  Same support, ordering, truncation and phase

@@ -89,6 +89,12 @@ _SIGS = {
     "lithogpu_socs_kernels_gpu": (C.c_int, [_vp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int,
                                             _vp, C.c_int, C.c_int, _vp, C.c_int, _vp, C.c_int, C.c_double, C.c_int,
                                             _vp, _vp, _vp, _vp]),
+    "lithogpu_layout_load": (C.c_int, [C.c_char_p, C.POINTER(_vp)]),
+    "lithogpu_layout_destroy": (None, [_vp]),
+    "lithogpu_layout_info": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "lithogpu_layout_layer": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_char_p), C.POINTER(C.c_int64),
+                                        C.POINTER(C.c_int64)]),
+    "lithogpu_layout_get": (C.c_int, [_vp, C.c_int, _vp, _vp]),
     "lithogpu_write_aimg": (C.c_int, [_vp, C.POINTER(Grid), C.c_int, _vp, _vp, C.c_int]),
     "lithogpu_read_aimg": (C.c_int, [_vp, C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_double),
                                      _vp]),

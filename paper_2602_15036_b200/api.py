@@ -606,6 +606,49 @@ def read_aimg(path: str, ctx: Optional[Context] = None):
 
 
 # ---------------------------------------------------------------------------
+# layout JSON (reference io.hpp load_layout / io.cpp:53-116)
+# ---------------------------------------------------------------------------
+@dataclass
+class Layout:
+    """load_layout result: dbu per nm as num/den, layers = [(name, [polygon (n, 2) int64, ...])]."""
+    dbu_num: int
+    dbu_den: int
+    layers: list
+
+    def dbu_per_nm(self) -> float:
+        return self.dbu_num / self.dbu_den
+
+
+def load_layout(path: str, device=None) -> Layout:
+    """Reference layout JSON -> polygons (lithogpu_layout_load / _get).  With
+    `device` (a torch device), each layer instead comes back as flattened
+    device buffers (xy [V, 2] int64, poly_start [P + 1] int64) ready for
+    lithogpu_rasterize."""
+    h = C.c_void_p()
+    check(lib().lithogpu_layout_load(path.encode(), C.byref(h)))
+    try:
+        nl, num, den = C.c_int(), C.c_int64(), C.c_int64()
+        check(lib().lithogpu_layout_info(h, C.byref(nl), C.byref(num), C.byref(den)))
+        layers = []
+        for li in range(nl.value):
+            name, npoly, nvert = C.c_char_p(), C.c_int64(), C.c_int64()
+            check(lib().lithogpu_layout_layer(h, li, C.byref(name), C.byref(npoly), C.byref(nvert)))
+            if device is not None:
+                xy = torch.empty((nvert.value, 2), dtype=torch.int64, device=device)
+                st = torch.empty(npoly.value + 1, dtype=torch.int64, device=device)
+                check(lib().lithogpu_layout_get(h, li, xy.data_ptr() if nvert.value else None, st.data_ptr()))
+                layers.append((name.value.decode(), (xy, st)))
+                continue
+            xy = np.empty((nvert.value, 2), np.int64)
+            st = np.empty(npoly.value + 1, np.int64)
+            check(lib().lithogpu_layout_get(h, li, xy.ctypes.data if nvert.value else None, st.ctypes.data))
+            layers.append((name.value.decode(), [xy[st[i]:st[i + 1]] for i in range(npoly.value)]))
+        return Layout(num.value, den.value, layers)
+    finally:
+        lib().lithogpu_layout_destroy(h)
+
+
+# ---------------------------------------------------------------------------
 # ILT
 # ---------------------------------------------------------------------------
 @dataclass

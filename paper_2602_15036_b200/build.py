@@ -19,7 +19,11 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CU_SOURCES = ["csrc/capi.cu", "csrc/fast_rows.cu", "csrc/fast_cols.cu", "csrc/kernelgen.cu"]
-CPP_SOURCES = ["host/socs_kernels.cpp"]
+CPP_SOURCES = ["host/socs_kernels.cpp", "host/layout_io.cpp"]
+# nlohmann/json (header-only; the reference's own JSON library) for the layout reader
+JSON_INC = os.environ.get("LITHO_JSON_INC", "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/"
+                                           "cudnn_frontend/thirdparty/nlohmann")
+CUDA_INC = "/usr/local/cuda/include"
 DEPS = ["csrc/fft.cuh", "csrc/geom.h", "csrc/socs_kernels.cuh", "csrc/raster_kernels.cuh",
         "csrc/util_kernels.cuh", "csrc/fftr.cuh", "csrc/socs_fast.h", "csrc/socs_fast.cuh",
         "csrc/fast_common.cuh", "csrc/contour_kernels.cuh", "../include/lithogpu.h"]
@@ -55,7 +59,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(obj)
         if force or _newer(obj, [src, "../include/lithogpu.h"]):
             jobs.append(["g++", "-O2", "-std=c++17", "-fPIC", "-fopenmp", "-ffp-contract=off",
-                         "-c", src, "-o", obj])
+                         "-I" + JSON_INC, "-I" + CUDA_INC, "-c", src, "-o", obj])
     with ThreadPoolExecutor(max_workers=8) as ex:
         for r in ex.map(_run, jobs):
             if verbose:

@@ -889,8 +889,9 @@ struct Plan : PlanBase {
       unsigned long long t0 = ~0ull, t1 = 0;
       int n = 0;
       for (int c = 0; c < lg::kTraceCtas; ++c) {
-        const unsigned long long a = h[(sl * lg::kTraceCtas + c) * 2], b = h[(sl * lg::kTraceCtas + c) * 2 + 1];
-        if (!a) continue;
+        const unsigned long long ar = h[(sl * lg::kTraceCtas + c) * 2], b = h[(sl * lg::kTraceCtas + c) * 2 + 1];
+        if (!ar) continue;
+        const unsigned long long a = ~ar;  // cells keep the complement of the earliest start
         ++n;
         t0 = std::min(t0, a);
         t1 = std::max(t1, b);

@@ -34,13 +34,15 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+// CTAs fold onto kTraceCtas cells (batched launches have far more CTAs):
+// cell[0] keeps ~min(start) (atomicMax of the complement), cell[1] max(end)
 __device__ __forceinline__ unsigned long long* trace_cell(const FGeo& g) {
   const unsigned cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-  return cta < unsigned(kTraceCtas) ? g.trace + (size_t(g.trace_slot) * kTraceCtas + cta) * 2 : nullptr;
+  return g.trace + (size_t(g.trace_slot) * kTraceCtas + cta % unsigned(kTraceCtas)) * 2;
 }
 __device__ __forceinline__ void trace_begin(const FGeo& g) {
   if (g.trace && threadIdx.x == 0)
-    if (auto* c = trace_cell(g)) c[0] = gtimer();
+    if (auto* c = trace_cell(g)) atomicMax(c, ~gtimer());
 }
 __device__ __forceinline__ void trace_end(const FGeo& g) {
   if (g.trace && (threadIdx.x & 31) == 0)

@@ -32,9 +32,24 @@ $CXX $INC -c "$ROOT/paper_2602_15036_b200/host/litho_dropin.cpp" -o "$OUT/obj/li
 for t in test_imaging test_geometry test_opc_ai test_contour; do
   $CXX $INC -I"$HERE" -I"$REF/tests" -I"$ROOT/oracle/shim" -c "$REF/tests/$t.cpp" -o "$OUT/obj/$t.o" & pids+=($!)
 done
+# the reference C ABI (litho_c.cpp) and its I/O + bench units, for dropin_capi
+JSON_INC="${LITHO_JSON_INC:-/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann}"
+for s in io bench; do
+  $CXX $INC -I"$JSON_INC" -c "$REF/src/core/$s.cpp" -o "$OUT/obj/capi_$s.o" & pids+=($!)
+done
+$CXX $INC -I"$REF/include" -I"$JSON_INC" -c "$REF/src/capi/litho_c.cpp" -o "$OUT/obj/capi_litho_c.o" & pids+=($!)
+$CXX $INC -I"$REF/include" -I"$JSON_INC" -c "$HERE/dropin_capi.cpp" -o "$OUT/obj/capi_driver.o" & pids+=($!)
 for p in "${pids[@]}"; do wait "$p"; done
+# ai.cpp stays the reference's own except intensity_gradient, which the
+# drop-in defines: the reference definition is made weak so the drop-in's
+# strong symbol wins at link time (build_field_tensor's call goes through
+# the PLT under -fPIC and lands on the GPU adjoint).  The maintainer-side
+# edit is deleting that one function.
+objcopy --weaken-symbol=_ZN5litho18intensity_gradientERKNS_9MaskFieldERKNS_13SocsKernelSetEd "$OUT/obj/ref_ai.o"
 LIBS="-L$ROOT/paper_2602_15036_b200 -llithogpu -Wl,-rpath,$ROOT/paper_2602_15036_b200 -Wl,-rpath,\$ORIGIN/../../../paper_2602_15036_b200 -L$CUDA/lib64 -lcusolver -lcudart"
 for t in test_imaging test_geometry test_opc_ai test_contour; do
   g++ -o "$OUT/$t" "$OUT/obj/$t.o" "$OUT/obj/litho_dropin.o" "$OUT"/obj/ref_*.o $LIBS
 done
+g++ -o "$OUT/dropin_capi" "$OUT/obj/capi_driver.o" "$OUT/obj/capi_litho_c.o" "$OUT/obj/capi_io.o" \
+  "$OUT/obj/capi_bench.o" "$OUT/obj/litho_dropin.o" "$OUT"/obj/ref_*.o $LIBS
 echo "build_dropin_tests: $OUT"

@@ -233,3 +233,40 @@ def test_segmented_ilt_allreduce_gloo():
     assert res[0][2] == res[1][2] == [1.0 / (it + 1) + 4 for it in range(7)]
     # segments of 2: costs 15, 30 | 45, 60 | 60, 60 -> stop after the third segment
     assert res[0][3] == res[1][3] == 6
+
+
+def test_layout_json_loader_round_trip_and_errors(tmp_path):
+    """lithogpu_layout_load (reference load_layout, io.cpp:53-116): the
+    reference JSON format in, flattened polygon buffers out; the reference's
+    validation messages."""
+    import json
+    polys = LY.line_space_contacts(300, 200, seed=2)
+    doc = {"format_version": 1, "dbu_per_nm": [2, 1],
+           "layers": [{"name": "M1", "polygons": [p.tolist() for p in polys]}, {"name": "empty", "polygons": []}]}
+    p = tmp_path / "l.json"
+    p.write_text(json.dumps(doc, indent=1))
+    lay = L.load_layout(str(p))
+    assert (lay.dbu_num, lay.dbu_den) == (2, 1) and lay.dbu_per_nm() == 2.0
+    assert [n for n, _ in lay.layers] == ["M1", "empty"]
+    got = lay.layers[0][1]
+    assert len(got) == len(polys) and all(np.array_equal(a, b) for a, b in zip(got, polys))
+    assert lay.layers[1][1] == []
+    bad = [({"format_version": 2, "dbu_per_nm": 1, "layers": []}, "missing or unsupported format_version"),
+           ({"format_version": 1, "dbu_per_nm": 1, "layers": [], "x": 1}, 'unknown key "x"'),
+           ({"format_version": 1, "layers": []}, "missing dbu_per_nm"),
+           ({"format_version": 1, "dbu_per_nm": 0, "layers": []}, "dbu_per_nm must be positive"),
+           ({"format_version": 1, "dbu_per_nm": 1, "layers": [{"name": "a", "polygons": [[[0, 0], [1.5, 0], [1, 1]]]}]},
+            "non-integer coordinate in"),
+           ({"format_version": 1, "dbu_per_nm": 1, "layers": [{"name": "a", "polygons": [[[0, 0, 1]]]}]},
+            "bad vertex in")]
+    for i, (d, msg) in enumerate(bad):
+        q = tmp_path / f"bad{i}.json"
+        q.write_text(json.dumps(d))
+        with pytest.raises(RuntimeError, match=msg):
+            L.load_layout(str(q))
+    q = tmp_path / "malformed.json"
+    q.write_text("{not json")
+    with pytest.raises(RuntimeError, match="malformed JSON"):
+        L.load_layout(str(q))
+    with pytest.raises(RuntimeError, match="cannot open"):
+        L.load_layout(str(tmp_path / "missing.json"))
