@@ -44,18 +44,22 @@ def _run(cmd):
     return r
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, out: str = OUT, defines=(), objdir: str = OBJ) -> str:
+    """Compile the library (incrementally).  `defines` / `out` / `objdir`
+    build an A/B variant of the same sources (e.g. -DLG_ADJROWS_MINB=4 into
+    variants/<name>/liblithogpu.so, loaded with LITHOGPU_LIB)."""
+    os.makedirs(objdir, exist_ok=True)
     jobs = []
     objs = []
+    dflags = ["-D" + d for d in defines]
     for src in CU_SOURCES:
-        obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
         objs.append(obj)
         if force or _newer(obj, [src] + DEPS):
-            jobs.append([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+            jobs.append([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *dflags,
                          "-Xptxas", "-v" if verbose else "-O3", "-c", src, "-o", obj])
     for src in CPP_SOURCES:
-        obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
         objs.append(obj)
         if force or _newer(obj, [src, "../include/lithogpu.h"]):
             jobs.append(["g++", "-O2", "-std=c++17", "-fPIC", "-fopenmp", "-ffp-contract=off",
@@ -64,9 +68,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for r in ex.map(_run, jobs):
             if verbose:
                 sys.stderr.write(r.stderr)
-    if force or jobs or not os.path.exists(OUT):
-        _run([NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lgomp", "-lcudart", "-lcublas", "-lcusolver"])
-    return OUT
+    if force or jobs or not os.path.exists(out):
+        _run([NVCC, *ARCH, "-shared", "-o", out, *objs, "-lgomp", "-lcudart", "-lcublas", "-lcusolver"])
+    return out
+
+
+def build_variant(name: str, defines) -> str:
+    """variants/<name>/liblithogpu.so with extra -D flags (A/B timing)."""
+    d = os.path.join(ROOT, "variants", name)
+    return build(out=os.path.join(d, "liblithogpu.so"), defines=defines, objdir=os.path.join(d, "obj"))
 
 
 if __name__ == "__main__":

@@ -30,6 +30,8 @@ int main(int argc, char** argv) {
     m.polygons.push_back(
         litho::Polygon{{{x, y_break + 30}, {x + 20, y_break + 30}, {x + 20, 976}, {x, 976}}});
   }
+  // closing line so the bbox is exactly [0, 976]^2
+  m.polygons.push_back(litho::Polygon{{{956, 0}, {976, 0}, {976, 976}, {956, 976}}});
   for (int x = 28; x + 16 <= 976; x += 192)
     m.polygons.push_back(litho::Polygon{{{x, 500}, {x + 16, 500}, {x + 16, 516}, {x, 516}}});
   layout.layers = {m};

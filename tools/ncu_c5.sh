@@ -17,5 +17,6 @@ for k in $KS; do
   ncu -i $OUT/cap_$k.ncu-rep --page raw --csv > $OUT/raw_$k.csv 2>/dev/null
   ncu -i $OUT/cap_$k.ncu-rep --page details --csv > $OUT/details_$k.csv 2>/dev/null
   ncu -i $OUT/cap_$k.ncu-rep --page source --csv > $OUT/source_$k.csv 2>/dev/null
+  mkdir -p /tmp/ncu_reps && mv $OUT/cap_$k.ncu-rep /tmp/ncu_reps/  # reps stay on the box (size cap)
 done
 ls -la $OUT
