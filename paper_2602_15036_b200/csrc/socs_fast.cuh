@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(256) fk_wlp_rows(FGeo g, const C32* __restrict
 // grid (ceil(ny/groups), F*K, tiles)
 // ===========================================================================
 #ifndef LG_ADJROWS_MINB
-#define LG_ADJROWS_MINB 2
+#define LG_ADJROWS_MINB 4  // C5 A/B: 4 CTAs/SM (64 regs) +3.4 % per iteration over 2 (profiles/r2_ab1_occupancy.log)
 #endif
 template <int L, bool UNIFORM, bool FROM_E>
 __global__ void __launch_bounds__(256, LG_ADJROWS_MINB) fk_adj_rows(FGeo g, const C32* __restrict__ T,
