@@ -6,14 +6,14 @@ in include/lithogpu.h); this package is the host-side mirror of the
 reference interface.  There is no CPU fallback.
 """
 from .api import (ContourSet, Context, DeviceKernels, Grid, IltParams, IltSolver, OpticalModel, ResistImage,
-                  SocsKernelSet, Layout, build_socs_kernels, load_layout, default_context, gaussian_blur, image_socs,
+                  SocsKernelSet, Layout, build_socs_kernels, load_layout, default_context, fft2, gaussian_blur, image_socs,
                   intensity_gradient, make_annular_source, make_circular_source, make_point_source,
                   evaluate_epe, marching_squares, measure_epe, rasterize_layer, read_aimg, write_aimg, resist_filter, tcc_support, threshold, z_print, z_round)
 
 __all__ = [
     "ContourSet", "evaluate_epe", "marching_squares", "measure_epe", "read_aimg", "write_aimg",
     "Context", "DeviceKernels", "Grid", "IltParams", "IltSolver", "OpticalModel", "ResistImage",
-    "SocsKernelSet", "Layout", "build_socs_kernels", "load_layout", "default_context", "gaussian_blur", "image_socs",
+    "SocsKernelSet", "Layout", "build_socs_kernels", "load_layout", "default_context", "fft2", "gaussian_blur", "image_socs",
     "intensity_gradient", "make_annular_source", "make_circular_source", "make_point_source",
     "rasterize_layer", "resist_filter", "tcc_support", "threshold", "z_print", "z_round",
 ]

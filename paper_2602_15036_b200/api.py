@@ -390,6 +390,23 @@ def image_socs(mask, kernels, dose: float = 1.0, focus: int = 0, precision: str 
     return dk.image(mask, dose, focus, want=("intensity",))["intensity"]
 
 
+def fft2(values, inverse: bool = False, precision: str = "f64", ctx: Optional[Context] = None) -> np.ndarray:
+    """fft2 (imaging.hpp:124, imaging.cpp:17-31): unnormalized 2-D DFT of a
+    [ny][nx] complex grid (x contiguous), forward e^{-i}, backward e^{+i}.
+    O(L log L) at every size (power-of-two Stockham, mixed radix 2/3/5/7,
+    Bluestein otherwise).  Returns a new complex128 array."""
+    a = np.asarray(values)
+    if a.ndim != 2:
+        raise ValueError("fft2: size mismatch")
+    ny, nx = a.shape
+    rt = np.float32 if precision == "f32" else np.float64
+    buf = np.ascontiguousarray(np.stack([a.real, a.imag], -1), rt)
+    ctx = ctx or default_context()
+    check(lib().lithogpu_fft2(ctx.handle, buf.ctypes.data, F32 if precision == "f32" else F64, nx, ny,
+                              1 if inverse else 0))
+    return buf[..., 0].astype(np.float64) + 1j * buf[..., 1].astype(np.float64)
+
+
 def gaussian_blur(grid: Grid, values, sigma_nm: float, ctx: Optional[Context] = None):
     """gaussian_blur (imaging.cpp:287-314): cyclic unit-sum truncated Gaussian."""
     if sigma_nm < 0:

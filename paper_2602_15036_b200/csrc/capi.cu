@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <complex>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -110,6 +111,12 @@ struct DevBuf {
   }
 };
 
+// device tables of one generic-path transform length (fft.cuh; make_tab)
+struct TabBufs {
+  DevBuf tw, twM, chirp, bhat;
+  bool built = false;
+};
+
 // Host -> device upload of a freshly built table that returns only when the
 // bytes are in device memory.  A plain cudaMemcpy from pageable memory may
 // return once the data is staged, before the DMA lands; the tables are then
@@ -205,6 +212,9 @@ struct lithogpu_ctx {
   }
 
   std::vector<std::unique_ptr<DevBuf>> scratch;  // staging pool (per call slots)
+  // lithogpu_fft2 transform tables, cached per (length, real type size);
+  // immutable once built, so later calls never rewrite a table in use
+  std::map<std::pair<int, int>, std::unique_ptr<TabBufs>> fft_tabs;
   DevBuf raster_tmp;
   std::unordered_map<const void*, int> smem_set;
   // optional per-launch CUDA-event timing (lithogpu_ctx_set_profiling)
@@ -458,6 +468,81 @@ void make_twiddles(int L, DevBuf& buf) {
   h2d_blocking(buf.p, h.data(), sizeof(lg::cx<T>) * L);
 }
 
+// Bluestein chirp w_n = exp(-i pi n^2 / L): n^2 reduced mod 2L in integers so
+// the angle is exact before the fp64 sin/cos
+static std::complex<double> chirp_at(long long n, int L) {
+  const long long m = (n % (2LL * L)) * (n % (2LL * L)) % (2LL * L);
+  const double a = M_PI * double(m) / double(L);
+  return {std::cos(a), -std::sin(a)};
+}
+
+// in-place fp64 radix-2 FFT (host, table setup only), sign -1
+static void host_fft_pow2(std::vector<std::complex<double>>& a) {
+  const int n = int(a.size());
+  for (int i = 1, j = 0; i < n; ++i) {
+    int bit = n >> 1;
+    for (; j & bit; bit >>= 1) j ^= bit;
+    j ^= bit;
+    if (i < j) std::swap(a[i], a[j]);
+  }
+  for (int len = 2; len <= n; len <<= 1) {
+    for (int i = 0; i < n; i += len)
+      for (int k = 0; k < len / 2; ++k) {
+        const double ang = -2.0 * M_PI * double(k) / double(len);
+        const std::complex<double> w(std::cos(ang), std::sin(ang));
+        const std::complex<double> u = a[i + k], v = a[i + k + len / 2] * w;
+        a[i + k] = u + v;
+        a[i + k + len / 2] = u - v;
+      }
+  }
+}
+
+// reuse: the buffers already hold this length's tables (only the view is
+// rebuilt)
+template <typename T>
+lg::Tab<T> make_tab(int L, TabBufs& b, bool reuse = false) {
+  using C = lg::cx<T>;
+  if (!reuse) make_twiddles<T>(L, b.tw);
+  lg::Tab<T> t{};
+  t.tw = b.tw.as<C>();
+  t.L = L;
+  t.kind = lg::fft_kind(L);
+  t.log2L = t.kind == lg::kFftPow2 ? lg::ilog2(L) : -1;
+  t.rad = lg::mixed_radices(L, t.nst);
+  t.M = lg::blue_len(L);
+  if (t.M) {
+    const int M = t.M;
+    t.log2M = lg::ilog2(M);
+    t.twM = b.twM.as<C>();
+    t.chirp = b.chirp.as<C>();
+    t.bhat = b.bhat.as<C>();
+    if (reuse) return t;
+    make_twiddles<T>(M, b.twM);
+    std::vector<C> ch(L), bh(M);
+    std::vector<std::complex<double>> f(M, 0.0);
+    for (int n = 0; n < L; ++n) {
+      const std::complex<double> w = chirp_at(n, L);
+      ch[n].x = T(w.real());
+      ch[n].y = T(w.imag());
+      f[n] = std::conj(w);                 // b_m = conj(w_m), m >= 0
+      if (n) f[M - n] = std::conj(w);      // and m < 0 (wrapped)
+    }
+    host_fft_pow2(f);
+    for (int k = 0; k < M; ++k) {
+      bh[k].x = T(f[k].real());
+      bh[k].y = T(f[k].imag());
+    }
+    b.chirp.ensure(sizeof(C) * L);
+    h2d_blocking(b.chirp.p, ch.data(), sizeof(C) * L);
+    b.bhat.ensure(sizeof(C) * M);
+    h2d_blocking(b.bhat.p, bh.data(), sizeof(C) * M);
+    t.twM = b.twM.as<C>();
+    t.chirp = b.chirp.as<C>();
+    t.bhat = b.bhat.as<C>();
+  }
+  return t;
+}
+
 // 1-D DFT of the reference's truncated unit-sum Gaussian on an N-grid
 // (imaging.cpp:292-305: radius min(N/2, ceil(6 sigma_px)+1), unit sum; the
 // 2-D kernel is the product of the two axes' 1-D kernels).
@@ -512,7 +597,8 @@ struct Plan : PlanBase {
   lg::Geo<T> g{};
   lithogpu_grid grid{};
   int F = 0, K = 0;
-  DevBuf twNx, twNy, twnx, twny, H, wk;
+  TabBufs twNx, twNy, twnx, twny;
+  DevBuf H, wk;
   // Gaussian transfer cache
   // Gaussian band tables, one immutable device table per resist sigma: a
   // solver or image() call with another sigma never overwrites a table that
@@ -563,14 +649,7 @@ struct Plan : PlanBase {
     g.ay = make_axis(Ny, loy, hiy, mixed);
     g.F = F;
     g.K = K;
-    auto tab = [&](int L, DevBuf& b) {
-      make_twiddles<T>(L, b);
-      lg::Tab<T> t;
-      t.tw = b.as<C>();
-      t.L = L;
-      t.log2L = lg::fast_len<T>(L) ? lg::ilog2(L) : -1;
-      return t;
-    };
+    auto tab = [&](int L, TabBufs& b) { return make_tab<T>(L, b); };
     g.tNx = tab(Nx, twNx);
     g.tNy = tab(Ny, twNy);
     g.tnx = tab(g.ax.n, twnx);
@@ -1984,17 +2063,16 @@ lithogpu_status lithogpu_fft2(lithogpu_ctx* ctx, void* data, lithogpu_dtype dtyp
         LG_CUDA(cudaMemcpyAsync(b.p, data, n * sizeof(C), cudaMemcpyHostToDevice, ctx->stream));
         d = b.as<C>();
       }
-      DevBuf& tx = ctx->slot(14);
-      DevBuf& ty = ctx->slot(15);
-      make_twiddles<T>(nx, tx);
-      make_twiddles<T>(ny, ty);
-      auto tab = [](int L, DevBuf& b) {
-        lg::Tab<T> t;
-        t.tw = b.as<C>();
-        t.L = L;
-        t.log2L = lg::fast_len<T>(L) ? lg::ilog2(L) : -1;
+      auto cached = [&](int L) {
+        auto& tb = ctx->fft_tabs[{L, int(sizeof(T))}];
+        if (!tb) tb.reset(new TabBufs);
+        const lg::Tab<T> t = make_tab<T>(L, *tb, tb->built);
+        tb->built = true;
         return t;
       };
+      const lg::Tab<T> tabx = cached(nx), taby = cached(ny);
+      auto tab = [&](int L, int) { return L == nx ? tabx : taby; };
+      const int tx = 0, ty = 0;
       const Launch lr = launch_cfg<T>(nx, 0), lc = launch_cfg<T>(ny, 0);
       ctx->smem_attr(lg::k_fft2_rows<T, -1>, lr.smem);
       ctx->smem_attr(lg::k_fft2_rows<T, +1>, lr.smem);

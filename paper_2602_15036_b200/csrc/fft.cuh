@@ -2,12 +2,19 @@
 //
 // One "row group" of TPR threads transforms one length-L complex row held in
 // shared memory (split re/im arrays, one pad word per 128 B so the strided
-// Stockham stores stay bank-conflict free).  Power-of-two L >= 16 runs a
-// Stockham autosort FFT with radix-16 register butterflies (16 values per
-// thread, TPR = L/16, final radix 8/4/2 stage as needed); any other length
-// falls back to a direct O(L^2) DFT with an exact twiddle table (correctness
-// path for the reference's odd test grids, reference tests use 12/16/24 and
-// 74x49 windows).
+// Stockham stores stay bank-conflict free).  Every length is O(L log L):
+//   * power-of-two L >= 16: Stockham autosort FFT with radix-16 register
+//     butterflies (16 values per thread, TPR = L/16, final radix 8/4/2 stage);
+//   * L whose prime factors are all <= 7 (12, 24, 49 = 7*7; not 74 = 2*37 or
+//     987 = 3*7*47): mixed-radix Stockham (radices 4, 2, 3, 5, 7),
+//     ping-ponging between the row and the group scratch;
+//   * any other L (a make_window size like 1234 = 2*617, opc.cpp:108-109):
+//     Bluestein's chirp-z, X_k = w_k sum_n (x_n w_n) conj(w_{k-n}),
+//     w_n = exp(-i pi n^2 / L), as a cyclic convolution of length
+//     M = 2^ceil(log2(2L-1)) on the power-of-two path, with the chirp and the
+//     chirp filter's spectrum precomputed in fp64 (n^2 reduced mod 2L exactly).
+// The reference's FFTW (imaging.cpp:17-31) is O(L log L) at every size; so is
+// this.
 //
 // Conventions are the reference fft2 (proj/src/core/imaging.cpp:17-31):
 // SIGN = -1 forward exp(-2 pi i k x / L), SIGN = +1 backward, unnormalized.
@@ -110,6 +117,41 @@ __host__ __device__ inline int tpr_for(int L) {
   return t < 1 ? 1 : t;
 }
 
+// transform kinds of the generic path (see the header comment)
+enum FftKind { kFftPow2 = 0, kFftMixed = 1, kFftBluestein = 2 };
+constexpr int kMaxMixedRadix = 7;
+__host__ __device__ inline int fft_kind(int L) {
+  if (is_pow2(L) && L >= 16) return kFftPow2;
+  int r = L;
+  for (int p = 2; p <= kMaxMixedRadix; ++p)
+    while (r % p == 0) r /= p;
+  return r == 1 ? kFftMixed : kFftBluestein;
+}
+// Bluestein convolution length (0 when L does not use Bluestein)
+__host__ __device__ inline int blue_len(int L) {
+  if (fft_kind(L) != kFftBluestein) return 0;
+  const int m = next_pow2(2 * L - 1);
+  return m < 16 ? 16 : m;
+}
+// threads a row group needs for a length-L transform
+__host__ __device__ inline int fft_tpr(int L) { return tpr_for(fft_kind(L) == kFftBluestein ? blue_len(L) : L); }
+// mixed-radix plan: radices (4 first, then 2, 3, 5, 7) as 4-bit nibbles
+__host__ __device__ inline unsigned long long mixed_radices(int L, int& nst) {
+  unsigned long long code = 0;
+  nst = 0;
+  int r = L;
+  auto push = [&](int R) {
+    code |= (unsigned long long)R << (4 * nst);
+    ++nst;
+    r /= R;
+  };
+  while (r % 4 == 0) push(4);
+  while (r % 2 == 0) push(2);
+  for (int p = 3; p <= kMaxMixedRadix; p += 2)
+    while (r % p == 0) push(p);
+  return code;
+}
+
 // lengths of the compile-time-planned fp32 fast path (fftr.cuh), ascending
 constexpr int kFastLens[] = {32, 64, 128, 192, 256, 384, 512, 768, 1024, 1536, 2048, 3072, 4096, 8192};
 
@@ -121,7 +163,17 @@ struct Row {
   T* sre;  // scratch (generic DFT only), length L unpadded
   T* sim;
   int L;
-  int log2L;  // >= 0 iff fast pow2 path
+  int log2L;  // >= 4 iff power-of-two path
+  int kind;   // FftKind
+  unsigned long long rad;  // mixed radix: radices as 4-bit nibbles, stage 0 lowest
+  int nst;                 // mixed radix: number of stages
+  // Bluestein: padded work row of length M (power of two) and its tables
+  T* bre;
+  T* bim;
+  int M, log2M;
+  const cx<T>* twM;    // exp(-2 pi i m / M)
+  const cx<T>* chirp;  // w_n = exp(-i pi n^2 / L), n < L
+  const cx<T>* bhat;   // FFT_M(conj w wrapped), k < M
   int t;      // thread index in group
   int TPR;
   bool cta_sync;  // TPR > 32 -> group spans warps
@@ -383,30 +435,131 @@ __device__ __forceinline__ void fft_pow2(const Row<T>& row) {
     stockham_stage<T, 2, S>(row, Ns);
 }
 
-// direct DFT, any L (correctness path)
-template <typename T, int S>
-__device__ void dft_generic(const Row<T>& row) {
-  const int L = row.L;
-  if (row.active) {
-    for (int q = row.t; q < L; q += row.TPR) {
-      T ar = 0, ai = 0;
-      int m = 0;
-      for (int x = 0; x < L; ++x) {
-        const cx<T> v = row.ld(x);
-        cx<T> w = row.tw[m];
+// ---- mixed radix (prime factors <= 13) ------------------------------------
+// direct radix-R DFT with the row's length-L table: W_R^m = tw[m L / R]
+template <int R, int S, typename T>
+__device__ __forceinline__ void dft_tab(cx<T> (&x)[R], const cx<T>* __restrict__ tw, int LR) {
+  if constexpr (R == 2 || R == 3 || R == 4) {
+    dftR<R, S>(x);
+  } else {
+    cx<T> y[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      cx<T> a = x[0];
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        cx<T> w = ldg_cx(tw + ((r * q) % R) * LR);
         if (S > 0) w.y = -w.y;
-        ar += v.x * w.x - v.y * w.y;
-        ai += v.x * w.y + v.y * w.x;
-        m += q;
-        if (m >= L) m -= L;
+        a = add(a, mul(x[r], w));
       }
-      row.sre[q] = ar;
-      row.sim[q] = ai;
+      y[q] = a;
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) x[q] = y[q];
+  }
+}
+
+// one out-of-place Stockham stage of radix R: src -> dst (padded = row layout)
+template <int R, int S, typename T>
+__device__ __forceinline__ void mixed_stage(const Row<T>& row, int Ns, const T* sre, const T* sim, bool spad,
+                                            T* dre, T* dim, bool dpad) {
+  const int L = row.L, LR = L / R, tstride = L / (Ns * R);
+  for (int j = row.t; j < LR; j += row.TPR) {
+    const int k = j % Ns;
+    cx<T> x[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = j + r * LR;
+      const int p = spad ? pidx<T>(i) : i;
+      x[r] = mk(sre[p], sim[p]);
+    }
+    if (Ns > 1) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        cx<T> w = ldg_cx(row.tw + r * k * tstride);
+        if (S > 0) w.y = -w.y;
+        x[r] = mul(x[r], w);
+      }
+    }
+    dft_tab<R, S>(x, row.tw, LR);
+    const int base = (j - k) * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = base + r * Ns;
+      const int p = dpad ? pidx<T>(i) : i;
+      dre[p] = x[r].x;
+      dim[p] = x[r].y;
+    }
+  }
+}
+
+template <typename T, int S>
+__device__ __noinline__ void fft_mixed(const Row<T>& row) {
+  // ping-pong row <-> scratch; every thread of the group runs the syncs
+  bool in_row = true;
+  int Ns = 1;
+  for (int s = 0; s < row.nst; ++s) {
+    const int R = int((row.rad >> (4 * s)) & 15u);
+    const T* sre = in_row ? row.re : row.sre;
+    const T* sim = in_row ? row.im : row.sim;
+    T* dre = in_row ? row.sre : row.re;
+    T* dim = in_row ? row.sim : row.im;
+    if (row.active) {
+      switch (R) {
+        case 2: mixed_stage<2, S>(row, Ns, sre, sim, in_row, dre, dim, !in_row); break;
+        case 3: mixed_stage<3, S>(row, Ns, sre, sim, in_row, dre, dim, !in_row); break;
+        case 4: mixed_stage<4, S>(row, Ns, sre, sim, in_row, dre, dim, !in_row); break;
+        case 5: mixed_stage<5, S>(row, Ns, sre, sim, in_row, dre, dim, !in_row); break;
+        default: mixed_stage<7, S>(row, Ns, sre, sim, in_row, dre, dim, !in_row); break;
+      }
+    }
+    row.sync();
+    Ns *= R;
+    in_row = !in_row;
+  }
+  if (!in_row) {  // result sits in the scratch: copy back
+    if (row.active)
+      for (int i = row.t; i < row.L; i += row.TPR) row.st(i, mk(row.sre[i], row.sim[i]));
+    row.sync();
+  }
+}
+
+// ---- Bluestein (any L) -----------------------------------------------------
+// forward: X_k = w_k sum_n (x_n w_n) b_{k-n}, b_m = conj(w_m) (cyclic, length
+// M >= 2L-1); backward = conj(forward(conj x)).
+template <typename T, int S>
+__device__ __noinline__ void fft_bluestein(const Row<T>& row) {
+  Row<T> m = row;  // the length-M work row (power-of-two Stockham)
+  m.re = row.bre;
+  m.im = row.bim;
+  m.L = row.M;
+  m.log2L = row.log2M;
+  m.tw = row.twM;
+  if (row.active) {
+    for (int n = row.t; n < row.M; n += row.TPR) {
+      cx<T> v = mk(T(0), T(0));
+      if (n < row.L) {
+        v = row.ld(n);
+        if (S > 0) v.y = -v.y;
+        v = mul(v, ldg_cx(row.chirp + n));
+      }
+      m.st(n, v);
     }
   }
   row.sync();
+  fft_pow2<T, -1>(m);
   if (row.active)
-    for (int q = row.t; q < L; q += row.TPR) row.st(q, mk(row.sre[q], row.sim[q]));
+    for (int k = row.t; k < row.M; k += row.TPR) m.st(k, mul(m.ld(k), ldg_cx(row.bhat + k)));
+  row.sync();
+  fft_pow2<T, +1>(m);
+  if (row.active) {
+    const T inv = T(1) / T(row.M);
+    for (int k = row.t; k < row.L; k += row.TPR) {
+      cx<T> v = scale(mul(m.ld(k), ldg_cx(row.chirp + k)), inv);
+      if (S > 0) v.y = -v.y;
+      row.st(k, v);
+    }
+  }
   row.sync();
 }
 
@@ -414,10 +567,12 @@ __device__ void dft_generic(const Row<T>& row) {
 // read the result right after (ends with a sync).
 template <typename T, int S>
 __device__ __forceinline__ void fft(const Row<T>& row) {
-  if (row.log2L >= 4)
+  if (row.kind == kFftPow2)
     fft_pow2<T, S>(row);
+  else if (row.kind == kFftMixed)
+    fft_mixed<T, S>(row);
   else
-    dft_generic<T, S>(row);
+    fft_bluestein<T, S>(row);
 }
 
 }  // namespace lg

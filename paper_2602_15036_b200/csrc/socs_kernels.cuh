@@ -19,11 +19,19 @@
 
 namespace lg {
 
+// per-length transform tables (filled by make_tab in capi.cu)
 template <typename T>
 struct Tab {
   const cx<T>* tw;  // exp(-2 pi i m / L)
   int L;
-  int log2L;  // >= 4 for the radix-16 Stockham path, -1 for direct DFT
+  int log2L;  // >= 4 for the radix-16 Stockham path, else -1
+  int kind;   // FftKind (fft.cuh)
+  int nst;    // mixed radix: stages, radices as nibbles in rad
+  unsigned long long rad;
+  int M, log2M;        // Bluestein convolution length (0 otherwise)
+  const cx<T>* twM;    // exp(-2 pi i m / M)
+  const cx<T>* chirp;  // exp(-i pi n^2 / L), n < L
+  const cx<T>* bhat;   // FFT_M of the wrapped conj chirp
 };
 
 template <typename T>
@@ -41,13 +49,24 @@ __host__ __device__ inline bool fast_len(int L) {
   return is_pow2(L) && L >= 16;
 }
 
-// elements of T: row A + row B + generic scratch + reduce area (32 doubles)
+// elements of T of the group scratch: the mixed-radix ping-pong row
+// (unpadded, max(LA, LB) complex) and the Bluestein work row (padded, M
+// complex) share it (a transform uses one or the other)
+template <typename T>
+__host__ __device__ inline int scratch_elems(int LA, int LB) {
+  const bool gen = !fast_len<T>(LA) || (LB && !fast_len<T>(LB));
+  const int mb = imax(blue_len(LA), LB ? blue_len(LB) : 0);
+  int e = gen ? 2 * imax(LA, LB) : 0;
+  if (mb) e = imax(e, 2 * padded_len<T>(mb));
+  return e;
+}
+
+// elements of T: row A + row B + scratch + reduce area (32 doubles)
 template <typename T>
 __host__ __device__ inline int group_elems(int LA, int LB) {
   int e = 2 * padded_len<T>(LA);
   if (LB) e += 2 * padded_len<T>(LB);
-  const bool gen = !fast_len<T>(LA) || (LB && !fast_len<T>(LB));
-  if (gen) e += 2 * imax(LA, LB);
+  e += scratch_elems<T>(LA, LB);
   e += 32 * 8 / int(sizeof(T));
   e = (e + 3) & ~3;
   return e;
@@ -55,7 +74,7 @@ __host__ __device__ inline int group_elems(int LA, int LB) {
 
 template <typename T>
 __host__ __device__ inline int group_threads(int LA, int LB) {
-  return imax(tpr_for(LA), LB ? tpr_for(LB) : 1);
+  return imax(fft_tpr(LA), LB ? fft_tpr(LB) : 1);
 }
 
 template <typename T>
@@ -77,8 +96,7 @@ struct Group {
     return base + 2 * padded_len<T>(LA) + (LB ? 2 * padded_len<T>(LB) : 0);
   }
   __device__ double* red() const {
-    const bool gen = !fast_len<T>(LA) || (LB && !fast_len<T>(LB));
-    return reinterpret_cast<double*>(scratch() + (gen ? 2 * imax(LA, LB) : 0));
+    return reinterpret_cast<double*>(scratch() + scratch_elems<T>(LA, LB));
   }
   __device__ Row<T> row(int which, const Tab<T>& tab, bool active) const {
     Row<T> r;
@@ -88,7 +106,17 @@ struct Group {
     r.sre = scratch();
     r.sim = r.sre + imax(LA, LB);
     r.log2L = tab.log2L;
-    r.TPR = tpr_for(tab.L);
+    r.kind = tab.kind;
+    r.nst = tab.nst;
+    r.rad = tab.rad;
+    r.bre = scratch();
+    r.bim = r.bre + padded_len<T>(tab.M > 0 ? tab.M : 1);
+    r.M = tab.M;
+    r.log2M = tab.log2M;
+    r.twM = tab.twM;
+    r.chirp = tab.chirp;
+    r.bhat = tab.bhat;
+    r.TPR = fft_tpr(tab.L);
     r.t = t;
     r.active = active && t < r.TPR;
     r.cta_sync = G > 32;
