@@ -24,9 +24,17 @@ CPP_SOURCES = ["host/socs_kernels.cpp", "host/layout_io.cpp"]
 JSON_INC = os.environ.get("LITHO_JSON_INC", "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/"
                                            "cudnn_frontend/thirdparty/nlohmann")
 CUDA_INC = "/usr/local/cuda/include"
-DEPS = ["csrc/fft.cuh", "csrc/geom.h", "csrc/socs_kernels.cuh", "csrc/raster_kernels.cuh",
-        "csrc/util_kernels.cuh", "csrc/fftr.cuh", "csrc/socs_fast.h", "csrc/socs_fast.cuh",
-        "csrc/fast_common.cuh", "csrc/contour_kernels.cuh", "../include/lithogpu.h"]
+_FAST = ["csrc/fast_common.cuh", "csrc/socs_fast.cuh", "csrc/fftr.cuh", "csrc/fft.cuh", "csrc/socs_fast.h",
+         "csrc/geom.h"]
+# per-source header dependencies (incremental rebuilds)
+DEPS = {
+    "csrc/capi.cu": ["csrc/fft.cuh", "csrc/geom.h", "csrc/socs_kernels.cuh", "csrc/raster_kernels.cuh",
+                     "csrc/util_kernels.cuh", "csrc/socs_fast.h", "csrc/contour_kernels.cuh",
+                     "../include/lithogpu.h"],
+    "csrc/fast_rows.cu": _FAST,
+    "csrc/fast_cols.cu": _FAST,
+    "csrc/kernelgen.cu": ["../include/lithogpu.h"],
+}
 
 
 def _newer(target, sources):
@@ -55,7 +63,7 @@ def build(force: bool = False, verbose: bool = False, out: str = OUT, defines=()
     for src in CU_SOURCES:
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         objs.append(obj)
-        if force or _newer(obj, [src] + DEPS):
+        if force or _newer(obj, [src] + DEPS[src] + [os.path.relpath(__file__, HERE)]):
             jobs.append([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *dflags,
                          "-Xptxas", "-v" if verbose else "-O3", "-c", src, "-o", obj])
     for src in CPP_SOURCES:

@@ -126,6 +126,12 @@ inline void pdl_launch(K kern, dim3 grid, dim3 block, size_t smem, cudaStream_t 
   cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
+// LITHOGPU_NO_SPARSE=1: dense first / last FFT stages everywhere (A/B)
+inline bool sparse_off() {
+  static const bool off = std::getenv("LITHOGPU_NO_SPARSE") != nullptr;
+  return off;
+}
+
 inline int cdivi(long long a, long long b) { return int((a + b - 1) / b); }
 
 }  // namespace lg

@@ -36,10 +36,12 @@ void fl_real_rows_fwd(const FGeo& g, cudaStream_t s, int tiles, int mode, const 
     const int gr = fgroups<L>(256);
     const dim3 grid(cdivi((g.ay.N + 1) / 2, gr), 1, tiles);
     const size_t extra = size_t(Pout + 1) * 2 * gr * sizeof(C32) + 16;  // transposed-store tile
+    auto go = [&](auto kern) { flaunch_x<L>(kern, grid, gr, extra, s, g, src, src_ts, steep, Pout, out, out_ts); };
+    const bool sp = Pout < RPlan<L>::TPR && !sparse_off();
     if (mode == 0)
-      flaunch_x<L>(fk_real_rows_fwd<L, 0>, grid, gr, extra, s, g, src, src_ts, steep, Pout, out, out_ts);
+      sp ? go(fk_real_rows_fwd<L, 0, true>) : go(fk_real_rows_fwd<L, 0, false>);
     else
-      flaunch_x<L>(fk_real_rows_fwd<L, 1>, grid, gr, extra, s, g, src, src_ts, steep, Pout, out, out_ts);
+      sp ? go(fk_real_rows_fwd<L, 1, true>) : go(fk_real_rows_fwd<L, 1, false>);
   });
 }
 
@@ -50,7 +52,13 @@ void fl_socs_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* T, long l
     constexpr int L = decltype(c)::value;
     int gr = fgroups<L>(256);
     if (gr > g.K) gr = g.K;
-    flaunch<L>(fk_socs_rows<L>, dim3(g.ay.n, g.F, tiles), gr, s, g, T, t_ts, wk, wk2, dose, Ir, ir_ts, Eo, e_ts);
+    auto go = [&](auto kern) {
+      flaunch<L>(kern, dim3(g.ay.n, g.F, tiles), gr, s, g, T, t_ts, wk, wk2, dose, Ir, ir_ts, Eo, e_ts);
+    };
+    if (centered_band(L, RPlan<L>::E, g.ax.lo, g.ax.hi) && !sparse_off())
+      go(fk_socs_rows<L, true>);
+    else
+      go(fk_socs_rows<L, false>);
   });
 }
 
@@ -60,8 +68,16 @@ void fl_resist_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* Rc, lon
   with_len(g.ax.N, [&](auto c) {
     constexpr int L = decltype(c)::value;
     const int gr = fgroups<L>(256);
-    flaunch_x<L>(fk_resist_rows<L>, dim3(cdivi((g.ay.N + 1) / 2, gr), g.F, tiles), gr, row_slab_bytes<L>(gr) + size_t(g.ax.P + 1) * 2 * gr * sizeof(C32) + 16, s, g, Rc,
-                c_ts, target, tg_ts, cf, beta, thr, Dr, d_ts, costp, cp_ts);
+    auto go = [&](auto kern) {
+      flaunch_x<L>(kern, dim3(cdivi((g.ay.N + 1) / 2, gr), g.F, tiles), gr,
+                   row_slab_bytes<L>(gr) + size_t(g.ax.P + 1) * 2 * gr * sizeof(C32) + 16, s, g, Rc, c_ts, target,
+                   tg_ts, cf, beta, thr, Dr, d_ts, costp, cp_ts);
+    };
+    // band inside the first / last register slot: sparse first / last FFT stage
+    if (g.ax.P < RPlan<L>::TPR && !sparse_off())
+      go(fk_resist_rows<L, true>);
+    else
+      go(fk_resist_rows<L, false>);
   });
 }
 
@@ -94,10 +110,18 @@ void fl_adj_rows(const FGeo& g, cudaStream_t s, int tiles, int nf, bool uniform,
     const dim3 grid(cdivi(g.ay.n, gr), nf * g.K, tiles);
     const size_t extra = size_t(g.ax.B) * (gr | 1) * sizeof(C32);  // staging tile
     auto go = [&](auto kern) { flaunch_x<L>(kern, grid, gr, extra, s, g, T, t_ts, Wsub, ws_ts, U, u_ts); };
-    if (uniform)
-      from_e ? go(fk_adj_rows<L, true, true>) : go(fk_adj_rows<L, true, false>);
-    else
-      from_e ? go(fk_adj_rows<L, false, true>) : go(fk_adj_rows<L, false, false>);
+    const bool cb = centered_band(L, RPlan<L>::E, g.ax.lo, g.ax.hi) && !sparse_off();
+    if (cb) {
+      if (uniform)
+        from_e ? go(fk_adj_rows<L, true, true, true>) : go(fk_adj_rows<L, true, false, true>);
+      else
+        from_e ? go(fk_adj_rows<L, false, true, true>) : go(fk_adj_rows<L, false, false, true>);
+    } else {
+      if (uniform)
+        from_e ? go(fk_adj_rows<L, true, true, false>) : go(fk_adj_rows<L, true, false, false>);
+      else
+        from_e ? go(fk_adj_rows<L, false, true, false>) : go(fk_adj_rows<L, false, false, false>);
+    }
   });
 }
 
@@ -109,12 +133,15 @@ void fl_grad_rows(const FGeo& g, cudaStream_t s, int tiles, bool ilt, const C32*
     const int gr = fgroups<L>(256);
     const dim3 grid(cdivi((g.ay.N + 1) / 2, gr), 1, tiles);
     const size_t extra = row_slab_bytes<L>(gr) + size_t(g.ax.Pm + 1) * 2 * gr * sizeof(C32) + 16;
+    const bool sp = g.ax.Pm < RPlan<L>::TPR && !sparse_off();
+    auto go = [&](auto kern, size_t ex) {
+      flaunch_x<L>(kern, grid, gr, ex, s, g, Gc, g_ts, grad, gr_ts, theta, th_ts, steep, step, Mr, mr_ts, gmaxp,
+                   gm_ts);
+    };
     if (ilt)
-      flaunch_x<L>(fk_grad_rows<L, true>, grid, gr, extra, s, g, Gc, g_ts, grad, gr_ts, theta, th_ts, steep,
-                  step, Mr, mr_ts, gmaxp, gm_ts);
+      sp ? go(fk_grad_rows<L, true, true>, extra) : go(fk_grad_rows<L, true, false>, extra);
     else
-      flaunch<L>(fk_grad_rows<L, false>, grid, gr, s, g, Gc, g_ts, grad, gr_ts, theta, th_ts,
-                  steep, step, Mr, mr_ts, gmaxp, gm_ts);
+      sp ? go(fk_grad_rows<L, false, true>, 0) : go(fk_grad_rows<L, false, false>, 0);
   });
 }
 

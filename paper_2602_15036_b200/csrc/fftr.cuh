@@ -17,6 +17,8 @@
 // forward, +1 backward, unnormalized.
 #pragma once
 
+#include <utility>
+
 #include "fft.cuh"
 
 namespace lg {
@@ -199,13 +201,73 @@ __device__ __forceinline__ GSync make_gsync(int gid, int groups) {
   return s;
 }
 
-template <typename T, int L, int SIGN, int S, typename X>
+// a * exp(S 2 pi i Q / R), R a power of two <= 16, any Q (compile-time rotations)
+template <int R, int Q, int S, typename T>
+__device__ __forceinline__ cx<T> rot(cx<T> a) {
+  constexpr int q = ((Q % R) + R) % R;
+  if constexpr (R >= 2 && 2 * q >= R) {
+    const cx<T> b = rot<R, q - R / 2, S>(a);
+    return mk(-b.x, -b.y);
+  } else if constexpr (R >= 4 && 4 * q >= R) {
+    return mul_si<S>(rot<R, q - R / 4, S>(a));
+  } else {
+    return twc<R, q, S>(a);  // q < R/4: 0, (R=16) 1..3, (R=8) 1
+  }
+}
+
+// y_q = a + b W^{S q (R-1)}, q < R
+template <int R, int SIGN, typename T, int... Q>
+__device__ __forceinline__ void sp_in_outputs(cx<T> (&y)[R], cx<T> a, cx<T> b, std::integer_sequence<int, Q...>) {
+  ((y[Q] = add(a, rot<R, Q * (R - 1), SIGN>(b))), ...);
+}
+// output q = R-1 of a radix-R DFT: sum_r x_r W^{S r (R-1)}
+template <int R, int SIGN, typename T, int... Q>
+__device__ __forceinline__ cx<T> sp_out_last(const cx<T> (&x)[R], std::integer_sequence<int, Q...>) {
+  cx<T> y = x[0];
+  ((Q > 0 ? (y = add(y, rot<R, Q * (R - 1), SIGN>(x[Q]))) : y), ...);
+  return y;
+}
+
+__host__ __device__ constexpr bool pow2r(int r) { return r == 2 || r == 4 || r == 8 || r == 16; }
+
+// Sparsity flags of fftr (band-limited rows):
+//   kSpIn:  only v[0] and v[E-1] are nonzero on entry (a band |p| < TPR);
+//   kSpOut: only v[0] and v[E-1] are needed on exit (the other slots are left
+//           undefined).  Each flag is honoured where the stage structure
+//           allows it (power-of-two radix, one butterfly per thread in the
+//           stage concerned) and ignored otherwise (the dense path is exact).
+constexpr int kSpIn = 1, kSpOut = 2;
+
+template <typename T, int L, int SIGN, int S, typename X, int SP = 0>
 __device__ __forceinline__ void fftr_stage(cx<T> (&v)[RPlan<L>::E], cx<T>* sm,
                                            const cx<T>* __restrict__ tw, int t, const GSync& sync) {
   using P = RPlan<L>;
   using G = Stg<L, S>;
   constexpr int E = P::E, R = G::R, NB = E / R, TPR = P::TPR, Ns = G::Ns;
   constexpr bool FIRST = S == 0, LAST = S == P::NS - 1;
+  constexpr bool SP_IN = FIRST && (SP & kSpIn) && NB == 1 && pow2r(R);
+  constexpr bool SP_OUT = LAST && (SP & kSpOut) && pow2r(R) && !FIRST;
+  if constexpr (SP_IN) {
+    // y_q = v0 + v_{R-1} W^{S q (R-1)}: one rotation per output
+    const cx<T> a = v[0], b = v[R - 1];
+    cx<T> y[R];
+    sp_in_outputs<R, SIGN>(y, a, b, std::make_integer_sequence<int, R>{});
+    if constexpr (LAST) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r] = y[r];
+      return;
+    } else {
+      sync();
+      constexpr int SWc = X::sw < 0 ? 0 : X::sw;
+      // Ns = 1: butterfly j = t writes t*R + r
+#pragma unroll
+      for (int r = 0; r < R; ++r) X::template st<T>(sm, L, t * R + r, y[r]);
+      (void)SWc;
+      sync();
+      fftr_stage<T, L, SIGN, S + 1, X, SP>(v, sm, tw, t, sync);
+      return;
+    }
+  }
   cx<T> x[NB][R];
   cx<T> w[NB][R];
   if constexpr (Ns > 1) {
@@ -247,7 +309,18 @@ __device__ __forceinline__ void fftr_stage(cx<T> (&v)[RPlan<L>::E], cx<T>* sm,
         x[b][r] = mul(x[b][r], ww);
       }
     }
-    dftR<R, SIGN>(x[b]);
+    if constexpr (!SP_OUT) dftR<R, SIGN>(x[b]);
+  }
+  if constexpr (SP_OUT) {
+    // only outputs q = 0 of butterfly 0 (-> v[0]) and q = R-1 of butterfly
+    // NB-1 (-> v[E-1]) are needed
+    cx<T> y0 = x[0][0];
+#pragma unroll
+    for (int r = 1; r < R; ++r) y0 = add(y0, x[0][r]);
+    const cx<T> y1 = sp_out_last<R, SIGN>(x[NB - 1], std::make_integer_sequence<int, R>{});
+    v[0] = y0;
+    v[E - 1] = y1;
+    return;
   }
   if constexpr (LAST) {
 #pragma unroll
@@ -277,15 +350,21 @@ __device__ __forceinline__ void fftr_stage(cx<T> (&v)[RPlan<L>::E], cx<T>* sm,
       }
     }
     sync();
-    fftr_stage<T, L, SIGN, S + 1, X>(v, sm, tw, t, sync);
+    fftr_stage<T, L, SIGN, S + 1, X, SP>(v, sm, tw, t, sync);
   }
 }
 
-// In-register FFT of the row held in the natural distribution.
-template <typename T, int L, int SIGN, typename X = typename XchOf<L>::type>
+// In-register FFT of the row held in the natural distribution (SP: kSpIn /
+// kSpOut sparsity flags, see fftr_stage).
+template <typename T, int L, int SIGN, typename X = typename XchOf<L>::type, int SP = 0>
 __device__ __forceinline__ void fftr(cx<T> (&v)[RPlan<L>::E], cx<T>* sm,
                                      const cx<T>* __restrict__ tw, int t, const GSync& sync) {
-  fftr_stage<T, L, SIGN, 0, X>(v, sm, tw, t, sync);
+  fftr_stage<T, L, SIGN, 0, X, SP>(v, sm, tw, t, sync);
+}
+template <typename T, int L, int SIGN, int SP>
+__device__ __forceinline__ void fftr_sp(cx<T> (&v)[RPlan<L>::E], cx<T>* sm,
+                                        const cx<T>* __restrict__ tw, int t, const GSync& sync) {
+  fftr_stage<T, L, SIGN, 0, typename XchOf<L>::type, SP>(v, sm, tw, t, sync);
 }
 
 // Store the natural-distribution row into sm (padded) so any element can be

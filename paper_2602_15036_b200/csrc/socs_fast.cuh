@@ -73,7 +73,14 @@ struct FGroup {
   __device__ __forceinline__ int idx(int e) const { return t + e * TPR; }
 };
 
-__device__ __forceinline__ float fsig(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
+// logistic sigmoid 1/(1+e^-x) on the SFU: ex2.approx.ftz + rcp.approx.ftz
+// (|rel err| ~ 2^-22; no denormal fix-up sequences)
+__device__ __forceinline__ float fsig(float x) {
+  float e, r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x * -1.4426950408889634f));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
+  return r;
+}
 
 // kernel-band slot of residue i mod L, or -1
 __device__ __forceinline__ int kslot(int i, int lo, int hi, int L) {
@@ -82,6 +89,35 @@ __device__ __forceinline__ int kslot(int i, int lo, int hi, int L) {
   r -= r >= L ? L : 0;
   return lo + r <= hi ? r : -1;
 }
+// Centered kernel band [lo, hi] (lo <= 0 <= hi, hi < L/2, -lo < L/2) of a
+// length-L register row in the natural distribution (E even, so L/2 is a
+// multiple of TPR): element e of thread t (index i = t + TPR e) lies in the
+// lower half when 2e < E and then has slot i - lo if i <= hi; in the upper
+// half it has slot i - L - lo if i >= L + lo.  So the slot is
+// base + off(e) with a per-thread base and a compile-time offset, and
+// validity is one bit per element: no per-element index arithmetic
+// (kslot) in the loops over kernels.  centered_band() checks the geometry
+// on the host.
+template <int L>
+struct BandMap {
+  static constexpr int E = RPlan<L>::E, TPR = RPlan<L>::TPR;
+  unsigned mask;  // bit e: element e is in the band
+  int base;       // t - lo
+  __host__ __device__ static constexpr int off(int e) { return TPR * e - (2 * e >= E ? L : 0); }
+  __device__ __forceinline__ BandMap(int t, int lo, int hi) : mask(0u), base(t - lo) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = t + TPR * e;
+      const bool in = (2 * e < E) ? (i <= hi) : (i >= L + lo);
+      mask |= in ? (1u << e) : 0u;
+    }
+  }
+  __device__ __forceinline__ bool has(int e) const { return (mask >> e) & 1u; }
+};
+__host__ __device__ inline bool centered_band(int L, int E, int lo, int hi) {
+  return E % 2 == 0 && lo <= 0 && hi >= 0 && 2 * hi < L && -2 * lo < L;
+}
+
 // intensity-band slot of residue i mod L (band2 layout of geom.h), or -1
 __device__ __forceinline__ int islot(const AxisGeom& a, int i, int L) {
   if (a.full) return i;  // full band: L == n == N, slot j = residue
@@ -96,10 +132,33 @@ __device__ __forceinline__ int islot(const AxisGeom& a, int i, int L) {
 // e holds indices t + e*TPR, so only e < ceil((P+1)/TPR) can hit [0, P] and
 // only e >= E - ceil(P/TPR) can hit the mirror [L-P, L): the other slots are
 // zero by a warp-uniform test, without per-element divergent branches.
-template <int L>
+template <int L, bool SPB = false>
 __device__ __forceinline__ void load_herm_pair(C32 (&v)[RPlan<L>::E], const FGroup<L>& g,
                                                const C32* a, const C32* b, int P, int ld) {
   constexpr int E = RPlan<L>::E, TPR = RPlan<L>::TPR;
+  if constexpr (SPB) {
+    // band P < TPR: only slot 0 (i = t <= P) and slot E-1 (mirror m = TPR - t
+    // <= P) can be nonzero
+    const int t = g.t, m = TPR - t;
+    C32 A = mk(0.f, 0.f), Bv = mk(0.f, 0.f), Am = mk(0.f, 0.f), Bm = mk(0.f, 0.f);
+    if (t <= P) {
+      A = a[size_t(t) * ld];
+      if (b) Bv = b[size_t(t) * ld];
+      if (t == 0) {
+        A.y = 0.f;
+        Bv.y = 0.f;
+      }
+    }
+    if (m <= P) {
+      Am = conjg(a[size_t(m) * ld]);
+      if (b) Bm = conjg(b[size_t(m) * ld]);
+    }
+    v[0] = mk(A.x - Bv.y, A.y + Bv.x);
+#pragma unroll
+    for (int e = 1; e < E - 1; ++e) v[e] = mk(0.f, 0.f);
+    v[E - 1] = mk(Am.x - Bm.y, Am.y + Bm.x);
+    return;
+  }
   const int nlo = (P + TPR) / TPR, nhi = (P + TPR - 1) / TPR;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
@@ -178,6 +237,14 @@ __device__ __forceinline__ void store_pair_cols(const FGroup<L>& G, size_t tile_
   }
 }
 
+// to_smem of the two slots a kSpOut transform defines (v[0], v[E-1])
+template <int L>
+__device__ __forceinline__ void to_smem_sp(const C32 (&v)[RPlan<L>::E], C32* sm, int t) {
+  constexpr int E = RPlan<L>::E, TPR = RPlan<L>::TPR;
+  sm[rpad(t)] = v[0];
+  sm[rpad(t + (E - 1) * TPR)] = v[E - 1];
+}
+
 // min resident CTAs for the full-resolution row kernels (64 registers with the
 // 2048 = 8*8*8*4 plan)
 #ifndef LG_FULLROW_MINB
@@ -197,7 +264,7 @@ __device__ __forceinline__ float warp_max(float v, int width) {
 // ===========================================================================
 // real row pairs -> half spectra [Pout+1][Ny] (MODE 0 raw, 1 sigmoid(steep x))
 // ===========================================================================
-template <int L, int MODE>
+template <int L, int MODE, bool SPB>
 __global__ void __launch_bounds__(256) fk_real_rows_fwd(FGeo g, const float* __restrict__ src,
                                                         long long src_ts, float steep, int Pout,
                                                         C32* __restrict__ out, long long out_ts) {
@@ -223,9 +290,15 @@ __global__ void __launch_bounds__(256) fk_real_rows_fwd(FGeo g, const float* __r
     }
     v[e] = mk(a, b);
   }
-  fftr<float, L, -1>(v, G.sm, g.twNx, G.t, G.sync);
+  // kSpOut when the output band fits the first / last slot: the same
+  // arithmetic as fk_grad_rows' fused next-iteration mask rows, so both
+  // producers of Mr agree bitwise
+  fftr_sp<float, L, -1, SPB ? kSpOut : 0>(v, G.sm, g.twNx, G.t, G.sync);
   G.sync();
-  to_smem<float, L>(v, G.sm, G.t);
+  if constexpr (SPB)
+    to_smem_sp<L>(v, G.sm, G.t);
+  else
+    to_smem<float, L>(v, G.sm, G.t);
   G.sync();
   store_pair_cols<L>(G, groups_bytes<L>(G.groups), out + blockIdx.z * out_ts, Ny,
                      2 * blockIdx.x * G.groups, Ny, Pout);
@@ -246,7 +319,7 @@ __global__ void __launch_bounds__(256) fk_real_rows_fwd(FGeo g, const float* __r
 #ifndef LG_SOCSROWS_MINB
 #define LG_SOCSROWS_MINB 3
 #endif
-template <int L>
+template <int L, bool CB>
 __global__ void __launch_bounds__(256, LG_SOCSROWS_MINB) fk_socs_rows(FGeo g, const C32* __restrict__ T,
                                                     long long t_ts, const float* __restrict__ wk,
                                                     const float* __restrict__ wk2, float dose,
@@ -260,21 +333,30 @@ __global__ void __launch_bounds__(256, LG_SOCSROWS_MINB) fk_socs_rows(FGeo g, co
   float acc[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) acc[e] = 0.f;
-  for (int k = G.gid; k < K; k += G.groups) {
+  const BandMap<L> bm(G.t, lo, hi);
+  // per-kernel row pointers advance by one kernel plane per slot
+  const long long tstep = (long long)ny * Bx, estep = (long long)ny * L;
+  const C32* src = T + blockIdx.z * t_ts + size_t(f * K + G.gid) * tstep + size_t(sy) * Bx;
+  C32* eo = Eo ? Eo + blockIdx.z * e_ts + (size_t(f * K + G.gid) * ny + sy) * L + G.t : nullptr;
+  for (int k = G.gid; k < K; k += G.groups, src += G.groups * tstep, eo += eo ? G.groups * estep : 0) {
     const int fk = f * K + k;
     if (g.slot_on && !g.slot_on[fk]) continue;  // empty slot (mixed kernel pairs)
-    const C32* src = T + blockIdx.z * t_ts + size_t(fk) * ny * Bx + size_t(sy) * Bx;
     C32 v[E];
+    if constexpr (CB) {
+      const C32* sb = src + bm.base;
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int sl = kslot(G.idx(e), lo, hi, L);
-      v[e] = sl >= 0 ? src[sl] : mk(0.f, 0.f);
+      for (int e = 0; e < E; ++e) v[e] = bm.has(e) ? sb[BandMap<L>::off(e)] : mk(0.f, 0.f);
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int sl = kslot(G.idx(e), lo, hi, L);
+        v[e] = sl >= 0 ? src[sl] : mk(0.f, 0.f);
+      }
     }
     fftr<float, L, +1>(v, G.sm, g.twnx, G.t, G.sync);
-    if (Eo) {  // keep the coherent field for the adjoint (fk_adj_rows<.., FROM_E>)
-      C32* eo = Eo + blockIdx.z * e_ts + (size_t(fk) * ny + sy) * L;
+    if (eo) {  // keep the coherent field for the adjoint (fk_adj_rows<.., FROM_E>)
 #pragma unroll
-      for (int e = 0; e < E; ++e) eo[G.idx(e)] = v[e];
+      for (int e = 0; e < E; ++e) eo[e * RPlan<L>::TPR] = v[e];
     }
     const float w = wk[fk] * dose;
     if (wk2) {  // kernel pair: E = E_a + i E_b with real E_a, E_b
@@ -317,7 +399,7 @@ __global__ void __launch_bounds__(256, LG_SOCSROWS_MINB) fk_socs_rows(FGeo g, co
 // Z = sig(beta (R - thr)), cost partial, D = 2 c_f (Z - Zt) beta Z (1 - Z),
 // FFT_Nx(D pair) -> Dr[f][px][y].  grid (ceil(Ny/2/groups), F, tiles)
 // ===========================================================================
-template <int L>
+template <int L, bool SPB>
 __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_resist_rows(FGeo g, const C32* __restrict__ Rc,
                                                       long long c_ts, const float* __restrict__ target,
                                                       long long tg_ts, const float* __restrict__ cf,
@@ -328,6 +410,7 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_resist_rows(FGeo g, c
   TraceScope trace_(g);
   constexpr int E = RPlan<L>::E, TPR = RPlan<L>::TPR;
   constexpr int WPG = TPR >= 32 ? TPR / 32 : 1;
+  constexpr int SP_IN = SPB ? kSpIn : 0, SP_OUT = SPB ? kSpOut : 0;
   const int Ny = g.ay.N, Px = g.ax.P, f = blockIdx.y, npairs = (Ny + 1) / 2;
   const int pair0 = blockIdx.x * G.groups + G.gid;
   const bool act = pair0 < npairs;
@@ -340,32 +423,33 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_resist_rows(FGeo g, c
   float* tsl = row_slab<L>(G.groups, G.gid);
   stage_rows_async<L>(tsl, tg + size_t(y0) * L, tg + size_t(has1 ? y1 : y0) * L, G.t);
   C32 v[E];
-  load_herm_pair<L>(v, G, rc + y0, has1 ? rc + y1 : nullptr, Px, Ny);  // column-major [px][y]
-  fftr<float, L, +1>(v, G.sm, g.twNx, G.t, G.sync);
+  load_herm_pair<L, SPB>(v, G, rc + y0, has1 ? rc + y1 : nullptr, Px, Ny);  // column-major [px][y]
+  fftr_sp<float, L, +1, SP_IN>(v, G.sm, g.twNx, G.t, G.sync);
   stage_wait();
   G.sync();
-  const float w = cf[f];
-  float c = 0.f;
+  // branch-free pointwise resist: an odd last row (no partner) is masked by h1
+  const float w = cf[f], h1 = has1 ? 1.f : 0.f;
+  const float k2 = 2.f * w * beta;
+  float c0 = 0.f, c1 = 0.f;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const float z0 = fsig(beta * (v[e].x - thr));
+    const float z1 = fsig(beta * (v[e].y - thr));
     const float e0 = z0 - tsl[G.idx(e)];
-    float d1 = 0.f;
-    c += e0 * e0;
-    if (has1) {
-      const float z1 = fsig(beta * (v[e].y - thr));
-      const float e1 = z1 - tsl[L + G.idx(e)];
-      c += e1 * e1;
-      d1 = 2.f * w * e1 * beta * z1 * (1.f - z1);
-    }
-    v[e] = mk(2.f * w * e0 * beta * z0 * (1.f - z0), d1);
+    const float e1 = z1 - tsl[L + G.idx(e)];
+    c0 += e0 * e0;
+    c1 += e1 * e1;
+    v[e] = mk(k2 * e0 * (z0 - z0 * z0), h1 * (k2 * e1 * (z1 - z1 * z1)));
   }
-  c = warp_sum(c * w, TPR < 32 ? TPR : 32);
+  float c = warp_sum((c0 + h1 * c1) * w, TPR < 32 ? TPR : 32);
   if (act && (G.t & 31) == 0)
     costp[blockIdx.z * cp_ts + (size_t(f) * npairs + pair) * WPG + (G.t >> 5)] = double(c);
-  fftr<float, L, -1>(v, G.sm, g.twNx, G.t, G.sync);
+  fftr_sp<float, L, -1, SP_OUT>(v, G.sm, g.twNx, G.t, G.sync);
   G.sync();
-  to_smem<float, L>(v, G.sm, G.t);
+  if constexpr (SPB)
+    to_smem_sp<L>(v, G.sm, G.t);
+  else
+    to_smem<float, L>(v, G.sm, G.t);
   G.sync();
   store_pair_cols<L>(G, groups_bytes<L>(G.groups) + row_slab_bytes<L>(G.groups),
                      Dr + blockIdx.z * d_ts + size_t(f) * (Px + 1) * Ny, Ny, 2 * blockIdx.x * G.groups, Ny, Px);
@@ -444,14 +528,14 @@ __global__ void __launch_bounds__(256) fk_wlp_rows(FGeo g, const C32* __restrict
 #ifndef LG_ADJROWS_MINB
 #define LG_ADJROWS_MINB 4  // C5 A/B: 4 CTAs/SM (64 regs) +3.4 % per iteration over 2 (profiles/r2_ab1_occupancy.log)
 #endif
-template <int L, bool UNIFORM, bool FROM_E>
+template <int L, bool UNIFORM, bool FROM_E, bool CB>
 __global__ void __launch_bounds__(256, LG_ADJROWS_MINB) fk_adj_rows(FGeo g, const C32* __restrict__ T,
                                                       long long t_ts, const float* __restrict__ Wsub,
                                                       long long ws_ts, C32* __restrict__ U,
                                                       long long u_ts) {
   FGroup<L> G;
   TraceScope trace_(g);
-  constexpr int E = RPlan<L>::E;
+  constexpr int E = RPlan<L>::E, TPR = RPlan<L>::TPR;
   const int ny = g.ay.n, Bx = g.ax.B, K = g.K, lo = g.ax.lo, hi = g.ax.hi;
   const int fk = blockIdx.y, f = fk / K;
   if (g.slot_on && !g.slot_on[fk]) return;  // empty slot: U never read
@@ -459,11 +543,16 @@ __global__ void __launch_bounds__(256, LG_ADJROWS_MINB) fk_adj_rows(FGeo g, cons
   const int sy0 = r0 + G.gid;
   const bool act = sy0 < ny;
   const int sy = act ? sy0 : ny - 1;
+  const BandMap<L> bm(G.t, lo, hi);
   C32 v[E];
   if (FROM_E) {  // T holds the fields E_fk[sy][x] kept by fk_socs_rows
-    const C32* src = T + blockIdx.z * t_ts + (size_t(fk) * ny + sy) * L;
+    const C32* src = T + blockIdx.z * t_ts + (size_t(fk) * ny + sy) * L + G.t;
 #pragma unroll
-    for (int e = 0; e < E; ++e) v[e] = src[G.idx(e)];
+    for (int e = 0; e < E; ++e) v[e] = src[e * TPR];
+  } else if (CB) {
+    const C32* sb = T + blockIdx.z * t_ts + size_t(fk) * ny * Bx + size_t(sy) * Bx + bm.base;
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = bm.has(e) ? sb[BandMap<L>::off(e)] : mk(0.f, 0.f);
   } else {
     const C32* src = T + blockIdx.z * t_ts + size_t(fk) * ny * Bx + size_t(sy) * Bx;
 #pragma unroll
@@ -474,9 +563,9 @@ __global__ void __launch_bounds__(256, LG_ADJROWS_MINB) fk_adj_rows(FGeo g, cons
   }
   float wv[E];
   if (!UNIFORM) {
-    const float* w = Wsub + blockIdx.z * ws_ts + (size_t(f) * ny + sy) * L;
+    const float* w = Wsub + blockIdx.z * ws_ts + (size_t(f) * ny + sy) * L + G.t;
 #pragma unroll
-    for (int e = 0; e < E; ++e) wv[e] = w[G.idx(e)];
+    for (int e = 0; e < E; ++e) wv[e] = w[e * TPR];
   }
   if (!FROM_E) fftr<float, L, +1>(v, G.sm, g.twnx, G.t, G.sync);
   if (!UNIFORM) {
@@ -489,10 +578,17 @@ __global__ void __launch_bounds__(256, LG_ADJROWS_MINB) fk_adj_rows(FGeo g, cons
   extern __shared__ __align__(16) unsigned char fsm_raw[];
   C32* tile = reinterpret_cast<C32*>(fsm_raw) + G.groups * rsm_len<L>();
   const int ld = G.groups | 1;
+  if constexpr (CB) {
+    C32* tb = tile + bm.base * ld + G.gid;
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int sl = kslot(G.idx(e), lo, hi, L);
-    if (sl >= 0) tile[sl * ld + G.gid] = v[e];
+    for (int e = 0; e < E; ++e)
+      if (bm.has(e)) tb[BandMap<L>::off(e) * ld] = v[e];
+  } else {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int sl = kslot(G.idx(e), lo, hi, L);
+      if (sl >= 0) tile[sl * ld + G.gid] = v[e];
+    }
   }
   __syncthreads();
   C32* o = U + blockIdx.z * u_ts + size_t(fk) * Bx * ny;
@@ -508,7 +604,7 @@ __global__ void __launch_bounds__(256, LG_ADJROWS_MINB) fk_adj_rows(FGeo g, cons
 // !ILT: write grad; ILT: theta update, then next iteration's mask rows.
 // grid (ceil(Ny/2/groups), 1, tiles)
 // ===========================================================================
-template <int L, bool ILT>
+template <int L, bool ILT, bool SPB>
 __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_grad_rows(FGeo g, const C32* __restrict__ Gc,
                                                     long long g_ts, float* __restrict__ grad,
                                                     long long gr_ts, float* __restrict__ theta,
@@ -519,6 +615,7 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_grad_rows(FGeo g, con
   TraceScope trace_(g);
   constexpr int E = RPlan<L>::E, TPR = RPlan<L>::TPR;
   constexpr int WPG = TPR >= 32 ? TPR / 32 : 1;
+  constexpr int SP_IN = SPB ? kSpIn : 0, SP_OUT = SPB ? kSpOut : 0;
   const int Ny = g.ay.N, Pm = g.ax.Pm, npairs = (Ny + 1) / 2;
   const int pair0 = blockIdx.x * G.groups + G.gid;
   const bool act = pair0 < npairs;
@@ -533,8 +630,8 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_grad_rows(FGeo g, con
     stage_rows_async<L>(tsl, th + size_t(y0) * L, th + size_t(has1 ? y1 : y0) * L, G.t);
   }
   C32 v[E];
-  load_herm_pair<L>(v, G, gc + y0, has1 ? gc + y1 : nullptr, Pm, Ny);  // column-major [px][y]
-  fftr<float, L, +1>(v, G.sm, g.twNx, G.t, G.sync);
+  load_herm_pair<L, SPB>(v, G, gc + y0, has1 ? gc + y1 : nullptr, Pm, Ny);  // column-major [px][y]
+  fftr_sp<float, L, +1, SP_IN>(v, G.sm, g.twNx, G.t, G.sync);
   if (ILT) {
     stage_wait();
     G.sync();
@@ -550,35 +647,40 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_grad_rows(FGeo g, con
     }
     return;
   }
+  // theta update, dL/dtheta = dL/dM * steep M (1 - M); rows written only by
+  // active groups, an odd last row (no partner) only for y0
   float gm = 0.f;
+  float* th0 = th + size_t(y0) * L;
+  float* th1 = th + size_t(has1 ? y1 : y0) * L;
+  float* gr0 = grad ? grad + blockIdx.z * gr_ts + size_t(y0) * L : nullptr;
+  float* gr1 = grad ? grad + blockIdx.z * gr_ts + size_t(has1 ? y1 : y0) * L : nullptr;
+  const bool w1 = act && has1;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int i = G.idx(e);
     const float t0 = tsl[i];
+    const float t1 = tsl[L + i];
     const float m0 = fsig(steep * t0);
-    const float g0 = v[e].x * steep * m0 * (1.f - m0);
+    const float m1 = fsig(steep * t1);
+    const float g0 = v[e].x * steep * (m0 - m0 * m0);
+    const float g1 = v[e].y * steep * (m1 - m1 * m1);
     const float n0 = t0 - step * g0;
-    gm = fmaxf(gm, fabsf(g0));
-    float n1v = 0.f;
-    if (has1) {
-      const float t1 = tsl[L + i];
-      const float m1 = fsig(steep * t1);
-      const float g1 = v[e].y * steep * m1 * (1.f - m1);
-      const float n1 = t1 - step * g1;
-      gm = fmaxf(gm, fabsf(g1));
-      if (act) th[size_t(y1) * L + i] = n1;
-      if (grad && act) grad[blockIdx.z * gr_ts + size_t(y1) * L + i] = g1;
-      n1v = fsig(steep * n1);
-    }
-    if (act) th[size_t(y0) * L + i] = n0;
-    if (grad && act) grad[blockIdx.z * gr_ts + size_t(y0) * L + i] = g0;  // dL/dtheta (lithogpu_ilt_gradient)
-    v[e] = mk(fsig(steep * n0), n1v);
+    const float n1 = t1 - step * g1;
+    gm = fmaxf(gm, fmaxf(fabsf(g0), has1 ? fabsf(g1) : 0.f));
+    if (act) th0[i] = n0;
+    if (w1) th1[i] = n1;
+    if (gr0 && act) gr0[i] = g0;  // dL/dtheta (lithogpu_ilt_gradient)
+    if (gr0 && w1) gr1[i] = g1;
+    v[e] = mk(fsig(steep * n0), has1 ? fsig(steep * n1) : 0.f);
   }
   gm = warp_max(gm, TPR < 32 ? TPR : 32);
   if (act && gmaxp && (G.t & 31) == 0) gmaxp[blockIdx.z * gm_ts + size_t(pair) * WPG + (G.t >> 5)] = gm;
-  fftr<float, L, -1>(v, G.sm, g.twNx, G.t, G.sync);
+  fftr_sp<float, L, -1, SP_OUT>(v, G.sm, g.twNx, G.t, G.sync);
   G.sync();
-  to_smem<float, L>(v, G.sm, G.t);
+  if constexpr (SPB)
+    to_smem_sp<L>(v, G.sm, G.t);
+  else
+    to_smem<float, L>(v, G.sm, G.t);
   G.sync();
   store_pair_cols<L>(G, groups_bytes<L>(G.groups) + row_slab_bytes<L>(G.groups), Mr + blockIdx.z * mr_ts, Ny,
                      2 * blockIdx.x * G.groups, Ny, Pm);

@@ -4,7 +4,7 @@ ILT iterations), in-graph, best of `reps`; each variant in a fresh process
 (LITHOGPU_LIB).  Also checks the variant's per-iteration costs against the
 first (baseline) variant.
 
-  python tools/ab_c5.py [--iters 10] [--reps 5] [--tiles 32] name=path ...
+  python tools/ab_c5.py [--iters 10] [--reps 5] [--tiles 32] name=path[,VAR=VAL...] ...
 """
 import argparse
 import json
@@ -61,6 +61,11 @@ def main():
     for v in a.variants:
         name, path = v.split("=", 1)
         env = dict(os.environ)
+        # name=path[,VAR=VAL...]: extra environment for the variant
+        path, *kv = path.split(",")
+        for x in kv:
+            k, val = x.split("=", 1)
+            env[k] = val
         if path != "default":
             env["LITHOGPU_LIB"] = os.path.abspath(path)
         r = subprocess.run([sys.executable, "-c", CHILD, a.config, str(a.iters), str(a.reps), str(a.tiles)],
