@@ -1,5 +1,7 @@
 // fp32 fast path: row-kernel launchers (see socs_fast.h).
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "fast_common.cuh"
 
@@ -107,9 +109,15 @@ void fl_adj_rows(const FGeo& g, cudaStream_t s, int tiles, int nf, bool uniform,
   with_len(g.ax.n, [&](auto c) {
     constexpr int L = decltype(c)::value;
     const int gr = fgroups<L>(256);
-    const dim3 grid(cdivi(g.ay.n, gr), nf * g.K, tiles);
+    const int nfk = nf * g.K;
+    // kernel slots per CTA: keep >= ~8 CTAs per SM, amortise setup beyond that
+    const long long units = (long long)cdivi(g.ay.n, gr) * nfk * tiles;
+    int kc = int(units / (148 * 8));
+    kc = kc < 1 ? 1 : (kc > 8 ? 8 : kc);
+    if (const char* e = std::getenv("LITHOGPU_ADJ_KC")) kc = std::max(1, std::atoi(e));
+    const dim3 grid(cdivi(g.ay.n, gr), cdivi(nfk, kc), tiles);
     const size_t extra = size_t(g.ax.B) * (gr | 1) * sizeof(C32);  // staging tile
-    auto go = [&](auto kern) { flaunch_x<L>(kern, grid, gr, extra, s, g, T, t_ts, Wsub, ws_ts, U, u_ts); };
+    auto go = [&](auto kern) { flaunch_x<L>(kern, grid, gr, extra, s, g, T, t_ts, Wsub, ws_ts, U, u_ts, kc, nfk); };
     const bool cb = centered_band(L, RPlan<L>::E, g.ax.lo, g.ax.hi) && !sparse_off();
     if (cb) {
       if (uniform)

@@ -532,70 +532,80 @@ template <int L, bool UNIFORM, bool FROM_E, bool CB>
 __global__ void __launch_bounds__(256, LG_ADJROWS_MINB) fk_adj_rows(FGeo g, const C32* __restrict__ T,
                                                       long long t_ts, const float* __restrict__ Wsub,
                                                       long long ws_ts, C32* __restrict__ U,
-                                                      long long u_ts) {
+                                                      long long u_ts, int kc, int nfk) {
   FGroup<L> G;
   TraceScope trace_(g);
   constexpr int E = RPlan<L>::E, TPR = RPlan<L>::TPR;
   const int ny = g.ay.n, Bx = g.ax.B, K = g.K, lo = g.ax.lo, hi = g.ax.hi;
-  const int fk = blockIdx.y, f = fk / K;
-  if (g.slot_on && !g.slot_on[fk]) return;  // empty slot: U never read
   const int r0 = blockIdx.x * G.groups;
   const int sy0 = r0 + G.gid;
   const bool act = sy0 < ny;
   const int sy = act ? sy0 : ny - 1;
   const BandMap<L> bm(G.t, lo, hi);
-  C32 v[E];
-  if (FROM_E) {  // T holds the fields E_fk[sy][x] kept by fk_socs_rows
-    const C32* src = T + blockIdx.z * t_ts + (size_t(fk) * ny + sy) * L + G.t;
-#pragma unroll
-    for (int e = 0; e < E; ++e) v[e] = src[e * TPR];
-  } else if (CB) {
-    const C32* sb = T + blockIdx.z * t_ts + size_t(fk) * ny * Bx + size_t(sy) * Bx + bm.base;
-#pragma unroll
-    for (int e = 0; e < E; ++e) v[e] = bm.has(e) ? sb[BandMap<L>::off(e)] : mk(0.f, 0.f);
-  } else {
-    const C32* src = T + blockIdx.z * t_ts + size_t(fk) * ny * Bx + size_t(sy) * Bx;
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int sl = kslot(G.idx(e), lo, hi, L);
-      v[e] = sl >= 0 ? src[sl] : mk(0.f, 0.f);
-    }
-  }
-  float wv[E];
-  if (!UNIFORM) {
-    const float* w = Wsub + blockIdx.z * ws_ts + (size_t(f) * ny + sy) * L + G.t;
-#pragma unroll
-    for (int e = 0; e < E; ++e) wv[e] = w[e * TPR];
-  }
-  if (!FROM_E) fftr<float, L, +1>(v, G.sm, g.twnx, G.t, G.sync);
-  if (!UNIFORM) {
-#pragma unroll
-    for (int e = 0; e < E; ++e) v[e] = scale(v[e], wv[e]);
-  }
-  fftr<float, L, -1>(v, G.sm, g.twnx, G.t, G.sync);
-  // stage the band outputs as tile[slot][row] (odd stride: conflict free),
-  // then write U[fk][slot][r0 .. r0+groups) as contiguous row segments
   extern __shared__ __align__(16) unsigned char fsm_raw[];
   C32* tile = reinterpret_cast<C32*>(fsm_raw) + G.groups * rsm_len<L>();
   const int ld = G.groups | 1;
-  if constexpr (CB) {
-    C32* tb = tile + bm.base * ld + G.gid;
-#pragma unroll
-    for (int e = 0; e < E; ++e)
-      if (bm.has(e)) tb[BandMap<L>::off(e) * ld] = v[e];
-  } else {
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int sl = kslot(G.idx(e), lo, hi, L);
-      if (sl >= 0) tile[sl * ld + G.gid] = v[e];
-    }
-  }
-  __syncthreads();
-  C32* o = U + blockIdx.z * u_ts + size_t(fk) * Bx * ny;
   const int nr = min(G.groups, ny - r0);
-  for (int idx = threadIdx.x; idx < Bx * G.groups; idx += blockDim.x) {
-    const int sl = idx / G.groups, rr = idx - sl * G.groups;
-    if (rr < nr) o[size_t(sl) * ny + r0 + rr] = tile[sl * ld + rr];
+  const int lgg = __ffs(G.groups) - 1;  // groups is a power of two (fgroups)
+  // kc kernel slots per CTA (amortises the setup over several transforms)
+  int fk = blockIdx.y * kc, f = fk / K, kin = fk - f * K;
+  for (int it = 0; it < kc; ++it, ++fk, ++kin) {
+    if (kin == K) {
+      kin = 0;
+      ++f;
+    }
+    if (fk >= nfk) break;  // nfk = nf * K slots of this launch
+    if (g.slot_on && !g.slot_on[fk]) continue;  // empty slot: U never read (CTA-uniform)
+    C32 v[E];
+    if (FROM_E) {  // T holds the fields E_fk[sy][x] kept by fk_socs_rows
+      const C32* src = T + blockIdx.z * t_ts + (size_t(fk) * ny + sy) * L + G.t;
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[e] = src[e * TPR];
+    } else if (CB) {
+      const C32* sb = T + blockIdx.z * t_ts + size_t(fk) * ny * Bx + size_t(sy) * Bx + bm.base;
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[e] = bm.has(e) ? sb[BandMap<L>::off(e)] : mk(0.f, 0.f);
+    } else {
+      const C32* src = T + blockIdx.z * t_ts + size_t(fk) * ny * Bx + size_t(sy) * Bx;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int sl = kslot(G.idx(e), lo, hi, L);
+        v[e] = sl >= 0 ? src[sl] : mk(0.f, 0.f);
+      }
+    }
+    float wv[E];
+    if (!UNIFORM) {
+      const float* w = Wsub + blockIdx.z * ws_ts + (size_t(f) * ny + sy) * L + G.t;
+#pragma unroll
+      for (int e = 0; e < E; ++e) wv[e] = w[e * TPR];
+    }
+    if (!FROM_E) fftr<float, L, +1>(v, G.sm, g.twnx, G.t, G.sync);
+    if (!UNIFORM) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[e] = scale(v[e], wv[e]);
+    }
+    fftr<float, L, -1>(v, G.sm, g.twnx, G.t, G.sync);
+    // stage the band outputs as tile[slot][row] (odd stride: conflict free),
+    // then write U[fk][slot][r0 .. r0+groups) as contiguous row segments
+    if constexpr (CB) {
+      C32* tb = tile + bm.base * ld + G.gid;
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (bm.has(e)) tb[BandMap<L>::off(e) * ld] = v[e];
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int sl = kslot(G.idx(e), lo, hi, L);
+        if (sl >= 0) tile[sl * ld + G.gid] = v[e];
+      }
+    }
+    __syncthreads();
+    C32* o = U + blockIdx.z * u_ts + size_t(fk) * Bx * ny + r0;
+    for (int idx = threadIdx.x; idx < Bx * G.groups; idx += blockDim.x) {
+      const int sl = idx >> lgg, rr = idx & (G.groups - 1);
+      if (rr < nr) o[size_t(sl) * ny + rr] = tile[sl * ld + rr];
+    }
+    __syncthreads();  // tile free for the next slot
   }
 }
 
