@@ -81,10 +81,23 @@ def build(force: bool = False, verbose: bool = False, out: str = OUT, defines=()
     return out
 
 
-def build_variant(name: str, defines) -> str:
-    """variants/<name>/liblithogpu.so with extra -D flags (A/B timing)."""
+def build_variant(name: str, defines, fast_only: bool = True) -> str:
+    """variants/<name>/liblithogpu.so with extra -D flags (A/B timing).
+    fast_only: the -D flags only reach the fp32 fast-path kernels
+    (fast_rows.cu / fast_cols.cu); the other objects come from the main
+    build (built first)."""
+    import shutil
     d = os.path.join(ROOT, "variants", name)
-    return build(out=os.path.join(d, "liblithogpu.so"), defines=defines, objdir=os.path.join(d, "obj"))
+    objdir = os.path.join(d, "obj")
+    if fast_only:
+        build()
+        os.makedirs(objdir, exist_ok=True)
+        for src in CU_SOURCES + CPP_SOURCES:
+            if src in ("csrc/fast_rows.cu", "csrc/fast_cols.cu"):
+                continue
+            o = os.path.basename(src) + ".o"
+            shutil.copy2(os.path.join(OBJ, o), os.path.join(objdir, o))
+    return build(out=os.path.join(d, "liblithogpu.so"), defines=defines, objdir=objdir)
 
 
 if __name__ == "__main__":

@@ -19,8 +19,13 @@ void fl_socs_cols(const FGeo& g, cudaStream_t s, int tiles, const C32* Mhat, lon
     constexpr int L = decltype(c)::value;
     const int gr = fgroups<L>(4 * RPlan<L>::TPR);  // 4 columns per CTA: -0.7 % vs 8 at C2
     const size_t extra = size_t(L) * (gr | 1) * sizeof(C32);  // staging tile
-    flaunch_x<L>(fk_socs_cols<L>, dim3(cdivi(g.ax.B, gr), g.F * g.K, tiles), gr, extra, s, g, Mhat, mh_ts,
-                 H, T, t_ts);
+    auto go = [&](auto kern) {
+      flaunch_x<L>(kern, dim3(cdivi(g.ax.B, gr), g.F * g.K, tiles), gr, extra, s, g, Mhat, mh_ts, H, T, t_ts);
+    };
+    if (centered_band(L, RPlan<L>::E, g.ay.lo, g.ay.hi) && !sparse_off())
+      go(fk_socs_cols<L, true>);
+    else
+      go(fk_socs_cols<L, false>);
   });
 }
 
@@ -52,8 +57,13 @@ void fl_adj_cols(const FGeo& g, cudaStream_t s, int tiles, const C32* U, long lo
   with_len(g.ay.n, [&](auto c) {
     constexpr int L = decltype(c)::value;
     const int kg = kgroups<L>(g.K);
-    flaunch<L>(fk_adj_cols<L>, dim3(g.ax.B, g.F * g.K / kg, tiles), kg, s, g, U, u_ts, H, wk, dose, Accp,
-               a_ts);
+    auto go = [&](auto kern) {
+      flaunch<L>(kern, dim3(g.ax.B, g.F * g.K / kg, tiles), kg, s, g, U, u_ts, H, wk, dose, Accp, a_ts);
+    };
+    if (centered_band(L, RPlan<L>::E, g.ay.lo, g.ay.hi) && !sparse_off())
+      go(fk_adj_cols<L, true>);
+    else
+      go(fk_adj_cols<L, false>);
   });
 }
 
@@ -87,13 +97,21 @@ bool fl_band_col2(const FGeo& g, cudaStream_t s, int tiles, int nf, bool sub_in,
       if constexpr (pair && CP::ok && CP::TPR <= 256) {
         const int gr = CP::TPR >= 128 ? 1 : 128 / CP::TPR;
         const size_t smem = size_t(gr) * (CP::SM + 2 * CP::NB) * sizeof(C32);
-        static size_t set_bytes = 0;
-        if (smem > 48 * 1024 && smem > set_bytes) {
-          cudaFuncSetAttribute(fk_band_col2<LI, LO>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-          set_bytes = smem;
-        }
-        pdl_launch(fk_band_col2<LI, LO>, dim3(cdivi(g.ax.P + 1, gr), nf, tiles), dim3(gr * CP::TPR), smem, s,
-                   g, in, in_ts, inv, gxh, gyb, outR, outI, o_ts);
+        const bool cb = !g.ay.full && centered_band(LI, RPlan<LI>::E, -g.ay.P, g.ay.P) &&
+                        centered_band(LO, RPlan<LO>::E, -g.ay.P, g.ay.P) && !sparse_off();
+        auto go = [&](auto kern) {
+          static size_t set_bytes = 0;
+          if (smem > 48 * 1024 && smem > set_bytes) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            set_bytes = smem;
+          }
+          pdl_launch(kern, dim3(cdivi(g.ax.P + 1, gr), nf, tiles), dim3(gr * CP::TPR), smem, s, g, in, in_ts,
+                     inv, gxh, gyb, outR, outI, o_ts);
+        };
+        if (cb)
+          go(fk_band_col2<LI, LO, true>);
+        else
+          go(fk_band_col2<LI, LO, false>);
         done = true;
       }
     });

@@ -44,7 +44,15 @@ LG_RPLAN(512, 8, 8, 8, 8)
 LG_RPLAN(1024, 16, 16, 8, 8)
 // 2048 = 8*4*8*8 on 256 threads: in-graph A/B at C2 against 8*8*8*4 (-1.0 %),
 // 4*8*8*8, 8*8*4*8 and the E = 16 plans 16*16*8, 16*8*16, 8*16*16 (+3-6 %)
+#if !defined(LG_PLAN2048) || LG_PLAN2048 == 0
 LG_RPLAN(2048, 8, 8, 4, 8, 8)
+#elif LG_PLAN2048 == 1
+LG_RPLAN(2048, 8, 8, 8, 8, 4)
+#elif LG_PLAN2048 == 2
+LG_RPLAN(2048, 8, 8, 8, 4, 8)
+#elif LG_PLAN2048 == 3
+LG_RPLAN(2048, 8, 4, 8, 8, 8)
+#endif
 LG_RPLAN(4096, 16, 16, 16, 16)
 LG_RPLAN(8192, 16, 16, 16, 16, 2)
 LG_RPLAN(192, 12, 12, 4, 4)
@@ -162,6 +170,12 @@ template <>
 struct XchOf<512> {  // [8,8,8] plan: XOR swizzle measured 29.6 vs 26.1 TFLOP/s for padding
   using type = Xch2<1>;
 };
+#ifdef LG_XCH2048
+template <>
+struct XchOf<2048> {
+  using type = Xch2<LG_XCH2048>;
+};
+#endif
 
 // float2 cells of one row buffer (>= the padded natural layout used by to_smem)
 template <int L>

@@ -205,6 +205,42 @@ __device__ __forceinline__ void stage_rows_async(float* dst, const float* r0, co
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 __device__ __forceinline__ void stage_wait() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// The same staging through the TMA engine (cp.async.bulk, one elected
+// thread, completion on an mbarrier): the two 4L-byte rows bypass the LSU
+// pipe, which the exchange traffic of the row FFTs saturates.
+// bar: the group's mbarrier (8 B of shared memory).  Readers call
+// stage_wait_tma() after at least one group barrier (orders the init).
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+template <int L>
+__device__ __forceinline__ void stage_rows_tma(float* dst, const float* r0, const float* r1, int t,
+                                               unsigned long long* bar) {
+  if (t != 0) return;
+  const unsigned b = smem_u32(bar);
+  constexpr unsigned bytes = L * sizeof(float);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(2 * bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(r0), "r"(bytes), "r"(b) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst + L)), "l"(r1), "r"(bytes), "r"(b) : "memory");
+}
+__device__ __forceinline__ void stage_wait_tma(unsigned long long* bar) {
+  const unsigned b = smem_u32(bar);
+  unsigned done = 0;
+  while (!done)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done) : "r"(b) : "memory");
+}
+#ifndef LG_NO_TMA_STAGE
+#define LG_TMA_STAGE 1
+#else
+#define LG_TMA_STAGE 0
+#endif
 template <int L>
 __host__ __device__ constexpr size_t row_slab_bytes(int groups) {
   return size_t(groups) * 2 * L * sizeof(float);
@@ -421,12 +457,20 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_resist_rows(FGeo g, c
   // target rows staged into shared memory behind the transform
   const float* tg = target + blockIdx.z * tg_ts;
   float* tsl = row_slab<L>(G.groups, G.gid);
-  stage_rows_async<L>(tsl, tg + size_t(y0) * L, tg + size_t(has1 ? y1 : y0) * L, G.t);
+  __shared__ unsigned long long stage_bar[16];
+  if (LG_TMA_STAGE)
+    stage_rows_tma<L>(tsl, tg + size_t(y0) * L, tg + size_t(has1 ? y1 : y0) * L, G.t, &stage_bar[G.gid]);
+  else
+    stage_rows_async<L>(tsl, tg + size_t(y0) * L, tg + size_t(has1 ? y1 : y0) * L, G.t);
   C32 v[E];
   load_herm_pair<L, SPB>(v, G, rc + y0, has1 ? rc + y1 : nullptr, Px, Ny);  // column-major [px][y]
   fftr_sp<float, L, +1, SP_IN>(v, G.sm, g.twNx, G.t, G.sync);
-  stage_wait();
-  G.sync();
+  if (LG_TMA_STAGE) {
+    stage_wait_tma(&stage_bar[G.gid]);
+  } else {
+    stage_wait();
+    G.sync();
+  }
   // branch-free pointwise resist: an odd last row (no partner) is masked by h1
   const float w = cf[f], h1 = has1 ? 1.f : 0.f;
   const float k2 = 2.f * w * beta;
@@ -635,16 +679,24 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_grad_rows(FGeo g, con
   const C32* gc = Gc + blockIdx.z * g_ts;
   float* th = theta + blockIdx.z * th_ts;
   float* tsl = nullptr;  // theta rows staged into shared memory behind the transform
+  __shared__ unsigned long long stage_bar[16];
   if (ILT) {
     tsl = row_slab<L>(G.groups, G.gid);
-    stage_rows_async<L>(tsl, th + size_t(y0) * L, th + size_t(has1 ? y1 : y0) * L, G.t);
+    if (LG_TMA_STAGE)
+      stage_rows_tma<L>(tsl, th + size_t(y0) * L, th + size_t(has1 ? y1 : y0) * L, G.t, &stage_bar[G.gid]);
+    else
+      stage_rows_async<L>(tsl, th + size_t(y0) * L, th + size_t(has1 ? y1 : y0) * L, G.t);
   }
   C32 v[E];
   load_herm_pair<L, SPB>(v, G, gc + y0, has1 ? gc + y1 : nullptr, Pm, Ny);  // column-major [px][y]
   fftr_sp<float, L, +1, SP_IN>(v, G.sm, g.twNx, G.t, G.sync);
   if (ILT) {
-    stage_wait();
-    G.sync();
+    if (LG_TMA_STAGE) {
+      stage_wait_tma(&stage_bar[G.gid]);
+    } else {
+      stage_wait();
+      G.sync();
+    }
   }
   if (!ILT) {
     if (!act) return;
@@ -742,7 +794,7 @@ __global__ void __launch_bounds__(256) fk_mask_cols(FGeo g, const C32* __restric
 // shared memory so T rows are written as contiguous segments.
 // grid (ceil(Bx/groups), F*K, tiles)
 // ===========================================================================
-template <int L>
+template <int L, bool CB>
 __global__ void __launch_bounds__(512) fk_socs_cols(FGeo g, const C32* __restrict__ Mhat,
                                                     long long mh_ts, const C32* __restrict__ H,
                                                     C32* __restrict__ T, long long t_ts) {
@@ -759,10 +811,19 @@ __global__ void __launch_bounds__(512) fk_socs_cols(FGeo g, const C32* __restric
   const C32* mh = Mhat + blockIdx.z * mh_ts + size_t(cx_) * By;
   const C32* h = H + (size_t(fk) * Bx + cx_) * By;
   C32 v[E];
+  if constexpr (CB) {
+    const BandMap<L> bm(G.t, g.ay.lo, g.ay.hi);
+    const C32* mb = mh + bm.base;
+    const C32* hb = h + bm.base;
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int jy = kslot(G.idx(e), g.ay.lo, g.ay.hi, L);
-    v[e] = jy >= 0 ? mul(mh[jy], ldg_cx(h + jy)) : mk(0.f, 0.f);
+    for (int e = 0; e < E; ++e)
+      v[e] = bm.has(e) ? mul(mb[BandMap<L>::off(e)], ldg_cx(hb + BandMap<L>::off(e))) : mk(0.f, 0.f);
+  } else {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int jy = kslot(G.idx(e), g.ay.lo, g.ay.hi, L);
+      v[e] = jy >= 0 ? mul(mh[jy], ldg_cx(h + jy)) : mk(0.f, 0.f);
+    }
   }
   fftr<float, L, +1>(v, G.sm, g.twny, G.t, G.sync);
   extern __shared__ __align__(16) unsigned char fsm_raw[];
@@ -771,11 +832,12 @@ __global__ void __launch_bounds__(512) fk_socs_cols(FGeo g, const C32* __restric
 #pragma unroll
   for (int e = 0; e < E; ++e) tile[G.idx(e) * ld + G.gid] = v[e];
   __syncthreads();
-  C32* o = T + blockIdx.z * t_ts + size_t(fk) * L * Bx;
+  C32* o = T + blockIdx.z * t_ts + size_t(fk) * L * Bx + c0;
   const int nc = min(G.groups, Bx - c0);
+  const int lgg = __ffs(G.groups) - 1;  // groups is a power of two (fgroups)
   for (int idx = threadIdx.x; idx < L * G.groups; idx += blockDim.x) {
-    const int sy = idx / G.groups, cc = idx - sy * G.groups;
-    if (cc < nc) o[size_t(sy) * Bx + c0 + cc] = tile[sy * ld + cc];
+    const int sy = idx >> lgg, cc = idx & (G.groups - 1);
+    if (cc < nc) o[size_t(sy) * Bx + cc] = tile[sy * ld + cc];
   }
 }
 
@@ -867,7 +929,7 @@ __device__ __forceinline__ GSync sub_gsync(int nthreads, int id) {
   return s;
 }
 
-template <int LIN, int LOUT>
+template <int LIN, int LOUT, bool CB>
 __global__ void __launch_bounds__(256) fk_band_col2(FGeo g, const C32* __restrict__ in,
                                                     long long in_ts, float inv,
                                                     const float* __restrict__ gxh,
@@ -897,13 +959,25 @@ __global__ void __launch_bounds__(256) fk_band_col2(FGeo g, const C32* __restric
     for (int e = 0; e < EI; ++e) v[e] = src[t + e * CP::TIN];
     fftr<float, LIN, -1>(v, sm, LIN == g.ay.N ? g.twNy : g.twny, t, s1);
     const float gx = gxh ? gxh[px] : 1.f;
+    if constexpr (CB) {  // intensity band |p| <= P = centered band [-P, P]
+      const BandMap<LIN> bm(t, -g.ay.P, g.ay.P);
 #pragma unroll
-    for (int e = 0; e < EI; ++e) {
-      const int j = islot(g.ay, t + e * CP::TIN, LIN);
-      if (j < 0) continue;
-      const C32 c = scale(v[e], inv);
-      if (outI) bbI[j] = c;
-      bbR[j] = gyb ? scale(c, gx * gyb[j]) : c;
+      for (int e = 0; e < EI; ++e) {
+        if (!bm.has(e)) continue;
+        const int j = bm.base + BandMap<LIN>::off(e);
+        const C32 c = scale(v[e], inv);
+        if (outI) bbI[j] = c;
+        bbR[j] = gyb ? scale(c, gx * gyb[j]) : c;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < EI; ++e) {
+        const int j = islot(g.ay, t + e * CP::TIN, LIN);
+        if (j < 0) continue;
+        const C32 c = scale(v[e], inv);
+        if (outI) bbI[j] = c;
+        bbR[j] = gyb ? scale(c, gx * gyb[j]) : c;
+      }
     }
   }
   gsync();
@@ -915,10 +989,17 @@ __global__ void __launch_bounds__(256) fk_band_col2(FGeo g, const C32* __restric
     if (!out) continue;
     const C32* bb = pass == 0 ? bbR : bbI;
     C32 v[EO];
+    if constexpr (CB) {
+      const BandMap<LOUT> bm(t, -g.ay.P, g.ay.P);
+      const C32* b0 = bb + bm.base;
 #pragma unroll
-    for (int e = 0; e < EO; ++e) {
-      const int j = islot(g.ay, t + e * CP::TOUT, LOUT);
-      v[e] = j >= 0 ? bb[j] : mk(0.f, 0.f);
+      for (int e = 0; e < EO; ++e) v[e] = bm.has(e) ? b0[BandMap<LOUT>::off(e)] : mk(0.f, 0.f);
+    } else {
+#pragma unroll
+      for (int e = 0; e < EO; ++e) {
+        const int j = islot(g.ay, t + e * CP::TOUT, LOUT);
+        v[e] = j >= 0 ? bb[j] : mk(0.f, 0.f);
+      }
     }
     fftr<float, LOUT, +1>(v, sm, LOUT == g.ay.N ? g.twNy : g.twny, t, s2);
     if (act) {
@@ -936,7 +1017,7 @@ __global__ void __launch_bounds__(256) fk_band_col2(FGeo g, const C32* __restric
 //   Accp[fk/KG][cx][qy]   (fk_grad_cols sums the F*K/KG partials, fixed order)
 // grid (Bx, F*K/KG, tiles)
 // ===========================================================================
-template <int L>
+template <int L, bool CB>
 __global__ void __launch_bounds__(256) fk_adj_cols(FGeo g, const C32* __restrict__ U,
                                                    long long u_ts, const C32* __restrict__ H,
                                                    const float* __restrict__ wk, float dose,
@@ -955,10 +1036,19 @@ __global__ void __launch_bounds__(256) fk_adj_cols(FGeo g, const C32* __restrict
   const float w = on ? wk[fk] * dose * sc : 0.f;
   const C32* h = H + (size_t(fk) * Bx + cx) * By;  // column-major [fk][cx][jy]
   G.sync();
+  if constexpr (CB) {
+    const BandMap<L> bm(G.t, g.ay.lo, g.ay.hi);
+    const C32* hb = h + bm.base;
+    C32* sb = G.sm + bm.base;
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int jy = kslot(G.idx(e), g.ay.lo, g.ay.hi, L);
-    if (jy >= 0) G.sm[jy] = scale(mulc(v[e], ldg_cx(h + jy)), w);
+    for (int e = 0; e < E; ++e)
+      if (bm.has(e)) sb[BandMap<L>::off(e)] = scale(mulc(v[e], ldg_cx(hb + BandMap<L>::off(e))), w);
+  } else {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int jy = kslot(G.idx(e), g.ay.lo, g.ay.hi, L);
+      if (jy >= 0) G.sm[jy] = scale(mulc(v[e], ldg_cx(h + jy)), w);
+    }
   }
   __syncthreads();
   extern __shared__ __align__(16) unsigned char fsm_raw[];
