@@ -429,6 +429,28 @@ lg::AxisGeom make_axis(int N, int lo, int hi, bool mixed = false) {
       }
     }
   }
+  // generic path: n need not divide N either (samples at s N / n); every
+  // length is O(n log n) (fft.cuh), so take the smallest power of two (radix-16
+  // register Stockham) or else the smallest 7-smooth length (mixed radix)
+  // >= max(2P+1, min(N, 32)) that fits in N.  LITHOGPU_DIVISOR_SUBGRID=1
+  // keeps the divisor rule below (A/B).
+  if (!std::getenv("LITHOGPU_DIVISOR_SUBGRID")) {
+    const int m = std::max(2 * P0 + 1, std::min(N, 32));
+    int n = 16;
+    while (n < m) n <<= 1;
+    if (n > N) {
+      n = m;
+      while (lg::fft_kind(n) == lg::kFftBluestein) ++n;
+    }
+    if (n < N) {
+      a.d = N % n == 0 ? N / n : 0;
+      a.n = n;
+      a.full = 0;
+      a.P = P0;
+      a.nb2 = 2 * P0 + 1;
+      return a;
+    }
+  }
   int best = 0;
   for (int d = N; d >= 1; --d) {
     if (N % d) continue;
