@@ -712,6 +712,8 @@ struct Plan : PlanBase {
       fast = ok(Nx) && ok(Ny) && ok(ax.n) && ok(ay.n) && !std::getenv("LITHOGPU_GENERIC");
       if (fast) {
         fg.ax = ax;
+        fg.tld = (Bx + 1) & ~1;
+        s_T = (long long)F * K * ay.n * fg.tld;
         fg.ay = ay;
         fg.F = F;
         fg.K = K;
@@ -1022,7 +1024,12 @@ struct Plan : PlanBase {
     ctx->prof_begin(name);
     fn();
     ctx->prof_end();
-    ctx->check_launch();
+    try {
+      ctx->check_launch();
+    } catch (const std::exception& e) {
+      fg.trace = nullptr;
+      throw std::runtime_error(std::string(name) + ": " + e.what());
+    }
     fg.trace = nullptr;
   }
 

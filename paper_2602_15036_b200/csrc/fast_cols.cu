@@ -100,11 +100,7 @@ bool fl_band_col2(const FGeo& g, cudaStream_t s, int tiles, int nf, bool sub_in,
         const bool cb = !g.ay.full && centered_band(LI, RPlan<LI>::E, -g.ay.P, g.ay.P) &&
                         centered_band(LO, RPlan<LO>::E, -g.ay.P, g.ay.P) && !sparse_off();
         auto go = [&](auto kern) {
-          static size_t set_bytes = 0;
-          if (smem > 48 * 1024 && smem > set_bytes) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-            set_bytes = smem;
-          }
+          if (smem > 32 * 1024) set_max_smem(kern, smem);  // static shared memory counts toward the 48 KB default too
           pdl_launch(kern, dim3(cdivi(g.ax.P + 1, gr), nf, tiles), dim3(gr * CP::TPR), smem, s, g, in, in_ts,
                      inv, gxh, gyb, outR, outI, o_ts);
         };

@@ -7,6 +7,7 @@
 #include <stdexcept>
 #include <string>
 #include <type_traits>
+#include <unordered_map>
 #include <unordered_set>
 
 #ifndef LG_DEFAULT_CARVEOUT
@@ -64,15 +65,23 @@ inline int spread_groups(long long units, int cap = 8) {
   return g;
 }
 
+// dynamic shared memory above 48 KB, raised once per kernel (keyed on the
+// kernel itself: kernels of one signature share a launcher instantiation)
+template <typename K>
+inline void set_max_smem(K kern, size_t smem) {
+  thread_local std::unordered_map<const void*, size_t> set;
+  size_t& cur = set[reinterpret_cast<const void*>(kern)];
+  if (smem > cur) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cur = smem;
+  }
+}
+
 // launch with `extra` bytes of shared memory after the row-group buffers
 template <int L, typename K, typename... A>
 inline void flaunch_x(K kern, dim3 grid, int groups, size_t extra, cudaStream_t s, A... args) {
   const size_t smem = size_t(groups) * rsm_len<L>() * sizeof(C32) + extra;
-  static size_t set_bytes = 0;  // per instantiation
-  if (smem > 48 * 1024 && smem > set_bytes) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    set_bytes = smem;
-  }
+  if (smem > 32 * 1024) set_max_smem(kern, smem);  // static shared memory counts toward the 48 KB default too
   pdl_launch(kern, grid, dim3(groups * RPlan<L>::TPR), smem, s, args...);
 }
 

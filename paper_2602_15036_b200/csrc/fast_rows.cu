@@ -55,7 +55,10 @@ void fl_socs_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* T, long l
     int gr = fgroups<L>(256);
     if (gr > g.K) gr = g.K;
     auto go = [&](auto kern) {
-      flaunch<L>(kern, dim3(g.ay.n, g.F, tiles), gr, s, g, T, t_ts, wk, wk2, dose, Ir, ir_ts, Eo, e_ts);
+      // + the TMA double buffer of T rows (2 rows per group)
+      const size_t pad = groups_bytes<L>(gr) - size_t(gr) * rsm_len<L>() * sizeof(C32);  // 16-byte alignment
+      flaunch_x<L>(kern, dim3(g.ay.n, g.F, tiles), gr, pad + size_t(gr) * 2 * g.tld * sizeof(C32), s, g, T, t_ts, wk,
+                   wk2, dose, Ir, ir_ts, Eo, e_ts);
     };
     if (centered_band(L, RPlan<L>::E, g.ax.lo, g.ax.hi) && !sparse_off())
       go(fk_socs_rows<L, true>);

@@ -364,25 +364,63 @@ __global__ void __launch_bounds__(256, LG_SOCSROWS_MINB) fk_socs_rows(FGeo g, co
   FGroup<L> G;
   TraceScope trace_(g);
   constexpr int E = RPlan<L>::E;
-  const int Bx = g.ax.B, ny = g.ay.n, lo = g.ax.lo, hi = g.ax.hi, K = g.K;
+  const int ny = g.ay.n, lo = g.ax.lo, hi = g.ax.hi, K = g.K, tld = g.tld;
   const int sy = blockIdx.x, f = blockIdx.y;
   float acc[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) acc[e] = 0.f;
   const BandMap<L> bm(G.t, lo, hi);
   // per-kernel row pointers advance by one kernel plane per slot
-  const long long tstep = (long long)ny * Bx, estep = (long long)ny * L;
-  const C32* src = T + blockIdx.z * t_ts + size_t(f * K + G.gid) * tstep + size_t(sy) * Bx;
+  const long long tstep = (long long)ny * tld, estep = (long long)ny * L;
+  const C32* src = T + blockIdx.z * t_ts + size_t(f * K + G.gid) * tstep + size_t(sy) * tld;
   C32* eo = Eo ? Eo + blockIdx.z * e_ts + (size_t(f * K + G.gid) * ny + sy) * L + G.t : nullptr;
-  for (int k = G.gid; k < K; k += G.groups, src += G.groups * tstep, eo += eo ? G.groups * estep : 0) {
+  // CB: the group's T rows stream through a TMA double buffer in shared memory
+  // (one bulk copy per kernel row, issued one row ahead; fk_socs_rows was
+  // latency-bound on these gathers)
+  extern __shared__ __align__(16) unsigned char fsm_raw[];
+  // 16-byte aligned for the bulk copies (groups_bytes rounds the exchange buffers up)
+  C32* rb = reinterpret_cast<C32*>(fsm_raw + groups_bytes<L>(G.groups)) + size_t(G.gid) * 2 * tld;
+  __shared__ unsigned long long tbar[16][2];
+  const unsigned rbytes = unsigned(tld) * sizeof(C32);
+  auto prefetch = [&](const C32* row, int b) {
+    if (G.t == 0) {
+      const unsigned bar = smem_u32(&tbar[G.gid][b]);
+      // the group's generic-proxy reads of this buffer (two slots ago) are
+      // ordered before the async-proxy overwrite
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(rbytes) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(smem_u32(rb + b * tld)), "l"(row), "r"(rbytes), "r"(bar) : "memory");
+    }
+  };
+  if constexpr (CB) {
+    if (G.t == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tbar[G.gid][0])) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tbar[G.gid][1])) : "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    G.sync();  // barrier inits before any wait
+    if (G.gid < K) prefetch(src, 0);
+  }
+  int it = 0;
+  for (int k = G.gid; k < K; k += G.groups, src += G.groups * tstep, eo += eo ? G.groups * estep : 0, ++it) {
     const int fk = f * K + k;
-    if (g.slot_on && !g.slot_on[fk]) continue;  // empty slot (mixed kernel pairs)
     C32 v[E];
     if constexpr (CB) {
-      const C32* sb = src + bm.base;
+      const int b = it & 1;
+      if (k + G.groups < K) prefetch(src + G.groups * tstep, b ^ 1);
+      unsigned done = 0;
+      const unsigned bar = smem_u32(&tbar[G.gid][b]), par = unsigned(it >> 1) & 1u;
+      while (!done)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done) : "r"(bar), "r"(par) : "memory");
+      if (g.slot_on && !g.slot_on[fk]) continue;  // empty slot (mixed kernel pairs)
+      const C32* sb = rb + b * tld + bm.base;
 #pragma unroll
       for (int e = 0; e < E; ++e) v[e] = bm.has(e) ? sb[BandMap<L>::off(e)] : mk(0.f, 0.f);
     } else {
+      if (g.slot_on && !g.slot_on[fk]) continue;  // empty slot (mixed kernel pairs)
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const int sl = kslot(G.idx(e), lo, hi, L);
@@ -606,11 +644,11 @@ __global__ void __launch_bounds__(256, LG_ADJROWS_MINB) fk_adj_rows(FGeo g, cons
 #pragma unroll
       for (int e = 0; e < E; ++e) v[e] = src[e * TPR];
     } else if (CB) {
-      const C32* sb = T + blockIdx.z * t_ts + size_t(fk) * ny * Bx + size_t(sy) * Bx + bm.base;
+      const C32* sb = T + blockIdx.z * t_ts + size_t(fk) * ny * g.tld + size_t(sy) * g.tld + bm.base;
 #pragma unroll
       for (int e = 0; e < E; ++e) v[e] = bm.has(e) ? sb[BandMap<L>::off(e)] : mk(0.f, 0.f);
     } else {
-      const C32* src = T + blockIdx.z * t_ts + size_t(fk) * ny * Bx + size_t(sy) * Bx;
+      const C32* src = T + blockIdx.z * t_ts + size_t(fk) * ny * g.tld + size_t(sy) * g.tld;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const int sl = kslot(G.idx(e), lo, hi, L);
@@ -644,10 +682,16 @@ __global__ void __launch_bounds__(256, LG_ADJROWS_MINB) fk_adj_rows(FGeo g, cons
       }
     }
     __syncthreads();
-    C32* o = U + blockIdx.z * u_ts + size_t(fk) * Bx * ny + r0;
-    for (int idx = threadIdx.x; idx < Bx * G.groups; idx += blockDim.x) {
-      const int sl = idx >> lgg, rr = idx & (G.groups - 1);
-      if (rr < nr) o[size_t(sl) * ny + rr] = tile[sl * ld + rr];
+    {  // fixed lane roles: thread -> row rr, slots sl0, sl0 + step, ...
+      const int rr = threadIdx.x & (G.groups - 1), step = blockDim.x >> lgg;
+      if (rr < nr) {
+        int sl = threadIdx.x >> lgg;
+        C32* op = U + blockIdx.z * u_ts + size_t(fk) * Bx * ny + r0 + size_t(sl) * ny + rr;
+        const C32* tp = tile + sl * ld + rr;
+        const size_t ostep = size_t(step) * ny;
+        const int tstep = step * ld;
+        for (; sl < Bx; sl += step, op += ostep, tp += tstep) *op = *tp;
+      }
     }
     __syncthreads();  // tile free for the next slot
   }
@@ -832,13 +876,18 @@ __global__ void __launch_bounds__(512) fk_socs_cols(FGeo g, const C32* __restric
 #pragma unroll
   for (int e = 0; e < E; ++e) tile[G.idx(e) * ld + G.gid] = v[e];
   __syncthreads();
-  C32* o = T + blockIdx.z * t_ts + size_t(fk) * L * Bx + c0;
   const int nc = min(G.groups, Bx - c0);
   const int lgg = __ffs(G.groups) - 1;  // groups is a power of two (fgroups)
-  for (int idx = threadIdx.x; idx < L * G.groups; idx += blockDim.x) {
-    const int sy = idx >> lgg, cc = idx & (G.groups - 1);
-    if (cc < nc) o[size_t(sy) * Bx + cc] = tile[sy * ld + cc];
-  }
+  // fixed lane roles: thread -> column cc, rows sy0, sy0 + step, ...
+  const int cc = threadIdx.x & (G.groups - 1), step = blockDim.x >> lgg;
+  if (cc >= nc) return;
+  int sy = threadIdx.x >> lgg;
+  C32* op = T + blockIdx.z * t_ts + size_t(fk) * L * g.tld + c0 + size_t(sy) * g.tld + cc;
+  const C32* tp = tile + sy * ld + cc;
+  const size_t ostep = size_t(step) * g.tld;
+  const int tstep = step * ld;
+#pragma unroll 4
+  for (; sy < L; sy += step, op += ostep, tp += tstep) *op = *tp;
 }
 
 // ===========================================================================

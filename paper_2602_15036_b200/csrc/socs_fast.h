@@ -23,6 +23,10 @@ struct FGeo {
   // launch `trace_slot`, kTraceCtas CTAs per slot; null = off
   unsigned long long* trace = nullptr;
   int trace_slot = 0;
+  // row stride (complex elements) of the per-kernel column spectra T[fk][sy][.]:
+  // the band width Bx rounded up to even, so every row is a 16-byte multiple
+  // (TMA bulk copies in fk_socs_rows)
+  int tld = 0;
   // mixed kernel pairs (Plan::make_pairs): 0 marks an empty kernel slot that
   // every kernel skips; null = all slots active
   const int* slot_on = nullptr;

@@ -24,7 +24,7 @@ cfg, iters, reps, tiles = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), int(s
 torch.cuda.set_device(0)
 st = torch.cuda.Stream(); torch.cuda.set_stream(st)
 ctx = L.Context(0); ctx.set_stream(st.cuda_stream)
-grid, polys, ks, _, _ = bench.make_problem(cfg, 0, "host")
+grid, polys, ks, _, _ = bench.make_problem(cfg, 0, "gpu", ctx)
 dk = L.DeviceKernels(ks, "f32", ctx)
 xy, starts = LY.polygon_arrays(polys)
 N = grid.nx
