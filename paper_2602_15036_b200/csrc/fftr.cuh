@@ -17,11 +17,20 @@
 // forward, +1 backward, unnormalized.
 #pragma once
 
+#include <type_traits>
 #include <utility>
 
 #include "fft.cuh"
 
 namespace lg {
+
+// Twiddles per butterfly: 1 = load W^k and form W^(rk) by products (the row
+// kernels are LSU-bound: C5 -5.3 % per iteration); 2 (default) = W^k from the
+// SFU as well (__sincosf, |angle| < 2 pi / R, abs err ~4e-7; another -2.5 %);
+// 0 = load every power (round 1).
+#ifndef LG_TW_REC
+#define LG_TW_REC 2
+#endif
 
 template <int L>
 struct RPlan;
@@ -44,7 +53,11 @@ LG_RPLAN(512, 8, 8, 8, 8)
 LG_RPLAN(1024, 16, 16, 8, 8)
 // 2048 = 8*4*8*8 on 256 threads: in-graph A/B at C2 against 8*8*8*4 (-1.0 %),
 // 4*8*8*8, 8*8*4*8 and the E = 16 plans 16*16*8, 16*8*16, 8*16*16 (+3-6 %)
-#if !defined(LG_PLAN2048) || LG_PLAN2048 == 0
+// 2048: 16*16*8 on 128 threads (two exchanges) since round 2: the row kernels
+// are LSU-bound, C5 -6.5 % per iteration against 8*4*8*8 (C2 +3.7 %, tail)
+#if !defined(LG_PLAN2048) || LG_PLAN2048 == 4
+LG_RPLAN(2048, 16, 16, 16, 8)
+#elif LG_PLAN2048 == 0
 LG_RPLAN(2048, 8, 8, 4, 8, 8)
 #elif LG_PLAN2048 == 1
 LG_RPLAN(2048, 8, 8, 8, 8, 4)
@@ -52,13 +65,23 @@ LG_RPLAN(2048, 8, 8, 8, 8, 4)
 LG_RPLAN(2048, 8, 8, 8, 4, 8)
 #elif LG_PLAN2048 == 3
 LG_RPLAN(2048, 8, 4, 8, 8, 8)
+#elif LG_PLAN2048 == 5
+LG_RPLAN(2048, 16, 8, 16, 16)
 #endif
 LG_RPLAN(4096, 16, 16, 16, 16)
 LG_RPLAN(8192, 16, 16, 16, 16, 2)
 LG_RPLAN(192, 12, 12, 4, 4)
 // 384 = 4*6*4*4: in-graph A/B at C2 against 12*4*4*2 (-1.5 %), 4*4*4*6,
 // 4*4*6*4, 6*4*4*4, 4*4*2*12 and the E = 24 plans 8*6*8 / 6*8*8 (+16-26 %)
+#if !defined(LG_PLAN384) || LG_PLAN384 == 0
 LG_RPLAN(384, 12, 4, 6, 4, 4)
+#elif LG_PLAN384 == 1
+LG_RPLAN(384, 24, 8, 6, 8)
+#elif LG_PLAN384 == 2
+LG_RPLAN(384, 24, 6, 8, 8)
+#elif LG_PLAN384 == 3
+LG_RPLAN(384, 12, 12, 4, 4, 2)
+#endif
 // 768 = 4*4*4*12: C4 A/B against 12*4*4*4 (+5 % tile-iter/s), 4*12*4*4 (+3 %),
 // 8*6*4*4 (E = 24, -1 %)
 LG_RPLAN(768, 12, 4, 4, 4, 12)
@@ -288,8 +311,26 @@ __device__ __forceinline__ void fftr_stage(cx<T> (&v)[RPlan<L>::E], cx<T>* sm,
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       const int k = (t + b * TPR) % Ns;
+#if LG_TW_REC
+      // one table load per butterfly, the other powers W^(r k) by products
+      // (LSU wavefronts traded for FMA-pipe work)
+#if LG_TW_REC == 2
+      if constexpr (std::is_same<T, float>::value) {
+        float sn, cs;
+        __sincosf(float(-2.0 * 3.14159265358979323846 / (Ns * R)) * float(k), &sn, &cs);
+        w[b][1] = mk(cs, sn);
+      } else {
+        w[b][1] = ldg_cx(tw + G::tw_off + k);
+      }
+#else
+      w[b][1] = ldg_cx(tw + G::tw_off + k);
+#endif
+#pragma unroll
+      for (int r = 2; r < R; ++r) w[b][r] = (r % 2 == 0) ? mul(w[b][r / 2], w[b][r / 2]) : mul(w[b][r - 1], w[b][1]);
+#else
 #pragma unroll
       for (int r = 1; r < R; ++r) w[b][r] = ldg_cx(tw + G::tw_off + (r - 1) * Ns + k);
+#endif
     }
   }
   constexpr int SW = X::sw;
