@@ -7,6 +7,20 @@
 
 namespace lg {
 
+// threads per CTA of the full-resolution row kernels (real_rows_fwd,
+// resist_rows, grad_rows) for `units` row pairs in the launch: 256 for batched
+// launches (C5 -3.6 % against 128), 128 for launches of fewer than 2048 pairs
+// 256-thread CTAs (C2, 1024 pairs: 1.8 % faster; C3, 3072: 2 % slower);
+// LITHOGPU_ROW_THREADS=<n> (A/B)
+static int fullrow_threads(long long units) {
+  static const int env = [] {
+    const char* e = std::getenv("LITHOGPU_ROW_THREADS");
+    return e ? std::max(32, std::atoi(e)) : 0;
+  }();
+  if (env) return env;
+  return units < 2048 ? 128 : 256;
+}
+
 int fast_tw_len(int len) {
   int n = 0;
   with_len(len, [&](auto c) { n = TwLen<decltype(c)::value>::value; });
@@ -35,7 +49,7 @@ void fl_real_rows_fwd(const FGeo& g, cudaStream_t s, int tiles, int mode, const 
                       long long src_ts, float steep, int Pout, C32* out, long long out_ts) {
   with_len(g.ax.N, [&](auto c) {
     constexpr int L = decltype(c)::value;
-    const int gr = fgroups<L>(256);
+    const int gr = fgroups<L>(fullrow_threads((long long)tiles * ((g.ay.N + 1) / 2)));
     const dim3 grid(cdivi((g.ay.N + 1) / 2, gr), 1, tiles);
     const size_t extra = size_t(Pout + 1) * 2 * gr * sizeof(C32) + 16;  // transposed-store tile
     auto go = [&](auto kern) { flaunch_x<L>(kern, grid, gr, extra, s, g, src, src_ts, steep, Pout, out, out_ts); };
@@ -72,7 +86,7 @@ void fl_resist_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* Rc, lon
                     C32* Dr, long long d_ts, double* costp, long long cp_ts) {
   with_len(g.ax.N, [&](auto c) {
     constexpr int L = decltype(c)::value;
-    const int gr = fgroups<L>(256);
+    const int gr = fgroups<L>(fullrow_threads((long long)tiles * g.F * ((g.ay.N + 1) / 2)));
     auto go = [&](auto kern) {
       flaunch_x<L>(kern, dim3(cdivi((g.ay.N + 1) / 2, gr), g.F, tiles), gr,
                    row_slab_bytes<L>(gr) + size_t(g.ax.P + 1) * 2 * gr * sizeof(C32) + 16, s, g, Rc, c_ts, target,
@@ -141,7 +155,7 @@ void fl_grad_rows(const FGeo& g, cudaStream_t s, int tiles, bool ilt, const C32*
                   float step, C32* Mr, long long mr_ts, double* gmaxp, long long gm_ts) {
   with_len(g.ax.N, [&](auto c) {
     constexpr int L = decltype(c)::value;
-    const int gr = fgroups<L>(256);
+    const int gr = fgroups<L>(fullrow_threads((long long)tiles * ((g.ay.N + 1) / 2)));
     const dim3 grid(cdivi((g.ay.N + 1) / 2, gr), 1, tiles);
     const size_t extra = row_slab_bytes<L>(gr) + size_t(g.ax.Pm + 1) * 2 * gr * sizeof(C32) + 16;
     const bool sp = g.ax.Pm < RPlan<L>::TPR && !sparse_off();
