@@ -81,6 +81,10 @@ LG_RPLAN(384, 24, 8, 6, 8)
 LG_RPLAN(384, 24, 6, 8, 8)
 #elif LG_PLAN384 == 3
 LG_RPLAN(384, 12, 12, 4, 4, 2)
+#elif LG_PLAN384 == 4
+LG_RPLAN(384, 12, 4, 4, 6, 4)
+#elif LG_PLAN384 == 5
+LG_RPLAN(384, 12, 4, 4, 4, 6)
 #endif
 // 768 = 4*4*4*12: C4 A/B against 12*4*4*4 (+5 % tile-iter/s), 4*12*4*4 (+3 %),
 // 8*6*4*4 (E = 24, -1 %)
@@ -116,7 +120,7 @@ struct TwLen {
 //     3 = i ^ ((i>>3)&31), 4 = i + (i>>5) padding.  (XOR variants only for
 //     power-of-two lengths.)
 template <int SW>
-__host__ __device__ __forceinline__ int swz(int i) {
+__host__ __device__ __forceinline__ constexpr int swz(int i) {
   if constexpr (SW == 0) return i + (i >> 4);
   else if constexpr (SW == 1) return i ^ ((i >> 3) & 15);
   else if constexpr (SW == 2) return i ^ ((i >> 4) & 31);
@@ -138,6 +142,27 @@ __host__ __device__ constexpr bool lin_ok(int C) {
 template <int SW>
 __host__ __device__ constexpr int lin_delta(int C) {
   return SW == 0 ? C + C / 16 : (SW == 4 ? C + C / 32 : C);
+}
+
+// Exact compile-time linearity test of one exchange access pattern: thread t
+// touches a(t) + c for the offsets c = b*cb + r*cr (b < NB, r < R), with
+// a(t) = (t - t%Ns)*R + t%Ns for a Stockham store (TPR % Ns == 0, so k = t % Ns
+// for every butterfly) or a(t) = t for a load.  Linear when
+// swz(a(t) + c) == swz(a(t)) + swz(c) for every t and c: the addresses are then
+// one swizzle per thread plus compile-time offsets (no per-element index math).
+template <int SW>
+__host__ __device__ constexpr bool lin_all(int TPR, int Ns, int R, int NB, int cb, int cr, bool store) {
+  if (SW < 0) return false;
+  if (store && TPR % Ns != 0) return false;
+  for (int t = 0; t < TPR; ++t) {
+    const int a = store ? (t - t % Ns) * R + t % Ns : t;
+    for (int b = 0; b < NB; ++b)
+      for (int r = 0; r < R; ++r) {
+        const int c = b * cb + r * cr;
+        if (swz<(SW < 0 ? 0 : SW)>(a + c) != swz<(SW < 0 ? 0 : SW)>(a) + swz<(SW < 0 ? 0 : SW)>(c)) return false;
+      }
+  }
+  return true;
 }
 
 template <int SW>
@@ -339,7 +364,7 @@ __device__ __forceinline__ void fftr_stage(cx<T> (&v)[RPlan<L>::E], cx<T>* sm,
     for (int b = 0; b < NB; ++b)
 #pragma unroll
       for (int r = 0; r < R; ++r) x[b][r] = v[b + r * NB];
-  } else if constexpr (SW >= 0 && lin_ok<(SW < 0 ? 0 : SW)>(TPR) && lin_ok<(SW < 0 ? 0 : SW)>(L / R)) {
+  } else if constexpr (SW >= 0 && lin_all<SW>(TPR, 1, R, NB, TPR, L / R, false)) {
     // one swizzle per thread, compile-time offsets
     constexpr int SWc = SW < 0 ? 0 : SW;
     const int p0 = swz<SWc>(t);
@@ -347,7 +372,7 @@ __device__ __forceinline__ void fftr_stage(cx<T> (&v)[RPlan<L>::E], cx<T>* sm,
     for (int b = 0; b < NB; ++b)
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        x[b][r] = X::template ld_raw<T>(sm, p0 + b * lin_delta<SWc>(TPR) + r * lin_delta<SWc>(L / R));
+        x[b][r] = X::template ld_raw<T>(sm, p0 + swz<SWc>(b * TPR + r * (L / R)));
   } else {
 #pragma unroll
     for (int b = 0; b < NB; ++b)
@@ -385,7 +410,7 @@ __device__ __forceinline__ void fftr_stage(cx<T> (&v)[RPlan<L>::E], cx<T>* sm,
   } else {
     sync();  // every thread finished reading sm (previous stage / previous use)
     constexpr int SWc = SW < 0 ? 0 : SW;
-    if constexpr (SW >= 0 && TPR % Ns == 0 && lin_ok<SWc>(Ns) && lin_ok<SWc>(TPR * R)) {
+    if constexpr (SW >= 0 && lin_all<SW>(TPR, Ns, R, NB, TPR * R, Ns, true)) {
       // k = j mod Ns is the same for every butterfly of the thread
       const int k = t % Ns;
       const int p0 = swz<SWc>((t - k) * R + k);
@@ -393,7 +418,7 @@ __device__ __forceinline__ void fftr_stage(cx<T> (&v)[RPlan<L>::E], cx<T>* sm,
       for (int b = 0; b < NB; ++b)
 #pragma unroll
         for (int r = 0; r < R; ++r)
-          X::template st_raw<T>(sm, p0 + b * lin_delta<SWc>(TPR * R) + r * lin_delta<SWc>(Ns), x[b][r]);
+          X::template st_raw<T>(sm, p0 + swz<SWc>(b * TPR * R + r * Ns), x[b][r]);
     } else {
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
