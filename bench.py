@@ -516,7 +516,7 @@ def _roofline(ctx, info, N, F, K, tiles, prof, iters, cfg):
     shares = {k: round(v[1] / tot, 4) for k, v in prof.items()}
     pk = _peaks()
     hbm_peak = pk.get("hbm_gbs") or pk.get("hbm_copy_gbs")
-    traffic, tsrc = _ncu_traffic(top, cfg)
+    traffic, tsrc = _ncu_traffic(top, cfg, tiles)
     whole_flops = sum(model[k][0] for k in model) * tiles
     return {"bound": "fp32", "kernel": top, "achieved": achieved, "peak": peak_fp32, "unit": "TFLOP/s",
             "frac": achieved / peak_fp32 if peak_fp32 else None, "traffic": traffic, "traffic_source": tsrc,
@@ -780,7 +780,7 @@ def _contours_c1(ctx, stream, dk, m32, grid, n_gauges=4096, radius=20.0):
     return out
 
 
-def _ncu_traffic(kernel, cfg="c5"):
+def _ncu_traffic(kernel, cfg="c5", tiles=None):
     """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` (per launch) from
     the newest committed `ncu --set full` capture summary of this config
     (profiles/r<round>_<cfg>_*_ncu.json, tools/ncu_summarize.py; newest =
@@ -802,8 +802,19 @@ def _ncu_traffic(kernel, cfg="c5"):
             continue
         c = caps.get("fk_" + kernel) or caps.get(kernel)
         if c and c.get("dram_bytes") is not None:
-            best = (c["dram_bytes"], f"{os.path.basename(p)} ({c.get('kernel')}, grid {c.get('grid')})")
-    return best if best else (None, None)
+            best = (c["dram_bytes"], f"{os.path.basename(p)} ({c.get('kernel')}, grid {c.get('grid')})",
+                    c.get("grid"))
+    if not best:
+        return None, None
+    b, src, grid = best
+    if tiles and grid:  # per launch of `tiles` tiles: scale by the capture's blockIdx.z tile count
+        try:
+            z = int(str(grid).strip("()").split(",")[2])
+            if z > 0 and z != tiles:
+                return b * tiles / z, src + f", scaled x{tiles}/{z} tiles"
+        except Exception:
+            pass
+    return b, src
 
 
 def _peaks():
