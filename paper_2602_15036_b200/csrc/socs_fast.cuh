@@ -447,8 +447,10 @@ __global__ void __launch_bounds__(256, LG_SOCSROWS_MINB) fk_socs_rows(FGeo g, co
 #pragma unroll
   for (int e = 0; e < E; ++e) red[G.idx(e)] = acc[e];
   __syncthreads();
-  if (G.gid != 0) return;
-  extern __shared__ __align__(16) unsigned char fsm_raw[];
+  // the LAST group transforms the summed row: with the kernel slots dealt out
+  // round-robin from group 0 it has the fewest of them (mixed pairs: half the
+  // slots of a pairing stack are empty), so the CTA's critical path is shortest
+  if (G.gid != G.groups - 1) return;
   const float* base = reinterpret_cast<const float*>(fsm_raw);
   constexpr int stride = 2 * rsm_len<L>();
   C32 v[E];
@@ -458,7 +460,7 @@ __global__ void __launch_bounds__(256, LG_SOCSROWS_MINB) fk_socs_rows(FGeo g, co
     for (int gg = 1; gg < G.groups; ++gg) s += base[gg * stride + G.idx(e)];
     v[e] = mk(s, 0.f);
   }
-  G.sync();  // every partial read before group 0 reuses its buffer
+  G.sync();  // every partial read before this group reuses its buffer
   fftr<float, L, -1>(v, G.sm, g.twnx, G.t, G.sync);
   C32* o = Ir + blockIdx.z * ir_ts + size_t(f) * (g.ax.P + 1) * ny + sy;
 #pragma unroll
@@ -1167,14 +1169,37 @@ __global__ void __launch_bounds__(256) fk_grad_cols(FGeo g, const C32* __restric
   const size_t plane = size_t(Bx) * By;
   extern __shared__ __align__(16) unsigned char fsm_raw[];
   C32* col = reinterpret_cast<C32*>(fsm_raw) + G.groups * rsm_len<L>() + G.gid * 2 * By;
-  for (int idx = G.t; idx < 2 * By; idx += G.TPR) {
-    const int which = idx >= By, jy = idx - which * By, slot = which ? sn : sp;
-    C32 q = mk(0.f, 0.f);
-    if (slot >= 0) {
-#pragma unroll 4
-      for (int k = 0; k < nsum; ++k) q = add(q, ldg_cx(a + k * plane + size_t(slot) * By + jy));
+  // up to 4 entries per thread summed side by side (independent loads in
+  // flight), each over the partials in fixed order k = 0..nsum-1
+  constexpr int MAXJ = 4;
+  if (2 * By <= MAXJ * G.TPR) {
+    const C32* src[MAXJ];
+    C32 q[MAXJ];
+#pragma unroll
+    for (int j = 0; j < MAXJ; ++j) {
+      const int idx = G.t + j * G.TPR;
+      const int which = idx >= By, jy = idx - which * By, slot = which ? sn : sp;
+      src[j] = (idx < 2 * By && slot >= 0) ? a + size_t(slot) * By + jy : nullptr;
+      q[j] = mk(0.f, 0.f);
     }
-    col[idx] = q;
+    for (int k = 0; k < nsum; ++k) {
+#pragma unroll
+      for (int j = 0; j < MAXJ; ++j)
+        if (src[j]) q[j] = add(q[j], ldg_cx(src[j] + k * plane));
+    }
+#pragma unroll
+    for (int j = 0; j < MAXJ; ++j)
+      if (G.t + j * G.TPR < 2 * By) col[G.t + j * G.TPR] = q[j];
+  } else {
+    for (int idx = G.t; idx < 2 * By; idx += G.TPR) {
+      const int which = idx >= By, jy = idx - which * By, slot = which ? sn : sp;
+      C32 q = mk(0.f, 0.f);
+      if (slot >= 0) {
+#pragma unroll 4
+        for (int k = 0; k < nsum; ++k) q = add(q, ldg_cx(a + k * plane + size_t(slot) * By + jy));
+      }
+      col[idx] = q;
+    }
   }
   G.sync();
   C32 v[E];
