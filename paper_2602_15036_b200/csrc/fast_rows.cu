@@ -7,6 +7,18 @@
 
 namespace lg {
 
+// sparsity mode of a full-resolution row transform pair whose band is
+// |p| <= P: bit 0 = the band fits slots 0 / E-1 (sparse first stage, 1-slot
+// gather), bit 1 = it fits the kSpOut slots (pruned last stage)
+template <int L>
+static int spm_of(int P) {
+  if (sparse_off()) return 0;
+  int m = 0;
+  if (P < RPlan<L>::TPR) m |= 1;
+  if (P < sp_out_slots<L>() * RPlan<L>::TPR) m |= 2;
+  return m;
+}
+
 // threads per CTA of the full-resolution row kernels (real_rows_fwd,
 // resist_rows, grad_rows) for `units` row pairs in the launch: 256 for batched
 // launches (C5 -3.6 % against 128), 128 for launches of fewer than 2048 pairs
@@ -53,11 +65,11 @@ void fl_real_rows_fwd(const FGeo& g, cudaStream_t s, int tiles, int mode, const 
     const dim3 grid(cdivi((g.ay.N + 1) / 2, gr), 1, tiles);
     const size_t extra = size_t(Pout + 1) * 2 * gr * sizeof(C32) + 16;  // transposed-store tile
     auto go = [&](auto kern) { flaunch_x<L>(kern, grid, gr, extra, s, g, src, src_ts, steep, Pout, out, out_ts); };
-    const bool sp = Pout < RPlan<L>::TPR && !sparse_off();
+    const bool sp = (spm_of<L>(Pout) & 2) != 0;
     if (mode == 0)
-      sp ? go(fk_real_rows_fwd<L, 0, true>) : go(fk_real_rows_fwd<L, 0, false>);
+      sp ? go(fk_real_rows_fwd<L, 0, 2>) : go(fk_real_rows_fwd<L, 0, 0>);
     else
-      sp ? go(fk_real_rows_fwd<L, 1, true>) : go(fk_real_rows_fwd<L, 1, false>);
+      sp ? go(fk_real_rows_fwd<L, 1, 2>) : go(fk_real_rows_fwd<L, 1, 0>);
   });
 }
 
@@ -92,11 +104,12 @@ void fl_resist_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* Rc, lon
                    row_slab_bytes<L>(gr) + size_t(g.ax.P + 1) * 2 * gr * sizeof(C32) + 16, s, g, Rc, c_ts, target,
                    tg_ts, cf, beta, thr, Dr, d_ts, costp, cp_ts);
     };
-    // band inside the first / last register slot: sparse first / last FFT stage
-    if (g.ax.P < RPlan<L>::TPR && !sparse_off())
-      go(fk_resist_rows<L, true>);
-    else
-      go(fk_resist_rows<L, false>);
+    // band inside the first / last register slots: sparse first / last FFT stage
+    switch (spm_of<L>(g.ax.P)) {
+      case 3: go(fk_resist_rows<L, 3>); break;
+      case 2: go(fk_resist_rows<L, 2>); break;
+      default: go(fk_resist_rows<L, 0>); break;
+    }
   });
 }
 
@@ -158,15 +171,21 @@ void fl_grad_rows(const FGeo& g, cudaStream_t s, int tiles, bool ilt, const C32*
     const int gr = fgroups<L>(fullrow_threads((long long)tiles * ((g.ay.N + 1) / 2)));
     const dim3 grid(cdivi((g.ay.N + 1) / 2, gr), 1, tiles);
     const size_t extra = row_slab_bytes<L>(gr) + size_t(g.ax.Pm + 1) * 2 * gr * sizeof(C32) + 16;
-    const bool sp = g.ax.Pm < RPlan<L>::TPR && !sparse_off();
+    const int spm = spm_of<L>(g.ax.Pm);
     auto go = [&](auto kern, size_t ex) {
       flaunch_x<L>(kern, grid, gr, ex, s, g, Gc, g_ts, grad, gr_ts, theta, th_ts, steep, step, Mr, mr_ts, gmaxp,
                    gm_ts);
     };
-    if (ilt)
-      sp ? go(fk_grad_rows<L, true, true>, extra) : go(fk_grad_rows<L, true, false>, extra);
-    else
-      sp ? go(fk_grad_rows<L, false, true>, 0) : go(fk_grad_rows<L, false, false>, 0);
+    if (ilt) {
+      switch (spm) {
+        case 3: go(fk_grad_rows<L, true, 3>, extra); break;
+        case 2: go(fk_grad_rows<L, true, 2>, extra); break;
+        default: go(fk_grad_rows<L, true, 0>, extra); break;
+      }
+    } else {
+      // the gradient write path reads every slot of the first transform
+      (spm & 1) ? go(fk_grad_rows<L, false, 1>, 0) : go(fk_grad_rows<L, false, 0>, 0);
+    }
   });
 }
 

@@ -294,11 +294,17 @@ __host__ __device__ constexpr bool pow2r(int r) { return r == 2 || r == 4 || r =
 
 // Sparsity flags of fftr (band-limited rows):
 //   kSpIn:  only v[0] and v[E-1] are nonzero on entry (a band |p| < TPR);
-//   kSpOut: only v[0] and v[E-1] are needed on exit (the other slots are left
-//           undefined).  Each flag is honoured where the stage structure
+//   kSpOut: only the slots [0, NB) and [E-NB, E) (NB = butterflies per thread
+//           in the last stage, sp_out_slots) are needed on exit (the other
+//           slots are left undefined).  Each flag is honoured where the stage structure
 //           allows it (power-of-two radix, one butterfly per thread in the
 //           stage concerned) and ignored otherwise (the dense path is exact).
 constexpr int kSpIn = 1, kSpOut = 2;
+// slots at each end that a kSpOut transform defines
+template <int L>
+__host__ __device__ constexpr int sp_out_slots() {
+  return RPlan<L>::E / RPlan<L>::R[RPlan<L>::NS - 1];
+}
 
 template <typename T, int L, int SIGN, int S, typename X, int SP = 0>
 __device__ __forceinline__ void fftr_stage(cx<T> (&v)[RPlan<L>::E], cx<T>* sm,
@@ -392,14 +398,16 @@ __device__ __forceinline__ void fftr_stage(cx<T> (&v)[RPlan<L>::E], cx<T>* sm,
     if constexpr (!SP_OUT) dftR<R, SIGN>(x[b]);
   }
   if constexpr (SP_OUT) {
-    // only outputs q = 0 of butterfly 0 (-> v[0]) and q = R-1 of butterfly
-    // NB-1 (-> v[E-1]) are needed
-    cx<T> y0 = x[0][0];
+    // only outputs q = 0 and q = R-1 of every butterfly are needed: slots
+    // [0, NB) and [E-NB, E) of the natural distribution
 #pragma unroll
-    for (int r = 1; r < R; ++r) y0 = add(y0, x[0][r]);
-    const cx<T> y1 = sp_out_last<R, SIGN>(x[NB - 1], std::make_integer_sequence<int, R>{});
-    v[0] = y0;
-    v[E - 1] = y1;
+    for (int b = 0; b < NB; ++b) {
+      cx<T> y0 = x[b][0];
+#pragma unroll
+      for (int r = 1; r < R; ++r) y0 = add(y0, x[b][r]);
+      v[b] = y0;
+      v[b + (R - 1) * NB] = sp_out_last<R, SIGN>(x[b], std::make_integer_sequence<int, R>{});
+    }
     return;
   }
   if constexpr (LAST) {

@@ -273,12 +273,15 @@ __device__ __forceinline__ void store_pair_cols(const FGroup<L>& G, size_t tile_
   }
 }
 
-// to_smem of the two slots a kSpOut transform defines (v[0], v[E-1])
+// to_smem of the slots a kSpOut transform defines ([0, NB) and [E-NB, E))
 template <int L>
 __device__ __forceinline__ void to_smem_sp(const C32 (&v)[RPlan<L>::E], C32* sm, int t) {
-  constexpr int E = RPlan<L>::E, TPR = RPlan<L>::TPR;
-  sm[rpad(t)] = v[0];
-  sm[rpad(t + (E - 1) * TPR)] = v[E - 1];
+  constexpr int E = RPlan<L>::E, TPR = RPlan<L>::TPR, NB = sp_out_slots<L>();
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    sm[rpad(t + b * TPR)] = v[b];
+    sm[rpad(t + (E - NB + b) * TPR)] = v[E - NB + b];
+  }
 }
 
 // min resident CTAs for the full-resolution row kernels (64 registers with the
@@ -300,7 +303,7 @@ __device__ __forceinline__ float warp_max(float v, int width) {
 // ===========================================================================
 // real row pairs -> half spectra [Pout+1][Ny] (MODE 0 raw, 1 sigmoid(steep x))
 // ===========================================================================
-template <int L, int MODE, bool SPB>
+template <int L, int MODE, int SPM>
 __global__ void __launch_bounds__(256) fk_real_rows_fwd(FGeo g, const float* __restrict__ src,
                                                         long long src_ts, float steep, int Pout,
                                                         C32* __restrict__ out, long long out_ts) {
@@ -329,9 +332,9 @@ __global__ void __launch_bounds__(256) fk_real_rows_fwd(FGeo g, const float* __r
   // kSpOut when the output band fits the first / last slot: the same
   // arithmetic as fk_grad_rows' fused next-iteration mask rows, so both
   // producers of Mr agree bitwise
-  fftr_sp<float, L, -1, SPB ? kSpOut : 0>(v, G.sm, g.twNx, G.t, G.sync);
+  fftr_sp<float, L, -1, (SPM & 2) ? kSpOut : 0>(v, G.sm, g.twNx, G.t, G.sync);
   G.sync();
-  if constexpr (SPB)
+  if constexpr ((SPM & 2) != 0)
     to_smem_sp<L>(v, G.sm, G.t);
   else
     to_smem<float, L>(v, G.sm, G.t);
@@ -475,7 +478,7 @@ __global__ void __launch_bounds__(256, LG_SOCSROWS_MINB) fk_socs_rows(FGeo g, co
 // Z = sig(beta (R - thr)), cost partial, D = 2 c_f (Z - Zt) beta Z (1 - Z),
 // FFT_Nx(D pair) -> Dr[f][px][y].  grid (ceil(Ny/2/groups), F, tiles)
 // ===========================================================================
-template <int L, bool SPB>
+template <int L, int SPM>
 __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_resist_rows(FGeo g, const C32* __restrict__ Rc,
                                                       long long c_ts, const float* __restrict__ target,
                                                       long long tg_ts, const float* __restrict__ cf,
@@ -486,7 +489,10 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_resist_rows(FGeo g, c
   TraceScope trace_(g);
   constexpr int E = RPlan<L>::E, TPR = RPlan<L>::TPR;
   constexpr int WPG = TPR >= 32 ? TPR / 32 : 1;
-  constexpr int SP_IN = SPB ? kSpIn : 0, SP_OUT = SPB ? kSpOut : 0;
+  // SPM bit 0: band inside slot 0 / E-1 (sparse first stage, 1-slot gather);
+  // bit 1: band inside the kSpOut slots (pruned last stage)
+  constexpr bool SPB = (SPM & 1) != 0, SPO = (SPM & 2) != 0;
+  constexpr int SP_IN = SPB ? kSpIn : 0, SP_OUT = SPO ? kSpOut : 0;
   const int Ny = g.ay.N, Px = g.ax.P, f = blockIdx.y, npairs = (Ny + 1) / 2;
   const int pair0 = blockIdx.x * G.groups + G.gid;
   const bool act = pair0 < npairs;
@@ -530,7 +536,7 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_resist_rows(FGeo g, c
     costp[blockIdx.z * cp_ts + (size_t(f) * npairs + pair) * WPG + (G.t >> 5)] = double(c);
   fftr_sp<float, L, -1, SP_OUT>(v, G.sm, g.twNx, G.t, G.sync);
   G.sync();
-  if constexpr (SPB)
+  if constexpr (SPO)
     to_smem_sp<L>(v, G.sm, G.t);
   else
     to_smem<float, L>(v, G.sm, G.t);
@@ -704,7 +710,7 @@ __global__ void __launch_bounds__(256, LG_ADJROWS_MINB) fk_adj_rows(FGeo g, cons
 // !ILT: write grad; ILT: theta update, then next iteration's mask rows.
 // grid (ceil(Ny/2/groups), 1, tiles)
 // ===========================================================================
-template <int L, bool ILT, bool SPB>
+template <int L, bool ILT, int SPM>
 __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_grad_rows(FGeo g, const C32* __restrict__ Gc,
                                                     long long g_ts, float* __restrict__ grad,
                                                     long long gr_ts, float* __restrict__ theta,
@@ -715,7 +721,10 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_grad_rows(FGeo g, con
   TraceScope trace_(g);
   constexpr int E = RPlan<L>::E, TPR = RPlan<L>::TPR;
   constexpr int WPG = TPR >= 32 ? TPR / 32 : 1;
-  constexpr int SP_IN = SPB ? kSpIn : 0, SP_OUT = SPB ? kSpOut : 0;
+  // SPM bit 0: band inside slot 0 / E-1 (sparse first stage, 1-slot gather);
+  // bit 1: band inside the kSpOut slots (pruned last stage)
+  constexpr bool SPB = (SPM & 1) != 0, SPO = (SPM & 2) != 0;
+  constexpr int SP_IN = SPB ? kSpIn : 0, SP_OUT = SPO ? kSpOut : 0;
   const int Ny = g.ay.N, Pm = g.ax.Pm, npairs = (Ny + 1) / 2;
   const int pair0 = blockIdx.x * G.groups + G.gid;
   const bool act = pair0 < npairs;
@@ -785,7 +794,7 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_grad_rows(FGeo g, con
   if (act && gmaxp && (G.t & 31) == 0) gmaxp[blockIdx.z * gm_ts + size_t(pair) * WPG + (G.t >> 5)] = gm;
   fftr_sp<float, L, -1, SP_OUT>(v, G.sm, g.twNx, G.t, G.sync);
   G.sync();
-  if constexpr (SPB)
+  if constexpr (SPO)
     to_smem_sp<L>(v, G.sm, G.t);
   else
     to_smem<float, L>(v, G.sm, G.t);
