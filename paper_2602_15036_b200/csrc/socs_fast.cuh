@@ -228,6 +228,14 @@ __device__ __forceinline__ void stage_rows_tma(float* dst, const float* r0, cons
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(smem_u32(dst + L)), "l"(r1), "r"(bytes), "r"(b) : "memory");
 }
+__device__ __forceinline__ void stage_wait_tma_parity(unsigned long long* bar, unsigned parity) {
+  const unsigned b = smem_u32(bar);
+  unsigned done = 0;
+  while (!done)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done) : "r"(b), "r"(parity) : "memory");
+}
 __device__ __forceinline__ void stage_wait_tma(unsigned long long* bar) {
   const unsigned b = smem_u32(bar);
   unsigned done = 0;
@@ -374,9 +382,7 @@ __global__ void __launch_bounds__(256, LG_SOCSROWS_MINB) fk_socs_rows(FGeo g, co
   for (int e = 0; e < E; ++e) acc[e] = 0.f;
   const BandMap<L> bm(G.t, lo, hi);
   // per-kernel row pointers advance by one kernel plane per slot
-  const long long tstep = (long long)ny * tld, estep = (long long)ny * L;
-  const C32* src = T + blockIdx.z * t_ts + size_t(f * K + G.gid) * tstep + size_t(sy) * tld;
-  C32* eo = Eo ? Eo + blockIdx.z * e_ts + (size_t(f * K + G.gid) * ny + sy) * L + G.t : nullptr;
+  const long long tstep = (long long)ny * tld;
   // CB: the group's T rows stream through a TMA double buffer in shared memory
   // (one bulk copy per kernel row, issued one row ahead; fk_socs_rows was
   // latency-bound on these gathers)
@@ -396,42 +402,25 @@ __global__ void __launch_bounds__(256, LG_SOCSROWS_MINB) fk_socs_rows(FGeo g, co
                    ::"r"(smem_u32(rb + b * tld)), "l"(row), "r"(rbytes), "r"(bar) : "memory");
     }
   };
-  if constexpr (CB) {
-    if (G.t == 0) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tbar[G.gid][0])) : "memory");
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tbar[G.gid][1])) : "memory");
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    G.sync();  // barrier inits before any wait
-    if (G.gid < K) prefetch(src, 0);
-  }
-  int it = 0;
-  for (int k = G.gid; k < K; k += G.groups, src += G.groups * tstep, eo += eo ? G.groups * estep : 0, ++it) {
+  // one kernel slot of this group: load its T row (CB: from the TMA buffer),
+  // transform, keep E, accumulate w |E|^2
+  auto slot = [&](int k, const C32* rowsrc) {
     const int fk = f * K + k;
     C32 v[E];
     if constexpr (CB) {
-      const int b = it & 1;
-      if (k + G.groups < K) prefetch(src + G.groups * tstep, b ^ 1);
-      unsigned done = 0;
-      const unsigned bar = smem_u32(&tbar[G.gid][b]), par = unsigned(it >> 1) & 1u;
-      while (!done)
-        asm volatile(
-            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-            : "=r"(done) : "r"(bar), "r"(par) : "memory");
-      if (g.slot_on && !g.slot_on[fk]) continue;  // empty slot (mixed kernel pairs)
-      const C32* sb = rb + b * tld + bm.base;
+      const C32* sb = rowsrc + bm.base;
 #pragma unroll
       for (int e = 0; e < E; ++e) v[e] = bm.has(e) ? sb[BandMap<L>::off(e)] : mk(0.f, 0.f);
     } else {
-      if (g.slot_on && !g.slot_on[fk]) continue;  // empty slot (mixed kernel pairs)
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const int sl = kslot(G.idx(e), lo, hi, L);
-        v[e] = sl >= 0 ? src[sl] : mk(0.f, 0.f);
+        v[e] = sl >= 0 ? rowsrc[sl] : mk(0.f, 0.f);
       }
     }
     fftr<float, L, +1>(v, G.sm, g.twnx, G.t, G.sync);
-    if (eo) {  // keep the coherent field for the adjoint (fk_adj_rows<.., FROM_E>)
+    if (Eo) {  // keep the coherent field for the adjoint (fk_adj_rows<.., FROM_E>)
+      C32* eo = Eo + blockIdx.z * e_ts + (size_t(fk) * ny + sy) * L + G.t;
 #pragma unroll
       for (int e = 0; e < E; ++e) eo[e * RPlan<L>::TPR] = v[e];
     }
@@ -444,6 +433,36 @@ __global__ void __launch_bounds__(256, LG_SOCSROWS_MINB) fk_socs_rows(FGeo g, co
 #pragma unroll
       for (int e = 0; e < E; ++e) acc[e] += w * (v[e].x * v[e].x + v[e].y * v[e].y);
     }
+  };
+  // this group's ACTIVE slots k = gid, gid + groups, ... (empty slots of mixed
+  // pairs skipped): only those are copied and waited for, so between two
+  // copies into one buffer every thread of the group passes the FFT's group
+  // barriers (a copy can never run a full mbarrier phase ahead of a waiter)
+  auto next_k = [&](int k) {
+    for (; k < K; k += G.groups)
+      if (!g.slot_on || g.slot_on[f * K + k]) return k;
+    return K;
+  };
+  const C32* trow0 = T + blockIdx.z * t_ts + size_t(f * K) * tstep + size_t(sy) * tld;
+  if constexpr (CB) {
+    if (G.t == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tbar[G.gid][0])) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tbar[G.gid][1])) : "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    G.sync();  // barrier inits before any wait
+    int k = next_k(G.gid);
+    if (k < K) prefetch(trow0 + size_t(k) * tstep, 0);
+    for (int j = 0; k < K; ++j) {
+      const int kn = next_k(k + G.groups);
+      if (kn < K) prefetch(trow0 + size_t(kn) * tstep, (j + 1) & 1);
+      const int b = j & 1;
+      stage_wait_tma_parity(&tbar[G.gid][b], unsigned(j >> 1) & 1u);
+      slot(k, rb + b * tld);
+      k = kn;
+    }
+  } else {
+    for (int k = next_k(G.gid); k < K; k = next_k(k + G.groups)) slot(k, trow0 + size_t(k) * tstep);
   }
   G.sync();  // exchange buffer free: publish the group's partial row
   float* red = reinterpret_cast<float*>(G.sm);
