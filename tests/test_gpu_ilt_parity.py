@@ -135,6 +135,31 @@ def test_ilt_gradient_c4(ctx):
     assert rel_linf(grad[0], g_ref) <= TOL
 
 
+@pytest.mark.timeout(300)
+def test_c4_graph_replays_complete(sctx):
+    """Regression: many graph-replayed C4 iterations on a stream (two-warp row
+    groups of the n = 768 plan, empty slots of the paired in-focus stack) run
+    to completion with a deterministic cost trajectory (a TMA double-buffer
+    phase race once hung here)."""
+    import torch
+    n, K, foci = 4096, 32, (-40.0, 0.0, 40.0)
+    ks = L.build_socs_kernels(euv(), L.Grid(n, n, 1.0), list(foci), k_fixed=K, backend="gpu", ctx=sctx)
+    target, theta0 = bench_tile(n, seed=5)
+    solver = L.IltSolver(ks, L.IltParams(focus_weights=[1.0 / 3] * 3, **ILT), 1, "f32", sctx)
+    cost = torch.zeros((50, 1), dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    first = None
+    for _ in range(12):
+        solver.set_tiles(target[None].astype(np.float32), theta0[None].astype(np.float32))
+        solver.run_device(50, cost)
+        sctx.synchronize()
+        c = cost[:, 0].cpu().numpy().copy()
+        if first is None:
+            first = c
+        assert np.array_equal(c, first)
+    assert first[-1] < first[0]
+
+
 def test_ilt_gradient_f64_path(ctx):
     """fp64 (reference-tolerance) path: gradient at 1e-9."""
     n, foci = 64, (-40.0, 0.0, 40.0)
