@@ -194,6 +194,13 @@ lithogpu_status lithogpu_ilt_get_tile(lithogpu_ilt* ilt, int tile, void* theta, 
  * e.g. the core [halo, halo+core)^2 written straight into the chip image). */
 lithogpu_status lithogpu_ilt_get_window(lithogpu_ilt* ilt, int tile, int x0, int y0, int w, int h, void* mask,
                                         int64_t row_stride, lithogpu_dtype dtype);
+/* The same, stream-ordered on the context stream without waiting: `mask` is
+ * device memory or PAGE-LOCKED host memory (cudaHostAlloc / pinned), valid
+ * once the context stream has passed the copy (lithogpu_ctx_synchronize).
+ * Lets a caller pipeline the D2H of one tile batch under the next batch's
+ * iterations (e.g. on a second context).  Pageable host memory: USAGE. */
+lithogpu_status lithogpu_ilt_get_window_async(lithogpu_ilt* ilt, int tile, int x0, int y0, int w, int h,
+                                              void* mask, int64_t row_stride, lithogpu_dtype dtype);
 /* all tiles: n_tiles*nx*ny (nullable outs) */
 lithogpu_status lithogpu_ilt_get_tiles(lithogpu_ilt* ilt, void* theta, void* mask,
                                        lithogpu_dtype dtype);

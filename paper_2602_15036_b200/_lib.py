@@ -75,6 +75,8 @@ _SIGS = {
     "lithogpu_ilt_gradient": (C.c_int, [_vp, _vp, _vp, C.c_int]),
     "lithogpu_ilt_get_window": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _vp, C.c_int64,
                                           C.c_int]),
+    "lithogpu_ilt_get_window_async": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _vp, C.c_int64,
+                                                C.c_int]),
     "lithogpu_ilt_get_tile": (C.c_int, [_vp, C.c_int, _vp, _vp, C.c_int]),
     "lithogpu_ilt_get_tiles": (C.c_int, [_vp, _vp, _vp, C.c_int]),
     "lithogpu_marching_squares": (C.c_int, [_vp, C.POINTER(Grid), _vp, C.c_double, C.POINTER(_vp)]),

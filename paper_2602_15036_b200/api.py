@@ -746,10 +746,12 @@ class IltSolver:
         check(lib().lithogpu_ilt_get_tiles(self._h, ptr(theta), ptr(mask), dtype))
         return theta, mask
 
-    def get_window(self, tile: int, x0: int, y0: int, w: int, h: int, out=None, dtype=F32):
+    def get_window(self, tile: int, x0: int, y0: int, w: int, h: int, out=None, dtype=F32, async_: bool = False):
         """Mask window of one tile (lithogpu_ilt_get_window) into `out`
         (numpy / CUDA tensor view with unit column stride, e.g. a block of
-        the stitched chip mask) or a new (h, w) host array."""
+        the stitched chip mask) or a new (h, w) host array.  async_: stream-
+        ordered without waiting (lithogpu_ilt_get_window_async; `out` must be
+        device or pinned host memory, valid after the context synchronizes)."""
         if out is None:
             out = np.empty((h, w), np.float32 if dtype == F32 else np.float64)
         if _is_torch(out):
@@ -760,7 +762,8 @@ class IltSolver:
                 raise ValueError("get_window: out needs unit column stride")
             ptr, stride = out.ctypes.data, out.strides[0] // out.itemsize
             dt = _NP2DT[out.dtype]
-        check(lib().lithogpu_ilt_get_window(self._h, tile, x0, y0, w, h, ptr, stride, dt))
+        fn = lib().lithogpu_ilt_get_window_async if async_ else lib().lithogpu_ilt_get_window
+        check(fn(self._h, tile, x0, y0, w, h, ptr, stride, dt))
         return out
 
     def close(self):

@@ -2331,8 +2331,21 @@ lithogpu_status lithogpu_ilt_gradient(lithogpu_ilt* ilt, double* cost, void* gra
   });
 }
 
+static lithogpu_status ilt_get_window_impl(lithogpu_ilt* ilt, int tile, int x0, int y0, int w, int h, void* mask,
+                                           int64_t row_stride, lithogpu_dtype dtype, bool async);
+
 lithogpu_status lithogpu_ilt_get_window(lithogpu_ilt* ilt, int tile, int x0, int y0, int w, int h, void* mask,
                                         int64_t row_stride, lithogpu_dtype dtype) {
+  return ilt_get_window_impl(ilt, tile, x0, y0, w, h, mask, row_stride, dtype, false);
+}
+
+lithogpu_status lithogpu_ilt_get_window_async(lithogpu_ilt* ilt, int tile, int x0, int y0, int w, int h,
+                                              void* mask, int64_t row_stride, lithogpu_dtype dtype) {
+  return ilt_get_window_impl(ilt, tile, x0, y0, w, h, mask, row_stride, dtype, true);
+}
+
+static lithogpu_status ilt_get_window_impl(lithogpu_ilt* ilt, int tile, int x0, int y0, int w, int h, void* mask,
+                                           int64_t row_stride, lithogpu_dtype dtype, bool async) {
   if (!ilt || !mask) {
     g_last_error = "lithogpu_ilt_get_window: null argument";
     return LITHOGPU_ERR_USAGE;
@@ -2347,11 +2360,21 @@ lithogpu_status lithogpu_ilt_get_window(lithogpu_ilt* ilt, int tile, int x0, int
     ctx->activate();
     const size_t es = dtype_size(dtype);
     const bool dev = is_device_ptr(mask);
+    if (async && !dev) {
+      cudaPointerAttributes a{};
+      if (cudaPointerGetAttributes(&a, mask) != cudaSuccess || a.type != cudaMemoryTypeHost) {
+        cudaGetLastError();
+        throw UsageError("lithogpu_ilt_get_window_async: mask must be device or page-locked host memory");
+      }
+    }
     void* dst = mask;
     long long stride = row_stride;
-    if (!dev) {
-      DevBuf& b = ctx->slot(0);
-      b.ensure(es * size_t(w) * h);
+    if (!dev) {  // staging window (stream-ordered reuse: the next call's kernel runs after this copy)
+      DevBuf& b = ctx->slot(async ? 22 : 0);
+      if (b.bytes < es * size_t(w) * h) {
+        if (async) LG_CUDA(cudaStreamSynchronize(ctx->stream));  // a pending copy may still read it
+        b.ensure(es * size_t(w) * h);
+      }
       dst = b.p;
       stride = w;
     }
@@ -2376,7 +2399,7 @@ lithogpu_status lithogpu_ilt_get_window(lithogpu_ilt* ilt, int tile, int x0, int
     if (!dev) {
       LG_CUDA(cudaMemcpy2DAsync(mask, size_t(row_stride) * es, dst, size_t(w) * es, size_t(w) * es, size_t(h),
                                 cudaMemcpyDeviceToHost, ctx->stream));
-      LG_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (!async) LG_CUDA(cudaStreamSynchronize(ctx->stream));
     }
   });
 }

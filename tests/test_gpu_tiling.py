@@ -156,3 +156,12 @@ def test_ilt_get_window_stitches_chip_mask(ctx):
     ctx.synchronize()
     assert np.array_equal(host, want)
     assert np.array_equal(dev.cpu().numpy(), want)
+    # stream-ordered variant into page-locked host memory; pageable memory is a usage error
+    pinned = torch.zeros((tl.chip.ny, tl.chip.nx), dtype=torch.float32).pin_memory()
+    for t in range(len(tl)):
+        i, j = tl.tile_ij(t)
+        ci.solver.get_window(t, h, h, c, c, out=pinned[j * c:(j + 1) * c, i * c:(i + 1) * c], async_=True)
+    ctx.synchronize()
+    assert np.array_equal(pinned.numpy(), want)
+    with pytest.raises(L.api.LithoUsageError):
+        ci.solver.get_window(0, h, h, c, c, out=host[:c, :c], async_=True)
