@@ -294,8 +294,9 @@ __device__ __forceinline__ void to_smem_sp(const C32 (&v)[RPlan<L>::E], C32* sm,
 
 // min resident CTAs for the full-resolution row kernels (64 registers with the
 // 2048 = 8*8*8*4 plan)
+// (after the twiddle-product change: 3 CTAs/SM, 85 registers, -1.1 % at C5)
 #ifndef LG_FULLROW_MINB
-#define LG_FULLROW_MINB 4
+#define LG_FULLROW_MINB 3
 #endif
 
 // warp-partial (deterministic) reduction: lane 0 of each warp-slice writes
@@ -635,7 +636,9 @@ __global__ void __launch_bounds__(256) fk_wlp_rows(FGeo g, const C32* __restrict
 // grid (ceil(ny/groups), F*K, tiles)
 // ===========================================================================
 #ifndef LG_ADJROWS_MINB
-#define LG_ADJROWS_MINB 4  // C5 A/B: 4 CTAs/SM (64 regs) +3.4 % per iteration over 2 (profiles/r2_ab1_occupancy.log)
+// C5 A/B: 4 CTAs/SM (64 regs) was +3.4 % over 2 (profiles/r2_ab1_occupancy.log); after the twiddle-product
+// change 3 CTAs/SM (85 regs) is 1.5 % faster than 4
+#define LG_ADJROWS_MINB 3
 #endif
 template <int L, bool UNIFORM, bool FROM_E, bool CB>
 __global__ void __launch_bounds__(256, LG_ADJROWS_MINB) fk_adj_rows(FGeo g, const C32* __restrict__ T,
