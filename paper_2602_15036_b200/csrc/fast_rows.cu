@@ -146,7 +146,10 @@ void fl_adj_rows(const FGeo& g, cudaStream_t s, int tiles, int nf, bool uniform,
     kc = kc < 1 ? 1 : (kc > 8 ? 8 : kc);
     if (const char* e = std::getenv("LITHOGPU_ADJ_KC")) kc = std::max(1, std::atoi(e));
     const dim3 grid(cdivi(g.ay.n, gr), cdivi(nfk, kc), tiles);
-    const size_t extra = size_t(g.ax.B) * (gr | 1) * sizeof(C32);  // staging tile
+    // staging tile (16-byte padded) + one E row per group (TMA buffer, FROM_E)
+    const size_t pad = groups_bytes<L>(gr) - size_t(gr) * rsm_len<L>() * sizeof(C32);
+    const size_t tile_bytes = (size_t(g.ax.B) * (gr | 1) * sizeof(C32) + 15) & ~size_t(15);
+    const size_t extra = pad + tile_bytes + ((from_e && LG_ADJ_TMA) ? size_t(gr) * L * sizeof(C32) : 0);
     auto go = [&](auto kern) { flaunch_x<L>(kern, grid, gr, extra, s, g, T, t_ts, Wsub, ws_ts, U, u_ts, kc, nfk); };
     const bool cb = centered_band(L, RPlan<L>::E, g.ax.lo, g.ax.hi) && !sparse_off();
     if (cb) {

@@ -635,6 +635,11 @@ __global__ void __launch_bounds__(256) fk_wlp_rows(FGeo g, const C32* __restrict
 //   U_fk[qx][sy] = FFT_nx(W_lp(sy,.) . IFFT_nx(T_fk[sy]))(qx), qx in band
 // grid (ceil(ny/groups), F*K, tiles)
 // ===========================================================================
+// TMA-prefetched E rows in adj_rows: measured neutral-to-slower at C5 / C4 / C2
+// (+0.2-0.6 %), so off by default (A/B switch)
+#ifndef LG_ADJ_TMA
+#define LG_ADJ_TMA 0
+#endif
 #ifndef LG_ADJROWS_MINB
 // C5 A/B: 4 CTAs/SM (64 regs) was +3.4 % over 2 (profiles/r2_ab1_occupancy.log); after the twiddle-product
 // change 3 CTAs/SM (85 regs) is 1.5 % faster than 4
@@ -659,18 +664,54 @@ __global__ void __launch_bounds__(256, LG_ADJROWS_MINB) fk_adj_rows(FGeo g, cons
   const int ld = G.groups | 1;
   const int nr = min(G.groups, ny - r0);
   const int lgg = __ffs(G.groups) - 1;  // groups is a power of two (fgroups)
-  // kc kernel slots per CTA (amortises the setup over several transforms)
-  int fk = blockIdx.y * kc, f = fk / K, kin = fk - f * K;
-  for (int it = 0; it < kc; ++it, ++fk, ++kin) {
-    if (kin == K) {
-      kin = 0;
-      ++f;
+  // kc kernel slots per CTA (amortises the setup over several transforms);
+  // empty slots (mixed pairs) are skipped, CTA-uniformly
+  const int fk_begin = blockIdx.y * kc, fk_end = min(fk_begin + kc, nfk);
+  auto next_active = [&](int x) {
+    for (; x < fk_end; ++x)
+      if (!g.slot_on || g.slot_on[x]) return x;
+    return -1;
+  };
+  // FROM_E (LG_ADJ_TMA): the group's E row (L complex, contiguous, from HBM)
+  // arrives by TMA bulk copy into shared memory, the next slot's copy issued
+  // as soon as this one is in registers (after a group barrier, so a copy
+  // never runs a phase ahead of a waiter)
+  const size_t tile_bytes = (size_t(Bx) * ld * sizeof(C32) + 15) & ~size_t(15);
+  C32* eb = reinterpret_cast<C32*>(fsm_raw + groups_bytes<L>(G.groups) + tile_bytes) + size_t(G.gid) * L;
+  __shared__ unsigned long long ebar[16];
+  auto erow = [&](int fk) { return T + blockIdx.z * t_ts + (size_t(fk) * ny + sy) * L; };
+  auto prefetch = [&](int fk) {
+    if (G.t == 0) {
+      const unsigned bar = smem_u32(&ebar[G.gid]);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(unsigned(L * sizeof(C32)))
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(smem_u32(eb)), "l"(erow(fk)), "r"(unsigned(L * sizeof(C32))), "r"(bar) : "memory");
     }
-    if (fk >= nfk) break;  // nfk = nf * K slots of this launch
-    if (g.slot_on && !g.slot_on[fk]) continue;  // empty slot: U never read (CTA-uniform)
+  };
+  constexpr bool TMA_E = FROM_E && LG_ADJ_TMA;
+  int cur = next_active(fk_begin);
+  if constexpr (TMA_E) {
+    if (G.t == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&ebar[G.gid])) : "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    G.sync();  // barrier init before any wait
+    if (cur >= 0) prefetch(cur);
+  }
+  for (int j = 0; cur >= 0; ++j) {
+    const int fk = cur, f = fk / K;
+    const int nxt = next_active(fk + 1);
     C32 v[E];
-    if (FROM_E) {  // T holds the fields E_fk[sy][x] kept by fk_socs_rows
-      const C32* src = T + blockIdx.z * t_ts + (size_t(fk) * ny + sy) * L + G.t;
+    if constexpr (TMA_E) {
+      stage_wait_tma_parity(&ebar[G.gid], unsigned(j) & 1u);
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[e] = eb[G.t + e * TPR];
+      G.sync();  // the group's reads of eb done before it is refilled
+      if (nxt >= 0) prefetch(nxt);
+    } else if (FROM_E) {  // T holds the fields E_fk[sy][x] kept by fk_socs_rows
+      const C32* src = erow(fk) + G.t;
 #pragma unroll
       for (int e = 0; e < E; ++e) v[e] = src[e * TPR];
     } else if (CB) {
@@ -724,6 +765,7 @@ __global__ void __launch_bounds__(256, LG_ADJROWS_MINB) fk_adj_rows(FGeo g, cons
       }
     }
     __syncthreads();  // tile free for the next slot
+    cur = nxt;
   }
 }
 
