@@ -1,4 +1,6 @@
 // fp32 fast path: column-kernel launchers (see socs_fast.h).
+#include <cstdlib>
+
 #include "fast_common.cuh"
 
 namespace lg {
@@ -17,7 +19,8 @@ void fl_socs_cols(const FGeo& g, cudaStream_t s, int tiles, const C32* Mhat, lon
                   const C32* H, C32* T, long long t_ts) {
   with_len(g.ay.n, [&](auto c) {
     constexpr int L = decltype(c)::value;
-    const int gr = fgroups<L>(4 * RPlan<L>::TPR);  // 4 columns per CTA: -0.7 % vs 8 at C2
+    int gr = fgroups<L>(4 * RPlan<L>::TPR);  // 4 columns per CTA: -0.7 % vs 8 at C2
+    if (const char* e = std::getenv("LITHOGPU_SOCSCOLS_GROUPS")) gr = fgroups<L>(std::atoi(e) * RPlan<L>::TPR);
     const size_t extra = size_t(L) * (gr | 1) * sizeof(C32);  // staging tile
     auto go = [&](auto kern) {
       flaunch_x<L>(kern, dim3(cdivi(g.ax.B, gr), g.F * g.K, tiles), gr, extra, s, g, Mhat, mh_ts, H, T, t_ts);
@@ -56,7 +59,7 @@ void fl_adj_cols(const FGeo& g, cudaStream_t s, int tiles, const C32* U, long lo
                  const C32* H, const float* wk, float dose, C32* Accp, long long a_ts) {
   with_len(g.ay.n, [&](auto c) {
     constexpr int L = decltype(c)::value;
-    const int kg = kgroups<L>(g.K);
+    const int kg = kgroups<L>(g.K);  // fl_grad_cols sums F*K/kg partials: keep the two in step
     auto go = [&](auto kern) {
       flaunch<L>(kern, dim3(g.ax.B, g.F * g.K / kg, tiles), kg, s, g, U, u_ts, H, wk, dose, Accp, a_ts);
     };
