@@ -292,6 +292,96 @@ __device__ __forceinline__ cx<T> sp_out_last(const cx<T> (&x)[R], std::integer_s
 
 __host__ __device__ constexpr bool pow2r(int r) { return r == 2 || r == 4 || r == 8 || r == 16; }
 
+// ---- twiddled radix-2^j butterflies with the first radix-2 layer fused into
+// FMAs (LG_FMA_L1).  For the pairs (r, r + R/2) of a twiddled stage:
+//   t = x_r W^r,  p = t + x_{r+R/2} W^{r+R/2}  (4 FFMA),  m = 2t - p  (2 FFMA)
+// instead of two complex products and two complex adds (-2 instructions per
+// pair); the rest of the radix-R DFT takes the (p, m) pairs.
+#ifndef LG_FMA_L1
+#define LG_FMA_L1 1
+#endif
+template <typename T>
+__device__ __forceinline__ void fma_pair(cx<T> t, cx<T> b, cx<T> wb, cx<T>& p, cx<T>& m) {
+  p.x = fma(b.x, wb.x, fma(-b.y, wb.y, t.x));
+  p.y = fma(b.x, wb.y, fma(b.y, wb.x, t.y));
+  m.x = fma(T(2), t.x, -p.x);
+  m.y = fma(T(2), t.y, -p.y);
+}
+// dft4 of (v0, v1, v2, v3) given p_r = v_r + v_{r+2}, m_r = v_r - v_{r+2}
+template <int S, typename T>
+__device__ __forceinline__ void dft4_pm(const cx<T>* p, const cx<T>* m, cx<T>* v) {
+  const cx<T> t3 = mul_si<S>(m[1]);
+  v[0] = add(p[0], p[1]);
+  v[2] = sub(p[0], p[1]);
+  v[1] = add(m[0], t3);
+  v[3] = sub(m[0], t3);
+}
+template <int S, typename T>
+__device__ __forceinline__ void dft8_pm(const cx<T>* p, const cx<T>* m, cx<T>* v) {
+  // evens v0, v2, v4, v6: pairs (v0, v4) = (p0, m0), (v2, v6) = (p2, m2)
+  cx<T> e[4], o[4];
+  const cx<T> pe[2] = {p[0], p[2]}, me[2] = {m[0], m[2]}, po[2] = {p[1], p[3]}, mo[2] = {m[1], m[3]};
+  dft4_pm<S>(pe, me, e);
+  dft4_pm<S>(po, mo, o);
+  o[1] = twc<8, 1, S>(o[1]);
+  o[2] = twc<8, 2, S>(o[2]);
+  o[3] = twc<8, 3, S>(o[3]);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    v[i] = add(e[i], o[i]);
+    v[i + 4] = sub(e[i], o[i]);
+  }
+}
+template <int S, typename T>
+__device__ __forceinline__ void dft16_pm(const cx<T>* p, const cx<T>* m, cx<T>* v) {
+  cx<T> pe[4], me[4], po[4], mo[4], e[8], o[8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    pe[i] = p[2 * i];
+    me[i] = m[2 * i];
+    po[i] = p[2 * i + 1];
+    mo[i] = m[2 * i + 1];
+  }
+  dft8_pm<S>(pe, me, e);
+  dft8_pm<S>(po, mo, o);
+  o[1] = twc<16, 1, S>(o[1]);
+  o[2] = twc<16, 2, S>(o[2]);
+  o[3] = twc<16, 3, S>(o[3]);
+  o[4] = twc<16, 4, S>(o[4]);
+  o[5] = twc<16, 5, S>(o[5]);
+  o[6] = twc<16, 6, S>(o[6]);
+  o[7] = twc<16, 7, S>(o[7]);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    v[i] = add(e[i], o[i]);
+    v[i + 8] = sub(e[i], o[i]);
+  }
+}
+// twiddled radix-R butterfly (R = 4, 8, 16): x[r] <- DFT_R(x[r] W^r), w[r] = W^r (w[0] unused)
+template <int R, int S, typename T>
+__device__ __forceinline__ void dftR_tw_fma(cx<T> (&x)[R], const cx<T> (&w)[R]) {
+  constexpr int H = R / 2;
+  cx<T> p[H], m[H];
+#pragma unroll
+  for (int r = 0; r < H; ++r) {
+    cx<T> wb = w[r + H];
+    if (S > 0) wb.y = -wb.y;
+    cx<T> t = x[r];
+    if (r > 0) {
+      cx<T> wa = w[r];
+      if (S > 0) wa.y = -wa.y;
+      t = mul(t, wa);
+    }
+    fma_pair(t, x[r + H], wb, p[r], m[r]);
+  }
+  if constexpr (R == 4)
+    dft4_pm<S>(p, m, x);
+  else if constexpr (R == 8)
+    dft8_pm<S>(p, m, x);
+  else
+    dft16_pm<S>(p, m, x);
+}
+
 // Sparsity flags of fftr (band-limited rows):
 //   kSpIn:  only v[0] and v[E-1] are nonzero on entry (a band |p| < TPR);
 //   kSpOut: only the slots [0, NB) and [E-NB, E) (NB = butterflies per thread
@@ -387,15 +477,19 @@ __device__ __forceinline__ void fftr_stage(cx<T> (&v)[RPlan<L>::E], cx<T>* sm,
   }
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
-    if constexpr (Ns > 1) {
+    if constexpr (Ns > 1 && !SP_OUT && LG_FMA_L1 && (R == 4 || R == 8 || R == 16)) {
+      dftR_tw_fma<R, SIGN>(x[b], w[b]);  // twiddles fused into the first radix-2 layer
+    } else {
+      if constexpr (Ns > 1) {
 #pragma unroll
-      for (int r = 1; r < R; ++r) {
-        cx<T> ww = w[b][r];
-        if (SIGN > 0) ww.y = -ww.y;
-        x[b][r] = mul(x[b][r], ww);
+        for (int r = 1; r < R; ++r) {
+          cx<T> ww = w[b][r];
+          if (SIGN > 0) ww.y = -ww.y;
+          x[b][r] = mul(x[b][r], ww);
+        }
       }
+      if constexpr (!SP_OUT) dftR<R, SIGN>(x[b]);
     }
-    if constexpr (!SP_OUT) dftR<R, SIGN>(x[b]);
   }
   if constexpr (SP_OUT) {
     // only outputs q = 0 and q = R-1 of every butterfly are needed: slots
