@@ -26,7 +26,7 @@ void fl_socs_cols(const FGeo& g, cudaStream_t s, int tiles, const C32* Mhat, lon
       flaunch_x<L>(kern, dim3(cdivi(g.ax.B, gr), g.F * g.K, tiles), gr, extra, s, g, Mhat, mh_ts, H, T, t_ts);
     };
     if (centered_band(L, RPlan<L>::E, g.ay.lo, g.ay.hi) && !sparse_off())
-      go(fk_socs_cols<L, true>);
+      band_fits_sp<L>(g.ay.lo, g.ay.hi) ? go(fk_socs_cols<L, true, true>) : go(fk_socs_cols<L, true, false>);
     else
       go(fk_socs_cols<L, false>);
   });
@@ -64,7 +64,7 @@ void fl_adj_cols(const FGeo& g, cudaStream_t s, int tiles, const C32* U, long lo
       flaunch<L>(kern, dim3(g.ax.B, g.F * g.K / kg, tiles), kg, s, g, U, u_ts, H, wk, dose, Accp, a_ts);
     };
     if (centered_band(L, RPlan<L>::E, g.ay.lo, g.ay.hi) && !sparse_off())
-      go(fk_adj_cols<L, true>);
+      band_fits_sp<L>(g.ay.lo, g.ay.hi) ? go(fk_adj_cols<L, true, true>) : go(fk_adj_cols<L, true, false>);
     else
       go(fk_adj_cols<L, false>);
   });

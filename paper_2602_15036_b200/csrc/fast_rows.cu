@@ -87,7 +87,7 @@ void fl_socs_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* T, long l
                    wk2, dose, Ir, ir_ts, Eo, e_ts);
     };
     if (centered_band(L, RPlan<L>::E, g.ax.lo, g.ax.hi) && !sparse_off())
-      go(fk_socs_rows<L, true>);
+      band_fits_sp<L>(g.ax.lo, g.ax.hi) ? go(fk_socs_rows<L, true, true>) : go(fk_socs_rows<L, true, false>);
     else
       go(fk_socs_rows<L, false>);
   });
@@ -152,7 +152,12 @@ void fl_adj_rows(const FGeo& g, cudaStream_t s, int tiles, int nf, bool uniform,
     const size_t extra = pad + tile_bytes + ((from_e && LG_ADJ_TMA) ? size_t(gr) * L * sizeof(C32) : 0);
     auto go = [&](auto kern) { flaunch_x<L>(kern, grid, gr, extra, s, g, T, t_ts, Wsub, ws_ts, U, u_ts, kc, nfk); };
     const bool cb = centered_band(L, RPlan<L>::E, g.ax.lo, g.ax.hi) && !sparse_off();
-    if (cb) {
+    if (cb && band_fits_sp<L>(g.ax.lo, g.ax.hi)) {
+      if (uniform)
+        from_e ? go(fk_adj_rows<L, true, true, true, true>) : go(fk_adj_rows<L, true, false, true, true>);
+      else
+        from_e ? go(fk_adj_rows<L, false, true, true, true>) : go(fk_adj_rows<L, false, false, true, true>);
+    } else if (cb) {
       if (uniform)
         from_e ? go(fk_adj_rows<L, true, true, true>) : go(fk_adj_rows<L, true, false, true>);
       else

@@ -383,13 +383,19 @@ __device__ __forceinline__ void dftR_tw_fma(cx<T> (&x)[R], const cx<T> (&w)[R]) 
 }
 
 // Sparsity flags of fftr (band-limited rows):
-//   kSpIn:  only v[0] and v[E-1] are nonzero on entry (a band |p| < TPR);
+//   kSpIn:  only the slots [0, NB) and [E-NB, E) (NB = butterflies per thread
+//           in the first stage, sp_in_slots) are nonzero on entry;
 //   kSpOut: only the slots [0, NB) and [E-NB, E) (NB = butterflies per thread
 //           in the last stage, sp_out_slots) are needed on exit (the other
 //           slots are left undefined).  Each flag is honoured where the stage structure
 //           allows it (power-of-two radix, one butterfly per thread in the
 //           stage concerned) and ignored otherwise (the dense path is exact).
 constexpr int kSpIn = 1, kSpOut = 2;
+// slots at each end that a kSpIn transform may hold nonzero
+template <int L>
+__host__ __device__ constexpr int sp_in_slots() {
+  return RPlan<L>::E / RPlan<L>::R[0];
+}
 // slots at each end that a kSpOut transform defines
 template <int L>
 __host__ __device__ constexpr int sp_out_slots() {
@@ -403,29 +409,10 @@ __device__ __forceinline__ void fftr_stage(cx<T> (&v)[RPlan<L>::E], cx<T>* sm,
   using G = Stg<L, S>;
   constexpr int E = P::E, R = G::R, NB = E / R, TPR = P::TPR, Ns = G::Ns;
   constexpr bool FIRST = S == 0, LAST = S == P::NS - 1;
-  constexpr bool SP_IN = FIRST && (SP & kSpIn) && NB == 1 && pow2r(R);
+  // kSpIn: only slots [0, NB) and [E-NB, E) are nonzero on entry, i.e. only
+  // inputs r = 0 and r = R-1 of every first-stage butterfly
+  constexpr bool SP_IN = FIRST && (SP & kSpIn) && pow2r(R);
   constexpr bool SP_OUT = LAST && (SP & kSpOut) && pow2r(R) && !FIRST;
-  if constexpr (SP_IN) {
-    // y_q = v0 + v_{R-1} W^{S q (R-1)}: one rotation per output
-    const cx<T> a = v[0], b = v[R - 1];
-    cx<T> y[R];
-    sp_in_outputs<R, SIGN>(y, a, b, std::make_integer_sequence<int, R>{});
-    if constexpr (LAST) {
-#pragma unroll
-      for (int r = 0; r < R; ++r) v[r] = y[r];
-      return;
-    } else {
-      sync();
-      constexpr int SWc = X::sw < 0 ? 0 : X::sw;
-      // Ns = 1: butterfly j = t writes t*R + r
-#pragma unroll
-      for (int r = 0; r < R; ++r) X::template st<T>(sm, L, t * R + r, y[r]);
-      (void)SWc;
-      sync();
-      fftr_stage<T, L, SIGN, S + 1, X, SP>(v, sm, tw, t, sync);
-      return;
-    }
-  }
   cx<T> x[NB][R];
   cx<T> w[NB][R];
   if constexpr (Ns > 1) {
@@ -455,7 +442,16 @@ __device__ __forceinline__ void fftr_stage(cx<T> (&v)[RPlan<L>::E], cx<T>* sm,
     }
   }
   constexpr int SW = X::sw;
-  if constexpr (FIRST) {
+  if constexpr (SP_IN) {
+    // y_q = x_0 + x_{R-1} W^{S q (R-1)}: one rotation per output, no butterfly
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      cx<T> y[R];
+      sp_in_outputs<R, SIGN>(y, v[b], v[b + (R - 1) * NB], std::make_integer_sequence<int, R>{});
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[b][r] = y[r];
+    }
+  } else if constexpr (FIRST) {
 #pragma unroll
     for (int b = 0; b < NB; ++b)
 #pragma unroll
@@ -488,7 +484,7 @@ __device__ __forceinline__ void fftr_stage(cx<T> (&v)[RPlan<L>::E], cx<T>* sm,
           x[b][r] = mul(x[b][r], ww);
         }
       }
-      if constexpr (!SP_OUT) dftR<R, SIGN>(x[b]);
+      if constexpr (!SP_OUT && !SP_IN) dftR<R, SIGN>(x[b]);
     }
   }
   if constexpr (SP_OUT) {

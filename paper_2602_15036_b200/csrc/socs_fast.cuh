@@ -117,6 +117,14 @@ struct BandMap {
 __host__ __device__ inline bool centered_band(int L, int E, int lo, int hi) {
   return E % 2 == 0 && lo <= 0 && hi >= 0 && 2 * hi < L && -2 * lo < L;
 }
+// the band [lo, hi] fits the kSpIn / kSpOut slots of the length-L plan
+// (centered): sparse first stage (band input) / pruned last stage (band output)
+template <int L>
+__host__ __device__ inline bool band_fits_sp(int lo, int hi) {
+  constexpr int TPR = RPlan<L>::TPR;
+  const int w = (sp_in_slots<L>() < sp_out_slots<L>() ? sp_in_slots<L>() : sp_out_slots<L>()) * TPR;
+  return hi < w && -lo < w;
+}
 
 // intensity-band slot of residue i mod L (band2 layout of geom.h), or -1
 __device__ __forceinline__ int islot(const AxisGeom& a, int i, int L) {
@@ -367,7 +375,7 @@ __global__ void __launch_bounds__(256) fk_real_rows_fwd(FGeo g, const float* __r
 #ifndef LG_SOCSROWS_MINB
 #define LG_SOCSROWS_MINB 3
 #endif
-template <int L, bool CB>
+template <int L, bool CB, bool SPF = false>
 __global__ void __launch_bounds__(256, LG_SOCSROWS_MINB) fk_socs_rows(FGeo g, const C32* __restrict__ T,
                                                     long long t_ts, const float* __restrict__ wk,
                                                     const float* __restrict__ wk2, float dose,
@@ -419,7 +427,7 @@ __global__ void __launch_bounds__(256, LG_SOCSROWS_MINB) fk_socs_rows(FGeo g, co
         v[e] = sl >= 0 ? rowsrc[sl] : mk(0.f, 0.f);
       }
     }
-    fftr<float, L, +1>(v, G.sm, g.twnx, G.t, G.sync);
+    fftr_sp<float, L, +1, SPF ? kSpIn : 0>(v, G.sm, g.twnx, G.t, G.sync);
     if (Eo) {  // keep the coherent field for the adjoint (fk_adj_rows<.., FROM_E>)
       C32* eo = Eo + blockIdx.z * e_ts + (size_t(fk) * ny + sy) * L + G.t;
 #pragma unroll
@@ -645,7 +653,7 @@ __global__ void __launch_bounds__(256) fk_wlp_rows(FGeo g, const C32* __restrict
 // change 3 CTAs/SM (85 regs) is 1.5 % faster than 4
 #define LG_ADJROWS_MINB 3
 #endif
-template <int L, bool UNIFORM, bool FROM_E, bool CB>
+template <int L, bool UNIFORM, bool FROM_E, bool CB, bool SPF = false>
 __global__ void __launch_bounds__(256, LG_ADJROWS_MINB) fk_adj_rows(FGeo g, const C32* __restrict__ T,
                                                       long long t_ts, const float* __restrict__ Wsub,
                                                       long long ws_ts, C32* __restrict__ U,
@@ -732,12 +740,12 @@ __global__ void __launch_bounds__(256, LG_ADJROWS_MINB) fk_adj_rows(FGeo g, cons
 #pragma unroll
       for (int e = 0; e < E; ++e) wv[e] = w[e * TPR];
     }
-    if (!FROM_E) fftr<float, L, +1>(v, G.sm, g.twnx, G.t, G.sync);
+    if (!FROM_E) fftr_sp<float, L, +1, SPF ? kSpIn : 0>(v, G.sm, g.twnx, G.t, G.sync);
     if (!UNIFORM) {
 #pragma unroll
       for (int e = 0; e < E; ++e) v[e] = scale(v[e], wv[e]);
     }
-    fftr<float, L, -1>(v, G.sm, g.twnx, G.t, G.sync);
+    fftr_sp<float, L, -1, SPF ? kSpOut : 0>(v, G.sm, g.twnx, G.t, G.sync);
     // stage the band outputs as tile[slot][row] (odd stride: conflict free),
     // then write U[fk][slot][r0 .. r0+groups) as contiguous row segments
     if constexpr (CB) {
@@ -913,7 +921,7 @@ __global__ void __launch_bounds__(256) fk_mask_cols(FGeo g, const C32* __restric
 // shared memory so T rows are written as contiguous segments.
 // grid (ceil(Bx/groups), F*K, tiles)
 // ===========================================================================
-template <int L, bool CB>
+template <int L, bool CB, bool SPF = false>
 __global__ void __launch_bounds__(512) fk_socs_cols(FGeo g, const C32* __restrict__ Mhat,
                                                     long long mh_ts, const C32* __restrict__ H,
                                                     C32* __restrict__ T, long long t_ts) {
@@ -944,7 +952,7 @@ __global__ void __launch_bounds__(512) fk_socs_cols(FGeo g, const C32* __restric
       v[e] = jy >= 0 ? mul(mh[jy], ldg_cx(h + jy)) : mk(0.f, 0.f);
     }
   }
-  fftr<float, L, +1>(v, G.sm, g.twny, G.t, G.sync);
+  fftr_sp<float, L, +1, SPF ? kSpIn : 0>(v, G.sm, g.twny, G.t, G.sync);
   extern __shared__ __align__(16) unsigned char fsm_raw[];
   C32* tile = reinterpret_cast<C32*>(fsm_raw) + G.groups * rsm_len<L>();
   const int ld = G.groups | 1;
@@ -1141,7 +1149,7 @@ __global__ void __launch_bounds__(256) fk_band_col2(FGeo g, const C32* __restric
 //   Accp[fk/KG][cx][qy]   (fk_grad_cols sums the F*K/KG partials, fixed order)
 // grid (Bx, F*K/KG, tiles)
 // ===========================================================================
-template <int L, bool CB>
+template <int L, bool CB, bool SPF = false>
 __global__ void __launch_bounds__(256) fk_adj_cols(FGeo g, const C32* __restrict__ U,
                                                    long long u_ts, const C32* __restrict__ H,
                                                    const float* __restrict__ wk, float dose,
@@ -1156,7 +1164,7 @@ __global__ void __launch_bounds__(256) fk_adj_cols(FGeo g, const C32* __restrict
   C32 v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) v[e] = on ? src[G.idx(e)] : mk(0.f, 0.f);
-  if (on) fftr<float, L, -1>(v, G.sm, g.twny, G.t, G.sync);
+  if (on) fftr_sp<float, L, -1, SPF ? kSpOut : 0>(v, G.sm, g.twny, G.t, G.sync);
   const float w = on ? wk[fk] * dose * sc : 0.f;
   const C32* h = H + (size_t(fk) * Bx + cx) * By;  // column-major [fk][cx][jy]
   G.sync();
