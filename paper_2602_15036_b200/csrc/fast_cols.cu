@@ -10,8 +10,13 @@ void fl_mask_cols(const FGeo& g, cudaStream_t s, int tiles, const C32* Mr, long 
   with_len(g.ay.N, [&](auto c) {
     constexpr int L = decltype(c)::value;
     const int gr = spread_groups<L>((long long)tiles * (g.ax.Pm + 1));
-    flaunch<L>(fk_mask_cols<L>, dim3(cdivi(g.ax.Pm + 1, gr), 1, tiles), gr, s, g, Mr, mr_ts, Mhat,
-                mh_ts);
+    auto go = [&](auto kern) {
+      flaunch<L>(kern, dim3(cdivi(g.ax.Pm + 1, gr), 1, tiles), gr, s, g, Mr, mr_ts, Mhat, mh_ts);
+    };
+    if (!sparse_off() && band_fits_sp_out<L>(g.ay.lo, g.ay.hi))
+      go(fk_mask_cols<L, true>);
+    else
+      go(fk_mask_cols<L, false>);
   });
 }
 
@@ -78,8 +83,14 @@ void fl_grad_cols(const FGeo& g, cudaStream_t s, int tiles, const C32* Acc, long
     const int gr = 1;  // one column per CTA: Pm+1 is small, spread it over SMs
     with_len(g.ay.n, [&](auto cn) { nsum /= kgroups<decltype(cn)::value>(g.K); });  // fk_adj_cols partials
     const size_t extra = size_t(gr) * 2 * g.ay.B * sizeof(C32);  // summed band columns
-    flaunch_x<L>(fk_grad_cols<L>, dim3(cdivi(g.ax.Pm + 1, gr) + 1, 1, tiles), gr, extra, s, g, Acc, a_ts, nsum, Gc,
-                g_ts, costp, cp_ts, ncost, cost_out, co_ts);
+    auto go = [&](auto kern) {
+      flaunch_x<L>(kern, dim3(cdivi(g.ax.Pm + 1, gr) + 1, 1, tiles), gr, extra, s, g, Acc, a_ts, nsum, Gc, g_ts, costp,
+                   cp_ts, ncost, cost_out, co_ts);
+    };
+    if (!sparse_off() && band_fits_sp_in<L>(g.ay.lo, g.ay.hi))
+      go(fk_grad_cols<L, true>);
+    else
+      go(fk_grad_cols<L, false>);
   });
 }
 
@@ -107,7 +118,11 @@ bool fl_band_col2(const FGeo& g, cudaStream_t s, int tiles, int nf, bool sub_in,
           pdl_launch(kern, dim3(cdivi(g.ax.P + 1, gr), nf, tiles), dim3(gr * CP::TPR), smem, s, g, in, in_ts,
                      inv, gxh, gyb, outR, outI, o_ts);
         };
-        if (cb)
+        // N -> n (W band): only the intensity band of the length-N FFT is read
+        const bool spo = cb && !sub_in && band_fits_sp_out<LI>(-g.ay.P, g.ay.P);
+        if (spo)
+          go(fk_band_col2<LI, LO, true, true>);
+        else if (cb)
           go(fk_band_col2<LI, LO, true>);
         else
           go(fk_band_col2<LI, LO, false>);

@@ -120,6 +120,16 @@ __host__ __device__ inline bool centered_band(int L, int E, int lo, int hi) {
 // the band [lo, hi] fits the kSpIn / kSpOut slots of the length-L plan
 // (centered): sparse first stage (band input) / pruned last stage (band output)
 template <int L>
+__host__ __device__ inline bool band_fits_sp_in(int lo, int hi) {
+  const int w = sp_in_slots<L>() * RPlan<L>::TPR;
+  return hi < w && -lo < w;
+}
+template <int L>
+__host__ __device__ inline bool band_fits_sp_out(int lo, int hi) {
+  const int w = sp_out_slots<L>() * RPlan<L>::TPR;
+  return hi < w && -lo < w;
+}
+template <int L>
 __host__ __device__ inline bool band_fits_sp(int lo, int hi) {
   constexpr int TPR = RPlan<L>::TPR;
   const int w = (sp_in_slots<L>() < sp_out_slots<L>() ? sp_in_slots<L>() : sp_out_slots<L>()) * TPR;
@@ -879,7 +889,7 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_grad_rows(FGeo g, con
 // mask half-spectrum columns -> kernel band M^ (Hermitian mirror for qx < 0)
 // grid (ceil((Pmx+1)/groups), 1, tiles)
 // ===========================================================================
-template <int L>
+template <int L, bool SPF = false>
 __global__ void __launch_bounds__(256) fk_mask_cols(FGeo g, const C32* __restrict__ Mr,
                                                     long long mr_ts, C32* __restrict__ Mhat,
                                                     long long mh_ts) {
@@ -894,7 +904,7 @@ __global__ void __launch_bounds__(256) fk_mask_cols(FGeo g, const C32* __restric
   C32 v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) v[e] = src[G.idx(e)];
-  fftr<float, L, -1>(v, G.sm, g.twNy, G.t, G.sync);
+  fftr_sp<float, L, -1, SPF ? kSpOut : 0>(v, G.sm, g.twNy, G.t, G.sync);  // band (and mirror) outputs only
   if (!act) return;
   const float inv = 1.0f / (float(g.ax.N) * float(L));
   C32* mh = Mhat + blockIdx.z * mh_ts;  // column-major band [cx][jy]
@@ -1061,7 +1071,7 @@ __device__ __forceinline__ GSync sub_gsync(int nthreads, int id) {
   return s;
 }
 
-template <int LIN, int LOUT, bool CB>
+template <int LIN, int LOUT, bool CB, bool SPF = false>
 __global__ void __launch_bounds__(256) fk_band_col2(FGeo g, const C32* __restrict__ in,
                                                     long long in_ts, float inv,
                                                     const float* __restrict__ gxh,
@@ -1089,7 +1099,7 @@ __global__ void __launch_bounds__(256) fk_band_col2(FGeo g, const C32* __restric
     C32 v[EI];
 #pragma unroll
     for (int e = 0; e < EI; ++e) v[e] = src[t + e * CP::TIN];
-    fftr<float, LIN, -1>(v, sm, LIN == g.ay.N ? g.twNy : g.twny, t, s1);
+    fftr_sp<float, LIN, -1, SPF ? kSpOut : 0>(v, sm, LIN == g.ay.N ? g.twNy : g.twny, t, s1);  // band outputs only
     const float gx = gxh ? gxh[px] : 1.f;
     if constexpr (CB) {  // intensity band |p| <= P = centered band [-P, P]
       const BandMap<LIN> bm(t, -g.ay.P, g.ay.P);
@@ -1223,7 +1233,7 @@ __device__ __forceinline__ void reduce_cost(const double* __restrict__ c, int n,
 // the last CTA reduces this iteration's cost partials (fixed order).
 // grid (ceil((Pmx+1)/groups) + 1, 1, tiles)
 // ===========================================================================
-template <int L>
+template <int L, bool SPF = false>
 __global__ void __launch_bounds__(256) fk_grad_cols(FGeo g, const C32* __restrict__ Acc,
                                                     long long a_ts, int nsum, C32* __restrict__ Gc,
                                                     long long g_ts, const double* __restrict__ costp,
@@ -1294,7 +1304,7 @@ __global__ void __launch_bounds__(256) fk_grad_cols(FGeo g, const C32* __restric
     if (sn >= 0 && jn >= 0) s = add(s, conjg(col[By + jn]));
     v[e] = scale(s, 0.5f);
   }
-  fftr<float, L, +1>(v, G.sm, g.twNy, G.t, G.sync);
+  fftr_sp<float, L, +1, SPF ? kSpIn : 0>(v, G.sm, g.twNy, G.t, G.sync);  // band input
   if (!act) return;
   C32* o = Gc + blockIdx.z * g_ts + size_t(px) * L;  // column-major [px][y]
 #pragma unroll
