@@ -16,6 +16,7 @@ static int spm_of(int P) {
   int m = 0;
   if (P < RPlan<L>::TPR) m |= 1;
   if (P < sp_out_slots<L>() * RPlan<L>::TPR) m |= 2;
+  if (!(m & 1) && P < 2 * RPlan<L>::TPR && RPlan<L>::E >= 4) m |= 4;  // 2-slot gather
   return m;
 }
 
@@ -107,7 +108,9 @@ void fl_resist_rows(const FGeo& g, cudaStream_t s, int tiles, const C32* Rc, lon
     // band inside the first / last register slots: sparse first / last FFT stage
     switch (spm_of<L>(g.ax.P)) {
       case 3: go(fk_resist_rows<L, 3>); break;
+      case 6: go(fk_resist_rows<L, 6>); break;
       case 2: go(fk_resist_rows<L, 2>); break;
+      case 4: go(fk_resist_rows<L, 4>); break;
       default: go(fk_resist_rows<L, 0>); break;
     }
   });
@@ -187,12 +190,15 @@ void fl_grad_rows(const FGeo& g, cudaStream_t s, int tiles, bool ilt, const C32*
     if (ilt) {
       switch (spm) {
         case 3: go(fk_grad_rows<L, true, 3>, extra); break;
+        case 6: go(fk_grad_rows<L, true, 6>, extra); break;
         case 2: go(fk_grad_rows<L, true, 2>, extra); break;
+        case 4: go(fk_grad_rows<L, true, 4>, extra); break;
         default: go(fk_grad_rows<L, true, 0>, extra); break;
       }
     } else {
       // the gradient write path reads every slot of the first transform
-      (spm & 1) ? go(fk_grad_rows<L, false, 1>, 0) : go(fk_grad_rows<L, false, 0>, 0);
+      (spm & 1) ? go(fk_grad_rows<L, false, 1>, 0)
+                : ((spm & 4) ? go(fk_grad_rows<L, false, 4>, 0) : go(fk_grad_rows<L, false, 0>, 0));
     }
   });
 }

@@ -150,31 +150,46 @@ __device__ __forceinline__ int islot(const AxisGeom& a, int i, int L) {
 // e holds indices t + e*TPR, so only e < ceil((P+1)/TPR) can hit [0, P] and
 // only e >= E - ceil(P/TPR) can hit the mirror [L-P, L): the other slots are
 // zero by a warp-uniform test, without per-element divergent branches.
-template <int L, bool SPB = false>
+template <int L, int NSL = 0>
 __device__ __forceinline__ void load_herm_pair(C32 (&v)[RPlan<L>::E], const FGroup<L>& g,
                                                const C32* a, const C32* b, int P, int ld) {
   constexpr int E = RPlan<L>::E, TPR = RPlan<L>::TPR;
-  if constexpr (SPB) {
-    // band P < TPR: only slot 0 (i = t <= P) and slot E-1 (mirror m = TPR - t
-    // <= P) can be nonzero
-    const int t = g.t, m = TPR - t;
-    C32 A = mk(0.f, 0.f), Bv = mk(0.f, 0.f), Am = mk(0.f, 0.f), Bm = mk(0.f, 0.f);
-    if (t <= P) {
-      A = a[size_t(t) * ld];
-      if (b) Bv = b[size_t(t) * ld];
-      if (t == 0) {
-        A.y = 0.f;
-        Bv.y = 0.f;
-      }
-    }
-    if (m <= P) {
-      Am = conjg(a[size_t(m) * ld]);
-      if (b) Bm = conjg(b[size_t(m) * ld]);
-    }
-    v[0] = mk(A.x - Bv.y, A.y + Bv.x);
+  if constexpr (NSL > 0) {
+    // band P < NSL*TPR: only slots e < NSL (index i = t + e TPR <= P) and
+    // e >= E - NSL (mirror m = L - i <= P) can be nonzero (compile-time zero
+    // elsewhere).  Rows y0, y0+1 of a column-major spectrum are adjacent
+    // (b == a + 1, 16-byte aligned): one 16-byte load per entry.
+    const bool adj = b == a + 1 && (ld % 2) == 0 && (reinterpret_cast<size_t>(a) & 15) == 0;
 #pragma unroll
-    for (int e = 1; e < E - 1; ++e) v[e] = mk(0.f, 0.f);
-    v[E - 1] = mk(Am.x - Bm.y, Am.y + Bm.x);
+    for (int e = 0; e < E; ++e) {
+      C32 A = mk(0.f, 0.f), Bv = mk(0.f, 0.f);
+      if (e < NSL || e >= E - NSL) {
+        const int i = g.idx(e);
+        const bool lo = e < NSL;
+        const int m = (i == 0 ? 0 : L - i);
+        const int src = lo ? i : m;
+        if (src <= P) {
+          if (adj) {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(a + size_t(src) * ld));
+            A = mk(q.x, q.y);
+            Bv = mk(q.z, q.w);
+          } else {
+            A = a[size_t(src) * ld];
+            if (b) Bv = b[size_t(src) * ld];
+          }
+          if (lo) {
+            if (m == i) {
+              A.y = 0.f;
+              Bv.y = 0.f;
+            }
+          } else {
+            A = conjg(A);
+            Bv = conjg(Bv);
+          }
+        }
+      }
+      v[e] = mk(A.x - Bv.y, A.y + Bv.x);
+    }
     return;
   }
   const int nlo = (P + TPR) / TPR, nhi = (P + TPR - 1) / TPR;
@@ -530,6 +545,7 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_resist_rows(FGeo g, c
   // SPM bit 0: band inside slot 0 / E-1 (sparse first stage, 1-slot gather);
   // bit 1: band inside the kSpOut slots (pruned last stage)
   constexpr bool SPB = (SPM & 1) != 0, SPO = (SPM & 2) != 0;
+  constexpr int NSL = SPB ? 1 : ((SPM & 4) ? 2 : 0);  // band slots at each end of the gather
   constexpr int SP_IN = SPB ? kSpIn : 0, SP_OUT = SPO ? kSpOut : 0;
   const int Ny = g.ay.N, Px = g.ax.P, f = blockIdx.y, npairs = (Ny + 1) / 2;
   const int pair0 = blockIdx.x * G.groups + G.gid;
@@ -547,7 +563,7 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_resist_rows(FGeo g, c
   else
     stage_rows_async<L>(tsl, tg + size_t(y0) * L, tg + size_t(has1 ? y1 : y0) * L, G.t);
   C32 v[E];
-  load_herm_pair<L, SPB>(v, G, rc + y0, has1 ? rc + y1 : nullptr, Px, Ny);  // column-major [px][y]
+  load_herm_pair<L, NSL>(v, G, rc + y0, has1 ? rc + y1 : nullptr, Px, Ny);  // column-major [px][y]
   fftr_sp<float, L, +1, SP_IN>(v, G.sm, g.twNx, G.t, G.sync);
   if (LG_TMA_STAGE) {
     stage_wait_tma(&stage_bar[G.gid]);
@@ -806,6 +822,7 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_grad_rows(FGeo g, con
   // SPM bit 0: band inside slot 0 / E-1 (sparse first stage, 1-slot gather);
   // bit 1: band inside the kSpOut slots (pruned last stage)
   constexpr bool SPB = (SPM & 1) != 0, SPO = (SPM & 2) != 0;
+  constexpr int NSL = SPB ? 1 : ((SPM & 4) ? 2 : 0);  // band slots at each end of the gather
   constexpr int SP_IN = SPB ? kSpIn : 0, SP_OUT = SPO ? kSpOut : 0;
   const int Ny = g.ay.N, Pm = g.ax.Pm, npairs = (Ny + 1) / 2;
   const int pair0 = blockIdx.x * G.groups + G.gid;
@@ -825,7 +842,7 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_grad_rows(FGeo g, con
       stage_rows_async<L>(tsl, th + size_t(y0) * L, th + size_t(has1 ? y1 : y0) * L, G.t);
   }
   C32 v[E];
-  load_herm_pair<L, SPB>(v, G, gc + y0, has1 ? gc + y1 : nullptr, Pm, Ny);  // column-major [px][y]
+  load_herm_pair<L, NSL>(v, G, gc + y0, has1 ? gc + y1 : nullptr, Pm, Ny);  // column-major [px][y]
   fftr_sp<float, L, +1, SP_IN>(v, G.sm, g.twNx, G.t, G.sync);
   if (ILT) {
     if (LG_TMA_STAGE) {
