@@ -193,21 +193,32 @@ __device__ __forceinline__ void load_herm_pair(C32 (&v)[RPlan<L>::E], const FGro
     return;
   }
   const int nlo = (P + TPR) / TPR, nhi = (P + TPR - 1) / TPR;
+  const bool adj = b == a + 1 && (ld % 2) == 0 && (reinterpret_cast<size_t>(a) & 15) == 0;
+  auto ld2 = [&](int src, C32& A, C32& Bv) {
+    if (adj) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(a + size_t(src) * ld));
+      A = mk(q.x, q.y);
+      Bv = mk(q.z, q.w);
+    } else {
+      A = a[size_t(src) * ld];
+      if (b) Bv = b[size_t(src) * ld];
+    }
+  };
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int i = g.idx(e);
     const int m = (i == 0 ? 0 : L - i);
     C32 A = mk(0.f, 0.f), Bv = mk(0.f, 0.f);
     if (e < nlo && i <= P) {
-      A = a[size_t(i) * ld];
-      if (b) Bv = b[size_t(i) * ld];
+      ld2(i, A, Bv);
       if (m == i) {
         A.y = 0.f;
         Bv.y = 0.f;
       }
     } else if (e >= E - nhi && m <= P) {
-      A = conjg(a[size_t(m) * ld]);
-      if (b) Bv = conjg(b[size_t(m) * ld]);
+      ld2(m, A, Bv);
+      A = conjg(A);
+      Bv = conjg(Bv);
     }
     v[e] = mk(A.x - Bv.y, A.y + Bv.x);
   }
