@@ -682,6 +682,10 @@ __global__ void __launch_bounds__(256) fk_wlp_rows(FGeo g, const C32* __restrict
 // ===========================================================================
 // TMA-prefetched E rows in adj_rows: measured neutral-to-slower at C5 / C4 / C2
 // (+0.2-0.6 %), so off by default (A/B switch)
+// L2 prefetch of the next slot's E row in adj_rows (A/B switch)
+#ifndef LG_ADJ_L2PF
+#define LG_ADJ_L2PF 1
+#endif
 #ifndef LG_ADJ_TMA
 #define LG_ADJ_TMA 0
 #endif
@@ -759,6 +763,15 @@ __global__ void __launch_bounds__(256, LG_ADJROWS_MINB) fk_adj_rows(FGeo g, cons
       const C32* src = erow(fk) + G.t;
 #pragma unroll
       for (int e = 0; e < E; ++e) v[e] = src[e * TPR];
+#if LG_ADJ_L2PF
+      // pull the next active slot's E row (from HBM) into L2 while this slot
+      // transforms: one 128-byte line per lane
+      if (nxt >= 0) {
+        constexpr int LINES = (L * int(sizeof(C32)) + 127) / 128;
+        const char* nrow = reinterpret_cast<const char*>(erow(nxt));
+        for (int ln = G.t; ln < LINES; ln += TPR) asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + ln * 128));
+      }
+#endif
     } else if (CB) {
       const C32* sb = T + blockIdx.z * t_ts + size_t(fk) * ny * g.tld + size_t(sy) * g.tld + bm.base;
 #pragma unroll
