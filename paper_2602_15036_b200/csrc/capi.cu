@@ -598,6 +598,12 @@ Launch launch_cfg(int LA, int LB, int target = 256) {
   l.RPC = std::max(1, target / l.G);
   l.block = l.RPC * l.G;
   l.smem = size_t(l.RPC) * lg::group_elems<T>(LA, LB) * sizeof(T);
+  // one row group must fit a CTA's shared memory (227 KB on sm_100); very long
+  // Bluestein lengths in fp64 do not
+  if (l.smem > 227u * 1024u)
+    throw std::runtime_error("transform length " + std::to_string(std::max(LA, LB)) + " needs " +
+                             std::to_string(l.smem / 1024) + " KB of shared memory per row group (" +
+                             (sizeof(T) == 8 ? "fp64" : "fp32") + " generic path; limit 227 KB)");
   return l;
 }
 
