@@ -237,11 +237,12 @@ __device__ __forceinline__ int rpad(int i) { return i + (i >> 4); }
 // Barrier of one row group: warp-level when the group fits a warp, else a
 // named barrier per group (id 1 + gid, <= 15 groups) or the CTA barrier.
 struct GSync {
-  int id;  // 0: __syncwarp; >0: bar.sync id; <0: __syncthreads
+  int id;  // 0: __syncwarp(mask); >0: bar.sync id; <0: __syncthreads
   int n;
+  unsigned mask = 0xffffffffu;  // id 0: the group's own lanes only
   __device__ __forceinline__ void operator()() const {
     if (id == 0)
-      __syncwarp();
+      __syncwarp(mask);
     else if (id > 0)
       asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
     else
@@ -249,17 +250,22 @@ struct GSync {
   }
 };
 
+// Groups narrower than a warp synchronise only their own lanes: groups that
+// share a warp run independent work (different kernel slots, some of them
+// empty), so a full-warp barrier would couple them.
 template <int L>
 __device__ __forceinline__ GSync make_gsync(int gid, int groups) {
   constexpr int TPR = RPlan<L>::TPR;
   GSync s;
   s.n = TPR;
-  if (TPR <= 32 && (32 % TPR) == 0)
+  if (TPR <= 32 && (32 % TPR) == 0) {
     s.id = 0;
-  else if (groups <= 15 && TPR % 32 == 0)
+    s.mask = TPR == 32 ? 0xffffffffu : (((1u << TPR) - 1u) << ((gid * TPR) & 31));
+  } else if (groups <= 15 && TPR % 32 == 0) {
     s.id = 1 + gid;
-  else
+  } else {
     s.id = -1;
+  }
   return s;
 }
 

@@ -489,7 +489,10 @@ __global__ void __launch_bounds__(256, LG_SOCSROWS_MINB) fk_socs_rows(FGeo g, co
     return K;
   };
   const C32* trow0 = T + blockIdx.z * t_ts + size_t(f * K) * tstep + size_t(sy) * tld;
-  if constexpr (CB) {
+  // the TMA buffer only for whole-warp groups (the 384 / 768 plans); narrower
+  // groups (short test transforms) gather straight from global memory
+  constexpr bool TMA_T = CB && RPlan<L>::TPR >= 32;
+  if constexpr (TMA_T) {
     if (G.t == 0) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tbar[G.gid][0])) : "memory");
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tbar[G.gid][1])) : "memory");
@@ -509,6 +512,7 @@ __global__ void __launch_bounds__(256, LG_SOCSROWS_MINB) fk_socs_rows(FGeo g, co
   } else {
     for (int k = next_k(G.gid); k < K; k = next_k(k + G.groups)) slot(k, trow0 + size_t(k) * tstep);
   }
+  (void)rbytes;
   G.sync();  // exchange buffer free: publish the group's partial row
   float* red = reinterpret_cast<float*>(G.sm);
 #pragma unroll
