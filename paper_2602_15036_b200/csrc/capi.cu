@@ -1011,6 +1011,7 @@ struct Plan : PlanBase {
     std::fclose(f);
   }
 
+  int zflip = 0;
   template <typename Fn>
   void fl(const char* name, Fn&& fn) {
     // LITHOGPU_ABLATE=name[,name..]: skip those launches (timing ablation
@@ -1027,6 +1028,9 @@ struct Plan : PlanBase {
     } else {
       fg.trace = nullptr;
     }
+    // alternate the tile order launch by launch (LITHOGPU_NO_ZREV=1: off)
+    static const bool zrev_off = std::getenv("LITHOGPU_NO_ZREV") != nullptr;
+    fg.zrev = zrev_off ? 0 : (zflip ^= 1);
     ctx->prof_begin(name);
     fn();
     ctx->prof_end();

@@ -28,6 +28,13 @@ __device__ __forceinline__ void pdl_entry() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
+// Tile index of this CTA: launches alternate the tile order (FGeo::zrev, set
+// per launch by the host) so each kernel starts on the tiles its predecessor
+// finished last, whose outputs are still in L2.
+__device__ __forceinline__ unsigned tz(const FGeo& g) {
+  return g.zrev ? gridDim.z - 1u - blockIdx.z : blockIdx.z;
+}
+
 // ---- launch trace (diagnostic; FGeo::trace) ----
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -369,7 +376,7 @@ __global__ void __launch_bounds__(256) fk_real_rows_fwd(FGeo g, const float* __r
   const int pair = act ? pair0 : npairs - 1;
   const int y0 = 2 * pair, y1 = y0 + 1;
   const bool has1 = y1 < Ny;
-  const float* s = src + blockIdx.z * src_ts;
+  const float* s = src + tz(g) * src_ts;
   C32 v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) {
@@ -392,7 +399,7 @@ __global__ void __launch_bounds__(256) fk_real_rows_fwd(FGeo g, const float* __r
   else
     to_smem<float, L>(v, G.sm, G.t);
   G.sync();
-  store_pair_cols<L>(G, groups_bytes<L>(G.groups), out + blockIdx.z * out_ts, Ny,
+  store_pair_cols<L>(G, groups_bytes<L>(G.groups), out + tz(g) * out_ts, Ny,
                      2 * blockIdx.x * G.groups, Ny, Pout);
 }
 
@@ -465,7 +472,7 @@ __global__ void __launch_bounds__(256, LG_SOCSROWS_MINB) fk_socs_rows(FGeo g, co
     }
     fftr_sp<float, L, +1, SPF ? kSpIn : 0>(v, G.sm, g.twnx, G.t, G.sync);
     if (Eo) {  // keep the coherent field for the adjoint (fk_adj_rows<.., FROM_E>)
-      C32* eo = Eo + blockIdx.z * e_ts + (size_t(fk) * ny + sy) * L + G.t;
+      C32* eo = Eo + tz(g) * e_ts + (size_t(fk) * ny + sy) * L + G.t;
 #pragma unroll
       for (int e = 0; e < E; ++e) eo[e * RPlan<L>::TPR] = v[e];
     }
@@ -488,7 +495,7 @@ __global__ void __launch_bounds__(256, LG_SOCSROWS_MINB) fk_socs_rows(FGeo g, co
       if (!g.slot_on || g.slot_on[f * K + k]) return k;
     return K;
   };
-  const C32* trow0 = T + blockIdx.z * t_ts + size_t(f * K) * tstep + size_t(sy) * tld;
+  const C32* trow0 = T + tz(g) * t_ts + size_t(f * K) * tstep + size_t(sy) * tld;
   // the TMA buffer only for whole-warp groups (the 384 / 768 plans); narrower
   // groups (short test transforms) gather straight from global memory
   constexpr bool TMA_T = CB && RPlan<L>::TPR >= 32;
@@ -533,7 +540,7 @@ __global__ void __launch_bounds__(256, LG_SOCSROWS_MINB) fk_socs_rows(FGeo g, co
   }
   G.sync();  // every partial read before this group reuses its buffer
   fftr<float, L, -1>(v, G.sm, g.twnx, G.t, G.sync);
-  C32* o = Ir + blockIdx.z * ir_ts + size_t(f) * (g.ax.P + 1) * ny + sy;
+  C32* o = Ir + tz(g) * ir_ts + size_t(f) * (g.ax.P + 1) * ny + sy;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int px = G.idx(e);
@@ -568,9 +575,9 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_resist_rows(FGeo g, c
   const int pair = act ? pair0 : npairs - 1;
   const int y0 = 2 * pair, y1 = y0 + 1;
   const bool has1 = y1 < Ny;
-  const C32* rc = Rc + blockIdx.z * c_ts + size_t(f) * Ny * (Px + 1);
+  const C32* rc = Rc + tz(g) * c_ts + size_t(f) * Ny * (Px + 1);
   // target rows staged into shared memory behind the transform
-  const float* tg = target + blockIdx.z * tg_ts;
+  const float* tg = target + tz(g) * tg_ts;
   float* tsl = row_slab<L>(G.groups, G.gid);
   __shared__ unsigned long long stage_bar[16];
   if (LG_TMA_STAGE)
@@ -602,7 +609,7 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_resist_rows(FGeo g, c
   }
   float c = warp_sum((c0 + h1 * c1) * w, TPR < 32 ? TPR : 32);
   if (act && (G.t & 31) == 0)
-    costp[blockIdx.z * cp_ts + (size_t(f) * npairs + pair) * WPG + (G.t >> 5)] = double(c);
+    costp[tz(g) * cp_ts + (size_t(f) * npairs + pair) * WPG + (G.t >> 5)] = double(c);
   fftr_sp<float, L, -1, SP_OUT>(v, G.sm, g.twNx, G.t, G.sync);
   G.sync();
   if constexpr (SPO)
@@ -611,7 +618,7 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_resist_rows(FGeo g, c
     to_smem<float, L>(v, G.sm, G.t);
   G.sync();
   store_pair_cols<L>(G, groups_bytes<L>(G.groups) + row_slab_bytes<L>(G.groups),
-                     Dr + blockIdx.z * d_ts + size_t(f) * (Px + 1) * Ny, Ny, 2 * blockIdx.x * G.groups, Ny, Px);
+                     Dr + tz(g) * d_ts + size_t(f) * (Px + 1) * Ny, Ny, 2 * blockIdx.x * G.groups, Ny, Px);
 }
 
 // ===========================================================================
@@ -631,12 +638,12 @@ __global__ void __launch_bounds__(256) fk_out_rows(FGeo g, const C32* __restrict
   const int y0 = blockIdx.x * G.groups + G.gid;
   const bool act = y0 < Ny;
   const int y = act ? y0 : Ny - 1;
-  const size_t cb = blockIdx.z * c_ts + size_t(f) * Ny * (Px + 1) + y;  // column-major [f][px][y]
+  const size_t cb = tz(g) * c_ts + size_t(f) * Ny * (Px + 1) + y;  // column-major [f][px][y]
   C32 v[E];
   load_herm_pair<L>(v, G, Ic ? Ic + cb : Rc + cb, (Ic && Rc) ? Rc + cb : nullptr, Px, Ny);
   fftr<float, L, +1>(v, G.sm, g.twNx, G.t, G.sync);
   if (!act) return;
-  const size_t ob = blockIdx.z * o_ts + (size_t(f) * Ny + y) * L;
+  const size_t ob = tz(g) * o_ts + (size_t(f) * Ny + y) * L;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int i = G.idx(e);
@@ -665,12 +672,12 @@ __global__ void __launch_bounds__(256) fk_wlp_rows(FGeo g, const C32* __restrict
   const int pair = act ? pair0 : npairs - 1;
   const int y0 = 2 * pair, y1 = y0 + 1;
   const bool has1 = y1 < ny;
-  const C32* wc = Wc + blockIdx.z * w_ts + size_t(f) * ny * (Px + 1);
+  const C32* wc = Wc + tz(g) * w_ts + size_t(f) * ny * (Px + 1);
   C32 v[E];
   load_herm_pair<L>(v, G, wc + y0, has1 ? wc + y1 : nullptr, Px, ny);  // column-major [px][sy]
   fftr<float, L, +1>(v, G.sm, g.twnx, G.t, G.sync);
   if (!act) return;
-  float* o = Wsub + blockIdx.z * ws_ts + size_t(f) * ny * L;
+  float* o = Wsub + tz(g) * ws_ts + size_t(f) * ny * L;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int i = G.idx(e);
@@ -732,7 +739,7 @@ __global__ void __launch_bounds__(256, LG_ADJROWS_MINB) fk_adj_rows(FGeo g, cons
   const size_t tile_bytes = (size_t(Bx) * ld * sizeof(C32) + 15) & ~size_t(15);
   C32* eb = reinterpret_cast<C32*>(fsm_raw + groups_bytes<L>(G.groups) + tile_bytes) + size_t(G.gid) * L;
   __shared__ unsigned long long ebar[16];
-  auto erow = [&](int fk) { return T + blockIdx.z * t_ts + (size_t(fk) * ny + sy) * L; };
+  auto erow = [&](int fk) { return T + tz(g) * t_ts + (size_t(fk) * ny + sy) * L; };
   auto prefetch = [&](int fk) {
     if (G.t == 0) {
       const unsigned bar = smem_u32(&ebar[G.gid]);
@@ -777,11 +784,11 @@ __global__ void __launch_bounds__(256, LG_ADJROWS_MINB) fk_adj_rows(FGeo g, cons
       }
 #endif
     } else if (CB) {
-      const C32* sb = T + blockIdx.z * t_ts + size_t(fk) * ny * g.tld + size_t(sy) * g.tld + bm.base;
+      const C32* sb = T + tz(g) * t_ts + size_t(fk) * ny * g.tld + size_t(sy) * g.tld + bm.base;
 #pragma unroll
       for (int e = 0; e < E; ++e) v[e] = bm.has(e) ? sb[BandMap<L>::off(e)] : mk(0.f, 0.f);
     } else {
-      const C32* src = T + blockIdx.z * t_ts + size_t(fk) * ny * g.tld + size_t(sy) * g.tld;
+      const C32* src = T + tz(g) * t_ts + size_t(fk) * ny * g.tld + size_t(sy) * g.tld;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const int sl = kslot(G.idx(e), lo, hi, L);
@@ -790,7 +797,7 @@ __global__ void __launch_bounds__(256, LG_ADJROWS_MINB) fk_adj_rows(FGeo g, cons
     }
     float wv[E];
     if (!UNIFORM) {
-      const float* w = Wsub + blockIdx.z * ws_ts + (size_t(f) * ny + sy) * L + G.t;
+      const float* w = Wsub + tz(g) * ws_ts + (size_t(f) * ny + sy) * L + G.t;
 #pragma unroll
       for (int e = 0; e < E; ++e) wv[e] = w[e * TPR];
     }
@@ -819,7 +826,7 @@ __global__ void __launch_bounds__(256, LG_ADJROWS_MINB) fk_adj_rows(FGeo g, cons
       const int rr = threadIdx.x & (G.groups - 1), step = blockDim.x >> lgg;
       if (rr < nr) {
         int sl = threadIdx.x >> lgg;
-        C32* op = U + blockIdx.z * u_ts + size_t(fk) * Bx * ny + r0 + size_t(sl) * ny + rr;
+        C32* op = U + tz(g) * u_ts + size_t(fk) * Bx * ny + r0 + size_t(sl) * ny + rr;
         const C32* tp = tile + sl * ld + rr;
         const size_t ostep = size_t(step) * ny;
         const int tstep = step * ld;
@@ -858,8 +865,8 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_grad_rows(FGeo g, con
   const int pair = act ? pair0 : npairs - 1;
   const int y0 = 2 * pair, y1 = y0 + 1;
   const bool has1 = y1 < Ny;
-  const C32* gc = Gc + blockIdx.z * g_ts;
-  float* th = theta + blockIdx.z * th_ts;
+  const C32* gc = Gc + tz(g) * g_ts;
+  float* th = theta + tz(g) * th_ts;
   float* tsl = nullptr;  // theta rows staged into shared memory behind the transform
   __shared__ unsigned long long stage_bar[16];
   if (ILT) {
@@ -882,7 +889,7 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_grad_rows(FGeo g, con
   }
   if (!ILT) {
     if (!act) return;
-    float* o = grad + blockIdx.z * gr_ts;
+    float* o = grad + tz(g) * gr_ts;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const int i = G.idx(e);
@@ -896,8 +903,8 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_grad_rows(FGeo g, con
   float gm = 0.f;
   float* th0 = th + size_t(y0) * L;
   float* th1 = th + size_t(has1 ? y1 : y0) * L;
-  float* gr0 = grad ? grad + blockIdx.z * gr_ts + size_t(y0) * L : nullptr;
-  float* gr1 = grad ? grad + blockIdx.z * gr_ts + size_t(has1 ? y1 : y0) * L : nullptr;
+  float* gr0 = grad ? grad + tz(g) * gr_ts + size_t(y0) * L : nullptr;
+  float* gr1 = grad ? grad + tz(g) * gr_ts + size_t(has1 ? y1 : y0) * L : nullptr;
   const bool w1 = act && has1;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
@@ -918,7 +925,7 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_grad_rows(FGeo g, con
     v[e] = mk(fsig(steep * n0), has1 ? fsig(steep * n1) : 0.f);
   }
   gm = warp_max(gm, TPR < 32 ? TPR : 32);
-  if (act && gmaxp && (G.t & 31) == 0) gmaxp[blockIdx.z * gm_ts + size_t(pair) * WPG + (G.t >> 5)] = gm;
+  if (act && gmaxp && (G.t & 31) == 0) gmaxp[tz(g) * gm_ts + size_t(pair) * WPG + (G.t >> 5)] = gm;
   fftr_sp<float, L, -1, SP_OUT>(v, G.sm, g.twNx, G.t, G.sync);
   G.sync();
   if constexpr (SPO)
@@ -926,7 +933,7 @@ __global__ void __launch_bounds__(256, LG_FULLROW_MINB) fk_grad_rows(FGeo g, con
   else
     to_smem<float, L>(v, G.sm, G.t);
   G.sync();
-  store_pair_cols<L>(G, groups_bytes<L>(G.groups) + row_slab_bytes<L>(G.groups), Mr + blockIdx.z * mr_ts, Ny,
+  store_pair_cols<L>(G, groups_bytes<L>(G.groups) + row_slab_bytes<L>(G.groups), Mr + tz(g) * mr_ts, Ny,
                      2 * blockIdx.x * G.groups, Ny, Pm);
 }
 
@@ -945,14 +952,14 @@ __global__ void __launch_bounds__(256) fk_mask_cols(FGeo g, const C32* __restric
   const int px0 = blockIdx.x * G.groups + G.gid;
   const bool act = px0 <= Pm;
   const int px = act ? px0 : Pm;
-  const C32* src = Mr + blockIdx.z * mr_ts + size_t(px) * L;
+  const C32* src = Mr + tz(g) * mr_ts + size_t(px) * L;
   C32 v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) v[e] = src[G.idx(e)];
   fftr_sp<float, L, -1, SPF ? kSpOut : 0>(v, G.sm, g.twNy, G.t, G.sync);  // band (and mirror) outputs only
   if (!act) return;
   const float inv = 1.0f / (float(g.ax.N) * float(L));
-  C32* mh = Mhat + blockIdx.z * mh_ts;  // column-major band [cx][jy]
+  C32* mh = Mhat + tz(g) * mh_ts;  // column-major band [cx][jy]
   const int By = g.ay.B;
   const int sp = band_slot(g.ax, px);
   const int sn = px > 0 ? band_slot(g.ax, -px) : -1;
@@ -990,7 +997,7 @@ __global__ void __launch_bounds__(512) fk_socs_cols(FGeo g, const C32* __restric
   const bool act = cx0 < Bx;
   const int cx_ = act ? cx0 : Bx - 1;
   // M^ and H are column-major [cx][jy]: each group reads contiguous columns
-  const C32* mh = Mhat + blockIdx.z * mh_ts + size_t(cx_) * By;
+  const C32* mh = Mhat + tz(g) * mh_ts + size_t(cx_) * By;
   const C32* h = H + (size_t(fk) * Bx + cx_) * By;
   C32 v[E];
   if constexpr (CB) {
@@ -1020,7 +1027,7 @@ __global__ void __launch_bounds__(512) fk_socs_cols(FGeo g, const C32* __restric
   const int cc = threadIdx.x & (G.groups - 1), step = blockDim.x >> lgg;
   if (cc >= nc) return;
   int sy = threadIdx.x >> lgg;
-  C32* op = T + blockIdx.z * t_ts + size_t(fk) * L * g.tld + c0 + size_t(sy) * g.tld + cc;
+  C32* op = T + tz(g) * t_ts + size_t(fk) * L * g.tld + c0 + size_t(sy) * g.tld + cc;
   const C32* tp = tile + sy * ld + cc;
   const size_t ostep = size_t(step) * g.tld;
   const int tstep = step * ld;
@@ -1046,14 +1053,14 @@ __global__ void __launch_bounds__(256) fk_band_colfwd(FGeo g, const C32* __restr
   const int px0 = blockIdx.x * G.groups + G.gid;
   const bool act = px0 <= Px;
   const int px = act ? px0 : Px;
-  const C32* src = in + blockIdx.z * in_ts + (size_t(f) * (Px + 1) + px) * L;
+  const C32* src = in + tz(g) * in_ts + (size_t(f) * (Px + 1) + px) * L;
   C32 v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) v[e] = src[G.idx(e)];
   fftr<float, L, -1>(v, G.sm, L == g.ay.N ? g.twNy : g.twny, G.t, G.sync);
   if (!act) return;
   const float gx = gxh ? gxh[px] : 1.f;
-  const size_t ob = blockIdx.z * o_ts + size_t(f) * nb2 * (Px + 1);
+  const size_t ob = tz(g) * o_ts + size_t(f) * nb2 * (Px + 1);
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int j = islot(g.ay, G.idx(e), L);
@@ -1079,7 +1086,7 @@ __global__ void __launch_bounds__(256) fk_band_colinv(FGeo g, const C32* __restr
   const int px0 = blockIdx.x * G.groups + G.gid;
   const bool act = px0 <= Px;
   const int px = act ? px0 : Px;
-  const C32* b = band + blockIdx.z * b_ts + size_t(f) * nb2 * (Px + 1);
+  const C32* b = band + tz(g) * b_ts + size_t(f) * nb2 * (Px + 1);
   C32 v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) {
@@ -1088,7 +1095,7 @@ __global__ void __launch_bounds__(256) fk_band_colinv(FGeo g, const C32* __restr
   }
   fftr<float, L, +1>(v, G.sm, L == g.ay.N ? g.twNy : g.twny, G.t, G.sync);
   if (!act) return;
-  C32* o = out + blockIdx.z * o_ts + (size_t(f) * (Px + 1) + px) * L;  // column-major [f][px][y]
+  C32* o = out + tz(g) * o_ts + (size_t(f) * (Px + 1) + px) * L;  // column-major [f][px][y]
 #pragma unroll
   for (int e = 0; e < E; ++e) o[G.idx(e)] = v[e];
 }
@@ -1140,7 +1147,7 @@ __global__ void __launch_bounds__(256) fk_band_col2(FGeo g, const C32* __restric
   const int px = act ? px0 : Px;
   if (t < CP::TIN) {
     const GSync s1 = CP::TIN == CP::TPR ? gsync : sub_gsync(CP::TIN, 1 + groups + gid);
-    const C32* src = in + blockIdx.z * in_ts + (size_t(f) * (Px + 1) + px) * LIN;
+    const C32* src = in + tz(g) * in_ts + (size_t(f) * (Px + 1) + px) * LIN;
     C32 v[EI];
 #pragma unroll
     for (int e = 0; e < EI; ++e) v[e] = src[t + e * CP::TIN];
@@ -1170,7 +1177,7 @@ __global__ void __launch_bounds__(256) fk_band_col2(FGeo g, const C32* __restric
   gsync();
   if (t >= CP::TOUT) return;
   const GSync s2 = CP::TOUT == CP::TPR ? gsync : sub_gsync(CP::TOUT, 1 + groups + gid);
-  const size_t ob = blockIdx.z * o_ts + (size_t(f) * (Px + 1) + px) * LOUT;  // column-major [f][px][y]
+  const size_t ob = tz(g) * o_ts + (size_t(f) * (Px + 1) + px) * LOUT;  // column-major [f][px][y]
   for (int pass = 0; pass < 2; ++pass) {
     C32* out = pass == 0 ? outR : outI;
     if (!out) continue;
@@ -1215,7 +1222,7 @@ __global__ void __launch_bounds__(256) fk_adj_cols(FGeo g, const C32* __restrict
   const int Bx = g.ax.B, By = g.ay.B, cx = blockIdx.x, fk = blockIdx.y * G.groups + G.gid;
   const float sc = float(2.0 / (double(g.ax.n) * double(g.ay.n)));  // 2 (N/n)^2 / N^2
   const bool on = !g.slot_on || g.slot_on[fk];  // empty slot contributes 0
-  const C32* src = U + blockIdx.z * u_ts + (size_t(fk) * Bx + cx) * L;
+  const C32* src = U + tz(g) * u_ts + (size_t(fk) * Bx + cx) * L;
   C32 v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) v[e] = on ? src[G.idx(e)] : mk(0.f, 0.f);
@@ -1240,7 +1247,7 @@ __global__ void __launch_bounds__(256) fk_adj_cols(FGeo g, const C32* __restrict
   __syncthreads();
   extern __shared__ __align__(16) unsigned char fsm_raw[];
   const C32* base = reinterpret_cast<const C32*>(fsm_raw);
-  C32* o = Accp + blockIdx.z * a_ts + (size_t(blockIdx.y) * Bx + cx) * By;
+  C32* o = Accp + tz(g) * a_ts + (size_t(blockIdx.y) * Bx + cx) * By;
   for (int jy = threadIdx.x; jy < By; jy += blockDim.x) {
     C32 acc = base[jy];
     for (int gg = 1; gg < G.groups; ++gg) acc = add(acc, base[gg * rsm_len<L>() + jy]);
@@ -1288,7 +1295,7 @@ __global__ void __launch_bounds__(256) fk_grad_cols(FGeo g, const C32* __restric
   TraceScope trace_(g);
   constexpr int E = RPlan<L>::E;
   if (blockIdx.x == gridDim.x - 1) {
-    if (cost_out) reduce_cost(costp + blockIdx.z * cp_ts, ncost, cost_out + blockIdx.z * co_ts);
+    if (cost_out) reduce_cost(costp + tz(g) * cp_ts, ncost, cost_out + tz(g) * co_ts);
     return;
   }
   const int Pm = g.ax.Pm, Bx = g.ax.B;
@@ -1299,7 +1306,7 @@ __global__ void __launch_bounds__(256) fk_grad_cols(FGeo g, const C32* __restric
   // group first sums band columns sp and -px (sn) in fixed order into shared
   // memory with all its threads (short code, loads in flight together), then
   // gathers the Hermitian column from there
-  const C32* a = Acc + blockIdx.z * a_ts;
+  const C32* a = Acc + tz(g) * a_ts;
   const int sp = band_slot(g.ax, px), sn = band_slot(g.ax, -px);
   const int By = g.ay.B;
   const size_t plane = size_t(Bx) * By;
@@ -1351,7 +1358,7 @@ __global__ void __launch_bounds__(256) fk_grad_cols(FGeo g, const C32* __restric
   }
   fftr_sp<float, L, +1, SPF ? kSpIn : 0>(v, G.sm, g.twNy, G.t, G.sync);  // band input
   if (!act) return;
-  C32* o = Gc + blockIdx.z * g_ts + size_t(px) * L;  // column-major [px][y]
+  C32* o = Gc + tz(g) * g_ts + size_t(px) * L;  // column-major [px][y]
 #pragma unroll
   for (int e = 0; e < E; ++e) o[G.idx(e)] = v[e];
 }

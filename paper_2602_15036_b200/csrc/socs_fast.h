@@ -27,6 +27,8 @@ struct FGeo {
   // the band width Bx rounded up to even, so every row is a 16-byte multiple
   // (TMA bulk copies in fk_socs_rows)
   int tld = 0;
+  // reverse the tile order (blockIdx.z) of this launch (see tz() in socs_fast.cuh)
+  int zrev = 0;
   // mixed kernel pairs (Plan::make_pairs): 0 marks an empty kernel slot that
   // every kernel skips; null = all slots active
   const int* slot_on = nullptr;
