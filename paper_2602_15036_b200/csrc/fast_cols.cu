@@ -1,4 +1,5 @@
 // fp32 fast path: column-kernel launchers (see socs_fast.h).
+#include <algorithm>
 #include <cstdlib>
 
 #include "fast_common.cuh"
@@ -65,8 +66,14 @@ void fl_adj_cols(const FGeo& g, cudaStream_t s, int tiles, const C32* U, long lo
   with_len(g.ay.n, [&](auto c) {
     constexpr int L = decltype(c)::value;
     const int kg = kgroups<L>(g.K);  // fl_grad_cols sums F*K/kg partials: keep the two in step
+    // band columns per CTA: keep >= ~8 CTAs per SM, amortise beyond that
+    const long long units = (long long)g.ax.B * (g.F * g.K / kg) * tiles;
+    int cc = int(units / (148 * 8));
+    cc = cc < 1 ? 1 : (cc > 4 ? 4 : cc);
+    if (const char* e = std::getenv("LITHOGPU_ADJCOLS_CC")) cc = std::max(1, std::atoi(e));
     auto go = [&](auto kern) {
-      flaunch<L>(kern, dim3(g.ax.B, g.F * g.K / kg, tiles), kg, s, g, U, u_ts, H, wk, dose, Accp, a_ts);
+      flaunch<L>(kern, dim3(cdivi(g.ax.B, cc), g.F * g.K / kg, tiles), kg, s, g, U, u_ts, H, wk, dose, Accp, a_ts,
+                 cc);
     };
     if (centered_band(L, RPlan<L>::E, g.ay.lo, g.ay.hi) && !sparse_off())
       band_fits_sp<L>(g.ay.lo, g.ay.hi) ? go(fk_adj_cols<L, true, true>) : go(fk_adj_cols<L, true, false>);

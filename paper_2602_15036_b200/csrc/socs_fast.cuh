@@ -1215,43 +1215,54 @@ template <int L, bool CB, bool SPF = false>
 __global__ void __launch_bounds__(256) fk_adj_cols(FGeo g, const C32* __restrict__ U,
                                                    long long u_ts, const C32* __restrict__ H,
                                                    const float* __restrict__ wk, float dose,
-                                                   C32* __restrict__ Accp, long long a_ts) {
+                                                   C32* __restrict__ Accp, long long a_ts, int cc) {
   FGroup<L> G;
   TraceScope trace_(g);
-  constexpr int E = RPlan<L>::E;
-  const int Bx = g.ax.B, By = g.ay.B, cx = blockIdx.x, fk = blockIdx.y * G.groups + G.gid;
+  constexpr int E = RPlan<L>::E, TPR = RPlan<L>::TPR;
+  const int Bx = g.ax.B, By = g.ay.B, fk = blockIdx.y * G.groups + G.gid;
   const float sc = float(2.0 / (double(g.ax.n) * double(g.ay.n)));  // 2 (N/n)^2 / N^2
   const bool on = !g.slot_on || g.slot_on[fk];  // empty slot contributes 0
-  const C32* src = U + tz(g) * u_ts + (size_t(fk) * Bx + cx) * L;
-  C32 v[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) v[e] = on ? src[G.idx(e)] : mk(0.f, 0.f);
-  if (on) fftr_sp<float, L, -1, SPF ? kSpOut : 0>(v, G.sm, g.twny, G.t, G.sync);
   const float w = on ? wk[fk] * dose * sc : 0.f;
-  const C32* h = H + (size_t(fk) * Bx + cx) * By;  // column-major [fk][cx][jy]
-  G.sync();
-  if constexpr (CB) {
-    const BandMap<L> bm(G.t, g.ay.lo, g.ay.hi);
-    const C32* hb = h + bm.base;
-    C32* sb = G.sm + bm.base;
-#pragma unroll
-    for (int e = 0; e < E; ++e)
-      if (bm.has(e)) sb[BandMap<L>::off(e)] = scale(mulc(v[e], ldg_cx(hb + BandMap<L>::off(e))), w);
-  } else {
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int jy = kslot(G.idx(e), g.ay.lo, g.ay.hi, L);
-      if (jy >= 0) G.sm[jy] = scale(mulc(v[e], ldg_cx(h + jy)), w);
-    }
-  }
-  __syncthreads();
   extern __shared__ __align__(16) unsigned char fsm_raw[];
   const C32* base = reinterpret_cast<const C32*>(fsm_raw);
-  C32* o = Accp + tz(g) * a_ts + (size_t(blockIdx.y) * Bx + cx) * By;
-  for (int jy = threadIdx.x; jy < By; jy += blockDim.x) {
-    C32 acc = base[jy];
-    for (int gg = 1; gg < G.groups; ++gg) acc = add(acc, base[gg * rsm_len<L>() + jy]);
-    o[jy] = acc;
+  // cc consecutive band columns per CTA; the next column's U row (HBM, written
+  // by adj_rows) is pulled into L2 while this one transforms
+  const int c0 = blockIdx.x * cc, c1 = min(c0 + cc, Bx);
+  for (int cx = c0; cx < c1; ++cx) {
+    const C32* src = U + tz(g) * u_ts + (size_t(fk) * Bx + cx) * L;
+    C32 v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = on ? src[G.idx(e)] : mk(0.f, 0.f);
+    if (on && cx + 1 < c1) {
+      constexpr int LINES = (L * int(sizeof(C32)) + 127) / 128;
+      const char* nrow = reinterpret_cast<const char*>(src + L);
+      for (int ln = G.t; ln < LINES; ln += TPR) asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + ln * 128));
+    }
+    if (on) fftr_sp<float, L, -1, SPF ? kSpOut : 0>(v, G.sm, g.twny, G.t, G.sync);
+    const C32* h = H + (size_t(fk) * Bx + cx) * By;  // column-major [fk][cx][jy]
+    G.sync();
+    if constexpr (CB) {
+      const BandMap<L> bm(G.t, g.ay.lo, g.ay.hi);
+      const C32* hb = h + bm.base;
+      C32* sb = G.sm + bm.base;
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (bm.has(e)) sb[BandMap<L>::off(e)] = scale(mulc(v[e], ldg_cx(hb + BandMap<L>::off(e))), w);
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int jy = kslot(G.idx(e), g.ay.lo, g.ay.hi, L);
+        if (jy >= 0) G.sm[jy] = scale(mulc(v[e], ldg_cx(h + jy)), w);
+      }
+    }
+    __syncthreads();
+    C32* o = Accp + tz(g) * a_ts + (size_t(blockIdx.y) * Bx + cx) * By;
+    for (int jy = threadIdx.x; jy < By; jy += blockDim.x) {
+      C32 acc = base[jy];
+      for (int gg = 1; gg < G.groups; ++gg) acc = add(acc, base[gg * rsm_len<L>() + jy]);
+      o[jy] = acc;
+    }
+    __syncthreads();  // exchange buffers free for the next column
   }
 }
 
